@@ -1,0 +1,175 @@
+/*
+ * amvm.h — C-ABI of the B200-native AMVM inner loop (libamvm.so).
+ *
+ * The reference (`dmmv`, a pure-Python package) has no FFI: its boundary is
+ * the Python call `dmmv.solve(inst, cfg) -> SolveReport`
+ * (/root/reference/pkg/src/dmmv/controller.py:211) plus the component
+ * functions it is built from.  Every entry point below replaces one of those
+ * Python functions; the Python host mirror (`paper_2508_13437_b200`) binds
+ * them with ctypes exactly as a maintainer of `dmmv` would.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes; no C++ exceptions cross the ABI.
+ *   - Every array pointer is a DEVICE pointer unless the name ends in `_host`.
+ *   - All calls are asynchronous on the caller's `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).
+ *   - The caller owns every buffer, including the workspace sized by
+ *     amvm_workspace_bytes(); the library keeps no pointer after return and
+ *     holds no global mutable state (re-entrant across streams/devices).
+ *   - Status: 0 = OK, negative = error; amvm_strerror() names it.  The
+ *     Python mirror raises ValueError for AMVM_ERR_INVALID (same messages as
+ *     the reference) and RuntimeError otherwise.
+ *   - A is stored COLUMN-major (`At`: column j is the m contiguous doubles at
+ *     At + j*m).  Every hot loop of the path streams columns of A
+ *     (localsearch.py:73,191, core.py:222,242), so that is the layout in HBM.
+ *   - Level indices are int32 (the reference uses np.intp; values < 2^31).
+ */
+#ifndef AMVM_H
+#define AMVM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMVM_ABI_VERSION 1
+
+enum {
+  AMVM_OK = 0,
+  AMVM_ERR_INVALID = -1,     /* bad argument (shape, range, NULL pointer)      */
+  AMVM_ERR_CUDA = -2,        /* a CUDA runtime call failed                     */
+  AMVM_ERR_WORKSPACE = -3,   /* workspace smaller than amvm_workspace_bytes()  */
+  AMVM_ERR_UNSUPPORTED = -4, /* shape outside what this build supports         */
+  AMVM_ERR_NO_DEVICE = -5    /* no sm_100 device / kernel image not loadable   */
+};
+
+/* One problem family sharing A.  count == 1 is the single-instance solve of
+ * controller.py:211; count > 1 is the shared-X batch (PTQ rows of one layer,
+ * PAPER.md:147-158) that the reference drives by looping over Instances.   */
+typedef struct {
+  int64_t m, n, nlev, count;
+  const double *At;     /* n x m, column-major A (see header comment)            */
+  const double *B;      /* count x m targets b                                    */
+  const double *levels; /* count x nlev strictly increasing levels (core.py:26)  */
+} amvm_problem;
+
+/* SolverConfig (controller.py:35-68) + module constants, as plain data.     */
+typedef struct {
+  double alpha;          /* impact decay, operators.py:54                      */
+  double sigma1, sigma2, sigma3, decay;  /* controller.py:44-47                */
+  double accept_tie_tol; /* ACCEPT_TIE_TOL controller.py:32                    */
+  double weight_floor;   /* WEIGHT_FLOOR controller.py:31                      */
+  double time_limit_s;   /* < 0: none (controller.py:236)                      */
+  int32_t r;             /* removal_count(destroy_rate, n), controller.py:206  */
+  int32_t k_eps;         /* FilterConfig.k_eps, localsearch.py:45               */
+  int32_t max_candidates;/* <= 0: no cap (None), localsearch.py:46             */
+  int32_t max_iters;     /* controller.py:40                                   */
+  int32_t l2_tiebreak;   /* accept() tie-break, controller.py:48,179           */
+  int32_t refresh_period;       /* REFRESH_PERIOD core.py:18                   */
+  int32_t one_opt_max_sweeps;   /* ONE_OPT_MAX_SWEEPS localsearch.py:20        */
+  int32_t ls_max_rounds;        /* LOCAL_SEARCH_MAX_ROUNDS localsearch.py:21   */
+  int32_t n_segment;            /* N_SEGMENT controller.py:30                  */
+  int32_t threads;       /* CTA size hint: 0 = auto, else 128/256/512          */
+} amvm_params;
+
+/* numpy PCG64 bit generator state == Generator.bit_generator.state.        */
+typedef struct {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+  uint32_t has_uint32, uinteger;
+} amvm_pcg64;
+
+/* A Solution (core.py:145-180) for each of `count` instances.              */
+typedef struct {
+  int32_t *idx;      /* count x n level indices                              */
+  double *residual;  /* count x m, s = A x - b                               */
+  double *objective; /* count, max |s|                                       */
+  int32_t *updates;  /* count, updates_since_refresh                         */
+} amvm_solution;
+
+/* Per-instance outputs of a solve (SolveReport, controller.py:194-203).    */
+typedef struct {
+  amvm_solution best;       /* best solution found                            */
+  double *initial_objective;/* count                                          */
+  int32_t *iterations;      /* count                                          */
+  int64_t *operator_uses;   /* count x 4, PAIRS order controller.py:23-28     */
+  double *trace_current_t;  /* count x max_iters (may be NULL = no trace)     */
+  double *trace_best_t;     /* count x max_iters                              */
+  uint8_t *trace_pair;      /* count x max_iters, PAIRS slot                  */
+  uint8_t *trace_accepted;  /* count x max_iters                              */
+  int64_t *moves_scored;    /* count x 2: [0] reference-equivalent candidate
+                               moves scored, [1] raw candidates scored
+                               (incl. speculative window work); may be NULL   */
+} amvm_result;
+
+/* ---- whole solve: replaces dmmv.solve (controller.py:211-286) ---------- */
+
+/* Workspace bytes for amvm_solve / the component calls on this problem.    */
+size_t amvm_workspace_bytes(const amvm_problem *prob, const amvm_params *prm);
+
+/* Runs the ALNS loop for every instance, starting from `start` (the
+ * initial_solution of controller.py:134, computed by the host) with
+ * `rng[k]` (seeded state in, final state out).  `start` is not modified.   */
+int amvm_solve(const amvm_problem *prob, const amvm_params *prm,
+               const amvm_solution *start, amvm_pcg64 *rng,
+               amvm_result *res, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- component calls (count == 1; the Solution is updated in place) ---- */
+
+/* one_opt, localsearch.py:59-88 */
+int amvm_one_opt(const amvm_problem *prob, const amvm_params *prm,
+                 amvm_solution *sol, void *ws, size_t ws_bytes, void *stream);
+
+/* local_search, localsearch.py:249-269 */
+int amvm_local_search(const amvm_problem *prob, const amvm_params *prm,
+                      amvm_solution *sol, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* find_candidates, localsearch.py:128-169: writes up to `cap` candidates in
+ * reference order (descending delta, then i, then j) and *count (device
+ * int32) = number written.                                                  */
+int amvm_find_candidates(const amvm_problem *prob, const amvm_params *prm,
+                         const amvm_solution *sol, int32_t *out_i,
+                         int32_t *out_j, double *out_delta, int32_t *count,
+                         int32_t cap, void *ws, size_t ws_bytes, void *stream);
+
+/* best_swap, localsearch.py:211-246: out4 (device double[4]) receives
+ * {i, j, delta, predicted_t}; i = -1 when no swap improves.                 */
+int amvm_best_swap(const amvm_problem *prob, const amvm_params *prm,
+                   const amvm_solution *sol, double *out4, void *ws,
+                   size_t ws_bytes, void *stream);
+
+/* impact_scores, operators.py:54-74: d (device double[n]).                 */
+int amvm_impact_scores(const amvm_problem *prob, const amvm_params *prm,
+                       const amvm_solution *sol, double *d, void *ws,
+                       size_t ws_bytes, void *stream);
+
+/* destroy operators, operators.py:34-39 (kind 0, random) and 77-105
+ * (kind 1, worst-remove).  Writes the ascending `removed` (device int32[r])
+ * and advances `rng`.                                                        */
+int amvm_destroy(const amvm_problem *prob, const amvm_params *prm, int kind,
+                 const amvm_solution *sol, amvm_pcg64 *rng, int32_t *removed,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* repair operators, operators.py:108-117 (kind 0, random; consumes rng) and
+ * 120-138 (kind 1, greedy).  `removed` ascending, `saved_idx` the prior
+ * levels (device int32[r] each).                                             */
+int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int kind,
+                amvm_solution *sol, amvm_pcg64 *rng, const int32_t *removed,
+                const int32_t *saved_idx, int32_t r, void *ws, size_t ws_bytes,
+                void *stream);
+
+/* compute_residual, core.py:183-197, as a device contraction for a batch:
+ * residual[k] = A @ levels[k][idx[k]] - B[k], objective[k] = max|residual|.
+ * (Summation order differs from host BLAS dgemv.)          */
+int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol,
+                          void *stream);
+
+const char *amvm_strerror(int status);
+int amvm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMVM_H */
