@@ -84,8 +84,8 @@ def lib():
     return _lib
 
 
-def _p(a: np.ndarray) -> int:
-    return a.ctypes.data
+def _p(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
 
 
 def make_params(n: int, *, destroy_rate=0.005, alpha=0.3, k_eps=100, max_iters=1000,
@@ -125,7 +125,8 @@ class _Batch:
         self.B = np.ascontiguousarray(np.atleast_2d(B), dtype=np.float64)
         self.L = np.ascontiguousarray(np.atleast_2d(L), dtype=np.float64)
         m, n = self.A.shape
-        self.prob = Problem(m, n, self.L.shape[1], self.B.shape[0], _p(self.A), _p(self.B), _p(self.L))
+        self.prob = Problem(m, n, self.L.shape[1], self.B.shape[0], self.A.ctypes.data,
+                            self.B.ctypes.data, self.L.ctypes.data)
 
 
 def _sol(idx, r, obj, cnt):
@@ -133,7 +134,7 @@ def _sol(idx, r, obj, cnt):
     r = np.ascontiguousarray(np.atleast_2d(r), dtype=np.float64).copy()
     obj = np.ascontiguousarray(np.atleast_1d(obj), dtype=np.float64).copy()
     cnt = np.ascontiguousarray(np.atleast_1d(cnt), dtype=np.int32).copy()
-    return (idx, r, obj, cnt), Sol(_p(idx), _p(r), _p(obj), _p(cnt))
+    return (idx, r, obj, cnt), Sol(idx.ctypes.data, r.ctypes.data, obj.ctypes.data, cnt.ctypes.data)
 
 
 def solve(A, B, levels, idx0, r0, obj0, cnt0, prm: Params, states, threads: int = 1) -> dict:
@@ -157,11 +158,10 @@ def solve(A, B, levels, idx0, r0, obj0, cnt0, prm: Params, states, threads: int 
         "trace_best_t": np.zeros((count, T)), "trace_pair": np.zeros((count, T), np.uint8),
         "trace_accepted": np.zeros((count, T), np.uint8), "moves_scored": np.zeros((count, 2), np.int64),
     }
-    res = Result(Sol(_p(out["best_idx"]), _p(out["best_residual"]), _p(out["best_objective"]),
-                     _p(out["best_updates"])),
-                 _p(out["initial_objective"]), _p(out["iterations"]), _p(out["operator_uses"]),
-                 _p(out["trace_current_t"]), _p(out["trace_best_t"]), _p(out["trace_pair"]),
-                 _p(out["trace_accepted"]), _p(out["moves_scored"]))
+    d = {k: v.ctypes.data for k, v in out.items()}
+    res = Result(Sol(d["best_idx"], d["best_residual"], d["best_objective"], d["best_updates"]),
+                 d["initial_objective"], d["iterations"], d["operator_uses"], d["trace_current_t"],
+                 d["trace_best_t"], d["trace_pair"], d["trace_accepted"], d["moves_scored"])
     rc = lib().orc_solve(C.byref(bt.prob), C.byref(prm), C.byref(start), rngs, C.byref(res), int(threads))
     if rc != 0:
         raise RuntimeError(f"orc_solve failed: {rc}")
