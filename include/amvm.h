@@ -36,6 +36,12 @@ extern "C" {
 
 #define AMVM_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define AMVM_API __attribute__((visibility("default")))
+#else
+#define AMVM_API
+#endif
+
 enum {
   AMVM_OK = 0,
   AMVM_ERR_INVALID = -1,     /* bad argument (shape, range, NULL pointer)      */
@@ -71,7 +77,7 @@ typedef struct {
   int32_t one_opt_max_sweeps;   /* ONE_OPT_MAX_SWEEPS localsearch.py:20        */
   int32_t ls_max_rounds;        /* LOCAL_SEARCH_MAX_ROUNDS localsearch.py:21   */
   int32_t n_segment;            /* N_SEGMENT controller.py:30                  */
-  int32_t threads;       /* CTA size hint: 0 = auto, else 128/256/512          */
+  int32_t threads;       /* CTA size: 0 = auto (this build: 256 only)         */
 } amvm_params;
 
 /* numpy PCG64 bit generator state == Generator.bit_generator.state.        */
@@ -106,56 +112,56 @@ typedef struct {
 /* ---- whole solve: replaces dmmv.solve (controller.py:211-286) ---------- */
 
 /* Workspace bytes for amvm_solve / the component calls on this problem.    */
-size_t amvm_workspace_bytes(const amvm_problem *prob, const amvm_params *prm);
+AMVM_API size_t amvm_workspace_bytes(const amvm_problem *prob, const amvm_params *prm);
 
 /* Runs the ALNS loop for every instance, starting from `start` (the
  * initial_solution of controller.py:134, computed by the host) with
  * `rng[k]` (seeded state in, final state out).  `start` is not modified.   */
-int amvm_solve(const amvm_problem *prob, const amvm_params *prm,
+AMVM_API int amvm_solve(const amvm_problem *prob, const amvm_params *prm,
                const amvm_solution *start, amvm_pcg64 *rng,
                amvm_result *res, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- component calls (count == 1; the Solution is updated in place) ---- */
 
 /* one_opt, localsearch.py:59-88 */
-int amvm_one_opt(const amvm_problem *prob, const amvm_params *prm,
+AMVM_API int amvm_one_opt(const amvm_problem *prob, const amvm_params *prm,
                  amvm_solution *sol, void *ws, size_t ws_bytes, void *stream);
 
 /* local_search, localsearch.py:249-269 */
-int amvm_local_search(const amvm_problem *prob, const amvm_params *prm,
+AMVM_API int amvm_local_search(const amvm_problem *prob, const amvm_params *prm,
                       amvm_solution *sol, void *ws, size_t ws_bytes,
                       void *stream);
 
 /* find_candidates, localsearch.py:128-169: writes up to `cap` candidates in
  * reference order (descending delta, then i, then j) and *count (device
  * int32) = number written.                                                  */
-int amvm_find_candidates(const amvm_problem *prob, const amvm_params *prm,
+AMVM_API int amvm_find_candidates(const amvm_problem *prob, const amvm_params *prm,
                          const amvm_solution *sol, int32_t *out_i,
                          int32_t *out_j, double *out_delta, int32_t *count,
                          int32_t cap, void *ws, size_t ws_bytes, void *stream);
 
 /* best_swap, localsearch.py:211-246: out4 (device double[4]) receives
  * {i, j, delta, predicted_t}; i = -1 when no swap improves.                 */
-int amvm_best_swap(const amvm_problem *prob, const amvm_params *prm,
+AMVM_API int amvm_best_swap(const amvm_problem *prob, const amvm_params *prm,
                    const amvm_solution *sol, double *out4, void *ws,
                    size_t ws_bytes, void *stream);
 
 /* impact_scores, operators.py:54-74: d (device double[n]).                 */
-int amvm_impact_scores(const amvm_problem *prob, const amvm_params *prm,
+AMVM_API int amvm_impact_scores(const amvm_problem *prob, const amvm_params *prm,
                        const amvm_solution *sol, double *d, void *ws,
                        size_t ws_bytes, void *stream);
 
 /* destroy operators, operators.py:34-39 (kind 0, random) and 77-105
  * (kind 1, worst-remove).  Writes the ascending `removed` (device int32[r])
  * and advances `rng`.                                                        */
-int amvm_destroy(const amvm_problem *prob, const amvm_params *prm, int kind,
+AMVM_API int amvm_destroy(const amvm_problem *prob, const amvm_params *prm, int kind,
                  const amvm_solution *sol, amvm_pcg64 *rng, int32_t *removed,
                  void *ws, size_t ws_bytes, void *stream);
 
 /* repair operators, operators.py:108-117 (kind 0, random; consumes rng) and
  * 120-138 (kind 1, greedy).  `removed` ascending, `saved_idx` the prior
  * levels (device int32[r] each).                                             */
-int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int kind,
+AMVM_API int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int kind,
                 amvm_solution *sol, amvm_pcg64 *rng, const int32_t *removed,
                 const int32_t *saved_idx, int32_t r, void *ws, size_t ws_bytes,
                 void *stream);
@@ -163,11 +169,16 @@ int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int kind,
 /* compute_residual, core.py:183-197, as a device contraction for a batch:
  * residual[k] = A @ levels[k][idx[k]] - B[k], objective[k] = max|residual|.
  * (Summation order differs from host BLAS dgemv.)          */
-int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol,
+AMVM_API int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol,
                           void *stream);
 
-const char *amvm_strerror(int status);
-int amvm_abi_version(void);
+/* Waits for `stream`, then returns the device-side status the last call on
+ * this workspace left in its header (AMVM_OK, or e.g. AMVM_ERR_UNSUPPORTED
+ * when a swap-candidate buffer overflowed).                                 */
+AMVM_API int amvm_status(const void *ws, void *stream);
+
+AMVM_API const char *amvm_strerror(int status);
+AMVM_API int amvm_abi_version(void);
 
 #ifdef __cplusplus
 }

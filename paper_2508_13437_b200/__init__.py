@@ -1,0 +1,57 @@
+"""B200-native AMVM inner loop for the Discrete Min-Max Violation problem.
+
+A drop-in for the ``solve()`` path of the reference ``dmmv`` package
+(arXiv 2508.13437): the same problem construction, ``solve()``, seed and
+iteration controls, and the same returned assignment, objective and trace —
+with every ALNS iteration running on the GPU through libamvm.so
+(include/amvm.h).  See DESIGN.md.
+"""
+
+__version__ = "0.1.0"
+
+from .controller import (  # noqa: F401
+    ACCEPT_TIE_TOL,
+    LOCAL_SEARCH_MAX_ROUNDS,
+    N_SEGMENT,
+    ONE_OPT_MAX_SWEEPS,
+    PAIRS,
+    WEIGHT_FLOOR,
+    DestroySet,
+    FilterConfig,
+    ImpactScores,
+    SolveReport,
+    SolverConfig,
+    SwapCandidate,
+    TraceEntry,
+    best_swap,
+    find_candidates,
+    greedy_repair,
+    impact_scores,
+    initial_solution,
+    local_search,
+    one_opt,
+    random_destroy,
+    random_repair,
+    removal_count,
+    solve,
+    worst_remove_destroy,
+)
+from .core import (  # noqa: F401
+    REFRESH_PERIOD,
+    Instance,
+    RowScreen,
+    Solution,
+    ValueSet,
+    compute_residual,
+    round_to_nearest,
+    row_screen,
+    two_nearest,
+)
+
+__all__ = [
+    "__version__", "Instance", "RowScreen", "Solution", "ValueSet", "compute_residual",
+    "round_to_nearest", "row_screen", "two_nearest", "DestroySet", "ImpactScores", "FilterConfig",
+    "SwapCandidate", "SolveReport", "SolverConfig", "TraceEntry", "best_swap", "find_candidates",
+    "greedy_repair", "impact_scores", "initial_solution", "local_search", "one_opt",
+    "random_destroy", "random_repair", "removal_count", "solve", "worst_remove_destroy",
+]

@@ -1,0 +1,454 @@
+// amvm.cu — kernels and the extern "C" boundary of libamvm.so (include/amvm.h).
+//
+// Build (see paper_2508_13437_b200/build.py):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
+//        -shared -Xcompiler -fPIC -o libamvm.so amvm.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "amvm_engine.cuh"
+
+using namespace amvm;
+
+// ------------------------------------------------------------------ kernels
+// Persistent solve: one CTA per resident slot, instances pulled from a
+// counter so uneven iteration counts balance across SMs.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_solve(KArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Engine<NT> E;
+  E.bind(a, smem, blockIdx.x);
+  WsHeader *hdr = (WsHeader *)a.ws;
+  for (;;) {
+    if (threadIdx.x == 0) E.sh->bc_i[15] = atomicAdd(&hdr->next, 1);
+    __syncthreads();
+    const int64_t inst = E.sh->bc_i[15];
+    __syncthreads();
+    if (inst >= a.count) break;
+    E.solve_instance(a, inst);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_op(KArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Engine<NT> E;
+  E.bind(a, smem, 0);
+  E.run_op(a);
+}
+
+// compute_residual (core.py:183-197) for a batch sharing A: residual[k] =
+// A @ levels_k[idx_k] - B[k] in numpy's OpenBLAS dgemv order, objective[k] =
+// max |residual[k]|.  CTA = kRI instances x all rows; thread = rows; each A
+// element loaded once feeds kRI instances (FP64 FMA, 4 lane-accumulators per
+// output exactly as the dgemv_t 4x4 kernel).  Rows outside the 4x4 groups
+// (m % 4 != 0) and m == 1 take the scalar emulation.
+constexpr int kRI = 8;
+constexpr int kRJ = 256;
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t nlev, int64_t count,
+                                                 const double *__restrict__ At, const double *__restrict__ B,
+                                                 const double *__restrict__ levels, const int32_t *__restrict__ idx,
+                                                 double *__restrict__ res, double *__restrict__ obj) {
+  __shared__ double xs[kRI][kRJ];
+  __shared__ double red[kRI][NT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * kRI;
+  const int ni = (int)(count - k0 < kRI ? count - k0 : kRI);
+  const int64_t g4 = m & ~(int64_t)3, m1 = n & -4;
+  double mx[kRI];
+#pragma unroll
+  for (int q = 0; q < kRI; ++q) mx[q] = 0.0;
+  if (m > 1) {
+    for (int64_t i0 = 0; i0 < g4; i0 += NT) {
+      const int64_t i = i0 + tid;
+      double y[kRI], l[kRI][4];
+#pragma unroll
+      for (int q = 0; q < kRI; ++q) {
+        y[q] = 0.0;
+        l[q][0] = l[q][1] = l[q][2] = l[q][3] = 0.0;
+      }
+      for (int64_t j0 = 0; j0 < m1; j0 += kRJ) {
+        const int jn = (int)(m1 - j0 < kRJ ? m1 - j0 : kRJ);
+        __syncthreads();
+        for (int e = tid; e < kRI * kRJ; e += NT) {
+          const int q = e / kRJ, jj = e - q * kRJ;
+          xs[q][jj] = (q < ni && jj < jn)
+                          ? levels[(k0 + q) * nlev + idx[(k0 + q) * n + j0 + jj]]
+                          : 0.0;
+        }
+        __syncthreads();
+        if (i < g4) {
+          for (int jj = 0; jj < jn; jj += 4) {
+            const int64_t j = j0 + jj;
+            const double a0 = __ldg(At + j * m + i), a1 = __ldg(At + (j + 1) * m + i);
+            const double a2 = __ldg(At + (j + 2) * m + i), a3 = __ldg(At + (j + 3) * m + i);
+#pragma unroll
+            for (int q = 0; q < kRI; ++q) {
+              l[q][0] = amvm::dfma(a0, xs[q][jj], l[q][0]);
+              l[q][1] = amvm::dfma(a1, xs[q][jj + 1], l[q][1]);
+              l[q][2] = amvm::dfma(a2, xs[q][jj + 2], l[q][2]);
+              l[q][3] = amvm::dfma(a3, xs[q][jj + 3], l[q][3]);
+            }
+            if (((j + 4) % 2048) == 0 || j + 4 == m1) {  // end of a dgemv_t block
+#pragma unroll
+              for (int q = 0; q < kRI; ++q) {
+                y[q] = amvm::dadd(y[q], amvm::dadd(amvm::dadd(l[q][0], l[q][2]), amvm::dadd(l[q][1], l[q][3])));
+                l[q][0] = l[q][1] = l[q][2] = l[q][3] = 0.0;
+              }
+            }
+          }
+        }
+      }
+      if (i < g4) {
+        for (int q = 0; q < ni; ++q) {
+          const double *lvq = levels + (k0 + q) * nlev;
+          const int32_t *ix = idx + (k0 + q) * n;
+          auto xv = [&](int64_t j) { return lvq[ix[j]]; };
+          double v = y[q];
+          switch (n & 3) {
+            case 1: v = amvm::dfma(At[m1 * m + i], xv(m1), v); break;
+            case 2: v = amvm::dadd(v, amvm::dfma(At[m1 * m + i], xv(m1), amvm::dmul(At[(m1 + 1) * m + i], xv(m1 + 1)))); break;
+            case 3:
+              v = amvm::dadd(v, amvm::dfma(At[(m1 + 2) * m + i], xv(m1 + 2),
+                               amvm::dfma(At[m1 * m + i], xv(m1), amvm::dmul(At[(m1 + 1) * m + i], xv(m1 + 1)))));
+              break;
+            default: break;
+          }
+          v = amvm::dsub(v, B[(k0 + q) * m + i]);
+          res[(k0 + q) * m + i] = v;
+          mx[q] = fmax(mx[q], fabs(v));
+        }
+      }
+    }
+    // leftover rows (4x2 / 4x1 kernels)
+    for (int64_t i = g4 + tid; i < m; i += NT) {
+      for (int q = 0; q < ni; ++q) {
+        const double *lvq = levels + (k0 + q) * nlev;
+        const int32_t *ix = idx + (k0 + q) * n;
+        double v = gemv_row([&](int64_t j) { return At[j * m + i]; }, [&](int64_t j) { return lvq[ix[j]]; }, n,
+                            gemv_kind(i, m));
+        v = amvm::dsub(v, B[(k0 + q) * m + i]);
+        res[(k0 + q) * m + i] = v;
+        mx[q] = fmax(mx[q], fabs(v));
+      }
+    }
+  } else if (warp < ni) {  // m == 1: numpy uses ddot
+    const int q = warp;
+    const double *lvq = levels + (k0 + q) * nlev;
+    const int32_t *ix = idx + (k0 + q) * n;
+    double v = warp_ddot_skx([&](int64_t j) { return At[j]; }, [&](int64_t j) { return lvq[ix[j]]; }, n, lane);
+    v = amvm::dsub(v, B[k0 + q]);
+    if (lane == 0) res[k0 + q] = v;
+    mx[q] = fabs(v);
+  }
+#pragma unroll
+  for (int q = 0; q < kRI; ++q) {
+    double v = warp_max(mx[q]);
+    if (lane == 0) red[q][warp] = v;
+  }
+  __syncthreads();
+  if (tid < ni) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[tid][w]);
+    obj[k0 + tid] = v;
+  }
+}
+
+// ---------------------------------------------------------------- planning
+namespace {
+
+struct Plan {
+  int nt;
+  size_t smem;
+  int cr_smem, tab, cap;
+  size_t slot_bytes;
+  int64_t slots;
+  size_t ws_bytes;
+};
+
+int64_t pow2ceil(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+template <int NT>
+size_t smem_bytes(int64_t m, int64_t nlev, int cr_smem, int tab) {
+  size_t s = sizeof(Shared<NT>) + 8 * ((nlev + 1) & ~1) + 8 * kTC * (kTK + 1);
+  if (tab) s += 8 * kG * nlev * nlev;
+  if (cr_smem) s += 8 * m;
+  return s;
+}
+
+template <int NT>
+int occupancy(size_t smem, bool op, int *blocks) {
+  auto fn = op ? k_op<NT> : k_solve<NT>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, NT, smem);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  return AMVM_OK;
+}
+
+size_t smem_for(int nt, int64_t m, int64_t nlev, int cr_smem, int tab) {
+  (void)nt;
+  return smem_bytes<256>(m, nlev, cr_smem, tab);
+}
+
+int occupancy_for(int nt, size_t smem, bool op, int *blocks) {
+  (void)nt;
+  return occupancy<256>(smem, op, blocks);
+}
+
+constexpr size_t kSmemMax = 220 * 1024;
+
+int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
+  if (!p || !prm) return AMVM_ERR_INVALID;
+  if (p->m < 1 || p->n < 1 || p->nlev < 1 || p->count < 1) return AMVM_ERR_INVALID;
+  if (p->n > 0x7fffffff || p->m > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
+  if (prm->r < 1 || prm->r > p->n || prm->k_eps < 1 || prm->max_iters < 0 || prm->refresh_period < 1 ||
+      prm->n_segment < 1)
+    return AMVM_ERR_INVALID;
+  int nt = prm->threads;
+  if (nt == 0) nt = 256;
+  if (nt != 256) return AMVM_ERR_UNSUPPORTED;  // this build instantiates NT = 256
+  P->nt = nt;
+  P->tab = p->nlev <= kTabMaxLev;
+  P->cr_smem = p->m * 8 <= 96 * 1024;
+  const int64_t n = p->n;
+  const int64_t maxc = prm->max_candidates;
+  int64_t cap = maxc > 0 ? std::max<int64_t>(std::max<int64_t>(2 * maxc, maxc + n), 1024)
+                         : std::max<int64_t>(n * (n - 1) / 2, 1024);
+  cap = pow2ceil(cap);
+  if (cap > ((int64_t)1 << 30)) return AMVM_ERR_UNSUPPORTED;
+  P->cap = (int)cap;
+  P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
+  if (P->smem > kSmemMax && P->cr_smem) {
+    P->cr_smem = 0;
+    P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
+  }
+  if (P->smem > kSmemMax && P->tab) {
+    P->tab = 0;
+    P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
+  }
+  if (P->smem > kSmemMax) return AMVM_ERR_UNSUPPORTED;  // nlev too large for the smem level table
+  const SlotLayout L = slot_layout(p->m, p->n, prm->k_eps, prm->r, cap);
+  P->slot_bytes = al256(L.total);
+  if (op) {
+    P->slots = 1;
+  } else {
+    int dev = 0, sms = 0, blocks = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return AMVM_ERR_NO_DEVICE;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return AMVM_ERR_CUDA;
+    int rc = occupancy_for(nt, P->smem, false, &blocks);
+    if (rc) return rc;
+    if (blocks < 1) return AMVM_ERR_UNSUPPORTED;
+    P->slots = std::min<int64_t>(p->count, (int64_t)blocks * sms);
+  }
+  P->ws_bytes = sizeof(WsHeader) + (size_t)P->slots * P->slot_bytes;
+  return AMVM_OK;
+}
+
+int cuda_rc(cudaError_t e) { return e == cudaSuccess ? AMVM_OK : AMVM_ERR_CUDA; }
+
+KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, void *ws) {
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.m = p->m; a.n = p->n; a.nlev = p->nlev; a.count = p->count;
+  a.At = p->At; a.B = p->B; a.levels = p->levels;
+  a.prm = *prm;
+  a.ws = (unsigned char *)ws;
+  a.slot_bytes = P.slot_bytes;
+  a.cr_smem = P.cr_smem; a.tab = P.tab; a.cap = P.cap;
+  a.time_budget_ns = prm->time_limit_s < 0 ? -1 : (int64_t)(prm->time_limit_s * 1e9);
+  return a;
+}
+
+int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a.ws, 0, sizeof(WsHeader), st);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  int blocks = 0;
+  int rc = occupancy_for(P.nt, P.smem, op, &blocks);  // also sets the smem attribute
+  if (rc) return rc;
+  const dim3 grid((unsigned)P.slots), block((unsigned)P.nt);
+  if (op) k_op<256><<<grid, block, P.smem, st>>>(a);
+  else k_solve<256><<<grid, block, P.smem, st>>>(a);
+  return cuda_rc(cudaGetLastError());
+}
+
+int run_op(const amvm_problem *prob, const amvm_params *prm, KArgs &a, void *ws, size_t ws_bytes,
+           void *stream) {
+  Plan P;
+  amvm_problem one = *prob;
+  one.count = 1;
+  int rc = make_plan(&one, prm, true, &P);
+  if (rc) return rc;
+  if (!ws || ws_bytes < P.ws_bytes) return AMVM_ERR_WORKSPACE;
+  KArgs b = base_args(&one, prm, P, ws);
+  b.op = a.op; b.kind = a.kind;
+  b.s_idx = a.s_idx; b.s_r = a.s_r; b.s_obj = a.s_obj; b.s_cnt = a.s_cnt; b.rng = a.rng;
+  b.x_i = a.x_i; b.x_j = a.x_j; b.x_cnt = a.x_cnt; b.x_saved = a.x_saved; b.x_d = a.x_d;
+  b.x_out4 = a.x_out4; b.x_cap = a.x_cap; b.x_r = a.x_r;
+  return launch(P, true, b, (cudaStream_t)stream);
+}
+
+bool sol_ok(const amvm_solution *s) { return s && s->idx && s->residual && s->objective && s->updates; }
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+int amvm_abi_version(void) { return AMVM_ABI_VERSION; }
+
+const char *amvm_strerror(int status) {
+  switch (status) {
+    case AMVM_OK: return "ok";
+    case AMVM_ERR_INVALID: return "invalid argument";
+    case AMVM_ERR_CUDA: return "CUDA runtime error";
+    case AMVM_ERR_WORKSPACE: return "workspace too small (see amvm_workspace_bytes)";
+    case AMVM_ERR_UNSUPPORTED: return "problem shape outside this build's limits";
+    case AMVM_ERR_NO_DEVICE: return "no usable sm_100 device";
+    default: return "unknown status";
+  }
+}
+
+size_t amvm_workspace_bytes(const amvm_problem *prob, const amvm_params *prm) {
+  Plan P;
+  if (make_plan(prob, prm, false, &P)) return 0;
+  Plan Q;
+  amvm_problem one = *prob;
+  one.count = 1;
+  if (make_plan(&one, prm, true, &Q)) return 0;
+  return std::max(P.ws_bytes, Q.ws_bytes);
+}
+
+int amvm_solve(const amvm_problem *prob, const amvm_params *prm, const amvm_solution *start, amvm_pcg64 *rng,
+               amvm_result *res, void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !prm || !sol_ok(start) || !rng || !res || !sol_ok(&res->best) || !res->initial_objective ||
+      !res->iterations || !res->operator_uses)
+    return AMVM_ERR_INVALID;
+  if (!prob->At || !prob->B || !prob->levels) return AMVM_ERR_INVALID;
+  Plan P;
+  int rc = make_plan(prob, prm, false, &P);
+  if (rc) return rc;
+  if (!ws || ws_bytes < P.ws_bytes) return AMVM_ERR_WORKSPACE;
+  KArgs a = base_args(prob, prm, P, ws);
+  a.s_idx = start->idx; a.s_r = start->residual; a.s_obj = start->objective; a.s_cnt = start->updates;
+  a.rng = rng;
+  a.res = *res;
+  return launch(P, false, a, (cudaStream_t)stream);
+}
+
+int amvm_status(const void *ws, void *stream) {
+  if (!ws) return AMVM_ERR_INVALID;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return AMVM_ERR_CUDA;
+  WsHeader h;
+  if (cudaMemcpy(&h, ws, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return AMVM_ERR_CUDA;
+  return h.status;
+}
+
+int amvm_one_opt(const amvm_problem *prob, const amvm_params *prm, amvm_solution *sol, void *ws,
+                 size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol)) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_ONE_OPT;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_local_search(const amvm_problem *prob, const amvm_params *prm, amvm_solution *sol, void *ws,
+                      size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol)) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_LOCAL_SEARCH;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_find_candidates(const amvm_problem *prob, const amvm_params *prm, const amvm_solution *sol,
+                         int32_t *out_i, int32_t *out_j, double *out_delta, int32_t *count, int32_t cap,
+                         void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol) || !out_i || !out_j || !out_delta || !count || cap < 0) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_FIND_CAND;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  a.x_i = out_i; a.x_j = out_j; a.x_d = out_delta; a.x_cnt = count; a.x_cap = cap;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_best_swap(const amvm_problem *prob, const amvm_params *prm, const amvm_solution *sol, double *out4,
+                   void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol) || !out4) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_BEST_SWAP;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  a.x_out4 = out4;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_impact_scores(const amvm_problem *prob, const amvm_params *prm, const amvm_solution *sol, double *d,
+                       void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol) || !d || prm->alpha < 0) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_IMPACT;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  a.x_d = d;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_destroy(const amvm_problem *prob, const amvm_params *prm, int kind, const amvm_solution *sol,
+                 amvm_pcg64 *rng, int32_t *removed, void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol) || !rng || !removed || (kind != 0 && kind != 1)) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_DESTROY;
+  a.kind = kind;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  a.rng = rng;
+  a.x_i = removed;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int kind, amvm_solution *sol, amvm_pcg64 *rng,
+                const int32_t *removed, const int32_t *saved_idx, int32_t r, void *ws, size_t ws_bytes,
+                void *stream) {
+  if (!prob || !sol_ok(sol) || !rng || !removed || !saved_idx || r < 0 || (kind != 0 && kind != 1) ||
+      prob->nlev < 2)
+    return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_REPAIR;
+  a.kind = kind;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  a.rng = rng;
+  a.x_i = const_cast<int32_t *>(removed);
+  a.x_saved = const_cast<int32_t *>(saved_idx);
+  a.x_r = r;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol, void *stream) {
+  if (!prob || !sol_ok(sol) || !prob->At || !prob->B || !prob->levels) return AMVM_ERR_INVALID;
+  if (prob->m < 1 || prob->n < 1 || prob->count < 1) return AMVM_ERR_INVALID;
+  const int64_t blocks = (prob->count + kRI - 1) / kRI;
+  k_residual<256><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      prob->m, prob->n, prob->nlev, prob->count, prob->At, prob->B, prob->levels, sol->idx, sol->residual,
+      sol->objective);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  e = cudaMemsetAsync(sol->updates, 0, sizeof(int32_t) * prob->count, (cudaStream_t)stream);
+  return cuda_rc(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,300 @@
+// amvm_device.cuh — device primitives for the AMVM engine (sm_100a).
+//
+// Everything here reproduces a piece of numpy/OpenBLAS arithmetic that the
+// reference's decisions depend on, written for the GPU:
+//   * PCG64 + the numpy Generator draws the path consumes,
+//   * numpy's pairwise 1-d sum, block-parallel over its fixed leaf tree,
+//   * OpenBLAS SkylakeX ddot (np.linalg.norm) and dgemv_t (A @ x) orders,
+//   * warp/block max reductions (max is exact, so any order is bitwise).
+// All residual arithmetic uses explicit __dmul_rn/__dadd_rn so no FMA
+// contraction can change a bit (the library is also built -fmad=false).
+#pragma once
+
+#include <cstdint>
+
+#define AMVM_FULL 0xffffffffu
+
+namespace amvm {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// ------------------------------------------------------------------ PCG64
+// numpy/random/src/pcg64/pcg64.h: 128-bit LCG, XSL-RR, advance then output;
+// next_uint32 hands out the low half first and buffers the high half.
+struct Pcg {
+  unsigned __int128 s, inc;
+  uint32_t has32, u32;
+};
+
+__device__ __forceinline__ uint64_t pcg_next64(Pcg &g) {
+  const unsigned __int128 mult =
+      ((unsigned __int128)0x2360ED051FC65DA4ULL << 64) | (unsigned __int128)0x4385DF649FCCF645ULL;
+  g.s = g.s * mult + g.inc;
+  uint64_t hi = (uint64_t)(g.s >> 64), lo = (uint64_t)g.s;
+  uint64_t x = hi ^ lo;
+  unsigned rot = (unsigned)(hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+__device__ __forceinline__ uint32_t pcg_next32(Pcg &g) {
+  if (g.has32) {
+    g.has32 = 0;
+    return g.u32;
+  }
+  uint64_t v = pcg_next64(g);
+  g.has32 = 1;
+  g.u32 = (uint32_t)(v >> 32);
+  return (uint32_t)v;
+}
+
+// Generator.random(): 53 random bits scaled to [0, 1).
+__device__ __forceinline__ double pcg_random(Pcg &g) {
+  return (double)(pcg_next64(g) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// random_bounded_uint64(off=0, rng, use_masked=false), rng <= 2^32-1: Lemire.
+__device__ __forceinline__ uint64_t pcg_bounded(Pcg &g, uint64_t rng) {
+  if (rng == 0) return 0;
+  if (rng == 0xFFFFFFFFULL) return pcg_next32(g);
+  uint32_t ex = (uint32_t)rng + 1u;
+  uint64_t m = (uint64_t)pcg_next32(g) * ex;
+  uint32_t left = (uint32_t)m;
+  if (left < ex) {
+    uint32_t thr = (uint32_t)(0xFFFFFFFFu - (uint32_t)rng) % ex;
+    while (left < thr) {
+      m = (uint64_t)pcg_next32(g) * ex;
+      left = (uint32_t)m;
+    }
+  }
+  return m >> 32;
+}
+
+// --------------------------------------------------------------- warp ops
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(AMVM_FULL, v, o));
+  return v;
+}
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(AMVM_FULL, v, o);
+  return v;
+}
+
+// Transpose-reduce: on entry each lane holds v[0..31]; on exit v[0] of lane
+// l is the max over the warp of everybody's v[l] (31 shuffles, not 160).
+__device__ __forceinline__ double warp_transpose_max32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      double send = up ? v[k] : v[k + s];
+      double keep = up ? v[k + s] : v[k];
+      double recv = __shfl_xor_sync(AMVM_FULL, send, s);
+      v[k] = fmax(keep, recv);
+    }
+  }
+  return v[0];
+}
+
+// -------------------------------------------------- numpy pairwise summation
+// numpy/_core/src/umath/loops_utils.h pairwise_sum: n < 8 sequential from 0;
+// n <= 128 eight accumulators + ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) + tail;
+// otherwise split at n2 = n/2 - (n/2)%8 and add the halves.
+template <class F>
+__device__ double pw_leaf(F &&get, int64_t lo, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = dadd(res, get(lo + i));
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = get(lo + k);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = dadd(r[k], get(lo + i + k));
+  }
+  double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+  for (; i < n; ++i) res = dadd(res, get(lo + i));
+  return res;
+}
+
+// Leaves of the pairwise tree of length n, in left-to-right order.  Returns
+// the count (<= cap); leaf k covers [lo[k], lo[k]+len[k]).
+__device__ inline int pw_leaves(int64_t n, int64_t *lo, int64_t *len, int cap) {
+  // explicit stack of (lo, n); push right then left so leaves pop in order
+  int64_t st_lo[48], st_n[48];
+  int sp = 0, cnt = 0;
+  st_lo[sp] = 0;
+  st_n[sp++] = n;
+  while (sp) {
+    --sp;
+    int64_t a = st_lo[sp], c = st_n[sp];
+    if (c <= 128) {
+      if (cnt < cap) {
+        lo[cnt] = a;
+        len[cnt] = c;
+      }
+      ++cnt;
+    } else {
+      int64_t n2 = c / 2;
+      n2 -= n2 % 8;
+      st_lo[sp] = a + n2;
+      st_n[sp++] = c - n2;
+      st_lo[sp] = a;
+      st_n[sp++] = n2;
+    }
+  }
+  return cnt;
+}
+
+// Combine leaf sums in the exact tree order (recursive shape, iterative walk).
+__device__ inline double pw_combine(int64_t n, const double *leaf_sum) {
+  // post-order evaluation with an explicit stack
+  int64_t st_n[48];
+  int st_state[48];
+  double st_val[48];
+  int sp = 0, leaf = 0;
+  st_n[0] = n;
+  st_state[0] = 0;
+  sp = 1;
+  double ret = 0.0;
+  while (sp) {
+    int top = sp - 1;
+    int64_t c = st_n[top];
+    if (c <= 128) {
+      ret = leaf_sum[leaf++];
+      --sp;
+      // deliver to parent
+      while (sp) {
+        int p = sp - 1;
+        if (st_state[p] == 1) {  // left done, now right
+          st_val[p] = ret;
+          st_state[p] = 2;
+          int64_t n2 = st_n[p] / 2;
+          n2 -= n2 % 8;
+          st_n[sp] = st_n[p] - n2;
+          st_state[sp] = 0;
+          ++sp;
+          break;
+        } else {  // state 2: right done
+          ret = dadd(st_val[p], ret);
+          --sp;
+        }
+      }
+    } else if (st_state[top] == 0) {
+      st_state[top] = 1;
+      int64_t n2 = c / 2;
+      n2 -= n2 % 8;
+      st_n[sp] = n2;
+      st_state[sp] = 0;
+      ++sp;
+    }
+  }
+  return ret;
+}
+
+// ---------------------------------------------- OpenBLAS SkylakeX ddot order
+// One warp computes x.y (x == y for norms): lane = accumulator slot (q, l) of
+// the 4 x 8-lane AVX-512 FMA accumulators over n & ~31, then lane 0 folds in
+// the kernel's exact order and runs the scalar FMA tail.  Returns the dot in
+// every lane.
+template <class GX, class GY>
+__device__ double warp_ddot_skx(GX &&gx, GY &&gy, int64_t n, int lane) {
+  const int64_t n1 = n & -16;
+  const int64_t n32 = n1 & ~(int64_t)31;
+  double a = 0.0;  // lane = 8*q + l
+  for (int64_t i = 0; i < n32; i += 32) a = dfma(gx(i + lane), gy(i + lane), a);
+  double dot = 0.0;
+  if (n1) {
+    // fold 512 -> 256: acc[q][l] = a[q][l] + a[q][l+4] (l < 4)
+    double hi = __shfl_down_sync(AMVM_FULL, a, 4);
+    double acc = dadd(a, hi);  // valid in lanes with (lane & 4) == 0
+    // remaining 16-block: acc[q][l] (q < 4, l < 4) gets x[n32 + 4q + l]
+    const int q = lane >> 3, l = lane & 7;
+    if (n1 - n32 == 16 && l < 4) acc = dfma(gx(n32 + 4 * q + l), gy(n32 + 4 * q + l), acc);
+    // gather acc[q][l] to lane 0
+    double v[4][4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+      for (int ll = 0; ll < 4; ++ll) v[qq][ll] = __shfl_sync(AMVM_FULL, acc, 8 * qq + ll);
+    double s[4];
+#pragma unroll
+    for (int ll = 0; ll < 4; ++ll) s[ll] = dadd(dadd(dadd(v[0][ll], v[1][ll]), v[2][ll]), v[3][ll]);
+    dot = dadd(dadd(s[0], s[2]), dadd(s[1], s[3]));
+  }
+  for (int64_t i = n1; i < n; ++i) dot = dfma(gy(i), gx(i), dot);
+  return dot;
+}
+
+// ------------------------------------------ OpenBLAS dgemv_t (numpy A @ x)
+// One output of A @ x for a C-contiguous A (kernel/x86_64/dgemv_t_4.c with
+// the Haswell micro-kernels, used for SkylakeX): K & -4 elements in blocks
+// of 2048 reduced by the kernel of the output's position (kind 4: 4x4,
+// 4-lane FMA, lanes (0+2)+(1+3); kind 2: 4x2, 2-lane mul+add; kind 1: 4x1,
+// two 2-lane mul+add accumulators), each block added to y; then the K & 3
+// leftover in the compiler-contracted scalar form.  `a(j)` = A[i][j].
+template <class GA, class GX>
+__device__ double gemv_row(GA &&a, GX &&x, int64_t K, int kind) {
+  const int64_t m1 = K & -4;
+  double y = 0.0;
+  for (int64_t p = 0; p < m1; p += 2048) {
+    const int64_t e = p + (m1 - p < 2048 ? m1 - p : 2048);
+    double t;
+    if (kind == 4) {
+      double l0 = 0, l1 = 0, l2 = 0, l3 = 0;
+      for (int64_t i = p; i < e; i += 4) {
+        l0 = dfma(a(i), x(i), l0);
+        l1 = dfma(a(i + 1), x(i + 1), l1);
+        l2 = dfma(a(i + 2), x(i + 2), l2);
+        l3 = dfma(a(i + 3), x(i + 3), l3);
+      }
+      t = dadd(dadd(l0, l2), dadd(l1, l3));
+    } else if (kind == 2) {
+      double l0 = 0, l1 = 0;
+      for (int64_t i = p; i < e; i += 2) {
+        l0 = dadd(l0, dmul(a(i), x(i)));
+        l1 = dadd(l1, dmul(a(i + 1), x(i + 1)));
+      }
+      t = dadd(l0, l1);
+    } else {
+      double u0 = 0, u1 = 0, v0 = 0, v1 = 0;
+      for (int64_t i = p; i < e; i += 4) {
+        u0 = dadd(u0, dmul(a(i), x(i)));
+        u1 = dadd(u1, dmul(a(i + 1), x(i + 1)));
+        v0 = dadd(v0, dmul(a(i + 2), x(i + 2)));
+        v1 = dadd(v1, dmul(a(i + 3), x(i + 3)));
+      }
+      t = dadd(dadd(u0, v0), dadd(u1, v1));
+    }
+    y = dadd(y, t);
+  }
+  switch (K & 3) {
+    case 1: y = dfma(a(m1), x(m1), y); break;
+    case 2: y = dadd(y, dfma(a(m1), x(m1), dmul(a(m1 + 1), x(m1 + 1)))); break;
+    case 3:
+      y = dadd(y, dfma(a(m1 + 2), x(m1 + 2), dfma(a(m1), x(m1), dmul(a(m1 + 1), x(m1 + 1)))));
+      break;
+    default: break;
+  }
+  return y;
+}
+
+// kernel kind of output row i of an m-row dgemv_t (4x4 groups, then 4x2, 4x1)
+__device__ __forceinline__ int gemv_kind(int64_t i, int64_t m) {
+  const int64_t g4 = m & ~(int64_t)3;
+  if (i < g4) return 4;
+  if ((m & 2) && i < g4 + 2) return 2;
+  return 1;
+}
+
+}  // namespace amvm

@@ -1,0 +1,1181 @@
+// amvm_engine.cuh — the AMVM iteration as a CTA-resident device state machine.
+//
+// One CTA owns one instance at a time (a persistent grid pulls instance ids
+// from an atomic counter), so an ALNS iteration — select, destroy, repair,
+// local search, accept, weight update, trace — never leaves the SM
+// (controller.py:233-275).  Inside the CTA:
+//   * thread t owns residual rows i = t + k*NT, so every rank-1/rank-2 update
+//     (core.py:208-245) is thread-local and needs no barrier;
+//   * block-uniform scalars (objectives, refresh counters, operator bank) are
+//     replicated in every thread's registers and evolve identically;
+//   * RNG draws and the few inherently sequential scans (Floyd sampling,
+//     cumsum of the worst-remove cdf) run on thread 0 and are broadcast;
+//   * A is column-major (At), so scoring streams each column once, coalesced
+//     across the CTA (localsearch.py:73-79), and W = 16 columns are scored
+//     per barrier with a speculative window: all columns of the window see
+//     the same residual, the lowest improving column is applied (exactly the
+//     sequential first-improvement of one_opt) and scanning resumes after it.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/amvm.h"
+#include "amvm_device.cuh"
+
+namespace amvm {
+
+constexpr int kWin = 16;       // one_opt speculative window (columns per barrier)
+constexpr int kG = 4;          // filter rows gathered row-major per find_candidates
+constexpr int kTabMaxLev = 32; // bound table in smem when nlev <= this
+constexpr int kTC = 128;       // impact tile: columns
+constexpr int kTK = 16;        // impact tile: rows
+
+struct Cand {
+  int32_t i, j;
+  double d;
+};
+
+// Everything a kernel launch needs, passed by value.
+struct KArgs {
+  int64_t m, n, nlev, count;
+  const double *At, *B, *levels;
+  amvm_params prm;
+  // start solution (solve) or in/out solution (component ops)
+  int32_t *s_idx;
+  double *s_r, *s_obj;
+  int32_t *s_cnt;
+  amvm_pcg64 *rng;
+  amvm_result res;
+  unsigned char *ws;  // workspace base (header + slots)
+  size_t slot_bytes;
+  int cr_smem, tab, cap;
+  int64_t time_budget_ns;  // < 0: none
+  // component-op extras
+  int op, kind;
+  int32_t *x_i, *x_j, *x_cnt;  // find_candidates out / removed in-out
+  int32_t *x_saved;
+  double *x_d, *x_out4;
+  int32_t x_cap, x_r;
+};
+
+enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR };
+
+struct WsHeader {
+  int32_t status;
+  int32_t next;
+  int32_t pad[62];
+};
+
+// Per-slot workspace carve-up (shared by host sizing and device use).
+struct SlotLayout {
+  size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
+      hset, rem, sav, pick, coin, ibuf, total;
+  int64_t nleaf, kk, hsz;
+};
+
+__host__ __device__ inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline uint64_t gen_mask(uint64_t v) {
+  v |= v >> 1; v |= v >> 2; v |= v >> 4; v |= v >> 8; v |= v >> 16; v |= v >> 32;
+  return v;
+}
+
+__host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t k_eps, int64_t r, int64_t cap) {
+  SlotLayout L;
+  int64_t mn = m > n ? m : n;
+  L.nleaf = mn / 64 + 4;
+  L.kk = k_eps < m ? k_eps : m;
+  if (L.kk < 1) L.kk = 1;
+  int64_t rr = r > 0 ? r : 1;
+  L.hsz = (int64_t)gen_mask((uint64_t)(1.2 * (double)rr)) + 1;
+  size_t o = 0;
+  L.ur = o; o = al256(o + 8 * m);
+  L.crg = o; o = al256(o + 8 * m);
+  L.uidx = o; o = al256(o + 4 * n);
+  L.cidx = o; o = al256(o + 4 * n);
+  L.dmv = o; o = al256(o + 8 * n);
+  L.dpv = o; o = al256(o + 8 * n);
+  L.dbuf = o; o = al256(o + 8 * n);
+  L.pbuf = o; o = al256(o + 8 * n);
+  L.lf_lo = o; o = al256(o + 16 * L.nleaf);
+  L.lf_len = o; o = al256(o + 16 * L.nleaf);
+  L.lf_sum = o; o = al256(o + 8 * L.nleaf);
+  L.rows = o; o = al256(o + 4 * L.kk);
+  L.reps = o; o = al256(o + 8 * L.kk);
+  L.rsgn = o; o = al256(o + 4 * L.kk);
+  L.ag = o; o = al256(o + 8 * kG * n);
+  L.cbuf = o; o = al256(o + sizeof(Cand) * cap);
+  L.hset = o; o = al256(o + 8 * L.hsz);
+  L.rem = o; o = al256(o + 4 * rr);
+  L.sav = o; o = al256(o + 4 * rr);
+  L.pick = o; o = al256(o + 4 * rr);
+  L.coin = o; o = al256(o + 4 * rr);
+  L.ibuf = o; o = al256(o + 4 * (n > L.kk ? n : L.kk));
+  L.total = o;
+  return L;
+}
+
+template <int NT>
+struct Shared {
+  static constexpr int NW = NT / 32;
+  double red[2][NW][32];
+  double redS[NW];
+  double bc_d[8];
+  int bc_i[16];
+  int wcnt[NW];
+  unsigned int hist[256];
+  int counter;
+  Pcg rng;
+};
+
+__device__ __forceinline__ uint64_t abs_key(double x) { return (uint64_t)__double_as_longlong(fabs(x)); }
+
+template <int NT>
+struct Engine {
+  static constexpr int NW = NT / 32;
+  // problem
+  int64_t m, n, nlev;
+  const double *At, *b;
+  double *lv;  // smem
+  const amvm_params *prm;
+  // state
+  double *cr, *ur;
+  int32_t *cidx, *uidx;
+  double *dmv, *dpv, *dbuf, *pbuf;
+  int64_t *lf_lo, *lf_len;
+  double *lf_sum;
+  int nleaf_m, nleaf_n;
+  int32_t *rows, *rsgn;
+  double *reps;
+  double *ag, *btab, *tile;
+  Cand *cbuf;
+  uint64_t *hset;
+  int32_t *rem, *sav, *pick, *coin, *ibuf;
+  int64_t kk, cap;
+  int tab;
+  Shared<NT> *sh;
+  int tid, lane, warp;
+  // replicated scalars
+  double cobj, uobj, bobj;
+  int ccnt, ucnt, bcnt;
+  double w[4], sc[4];
+  int64_t seg[4], life[4], bit;
+  int64_t mv_ref, mv_raw;
+  int32_t *status;
+
+  // ------------------------------------------------------------ utilities
+  __device__ void fail(int code) {
+    if (tid == 0) atomicCAS(status, 0, code);
+  }
+
+  __device__ double block_max_own(double mx) {
+    mx = warp_max(mx);
+    if (lane == 0) sh->redS[warp] = mx;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) t = fmax(t, sh->redS[k]);
+    __syncthreads();
+    return t;
+  }
+
+  __device__ double own_max_abs() {
+    double mx = 0.0;
+    for (int64_t i = tid; i < m; i += NT) mx = fmax(mx, fabs(cr[i]));
+    return block_max_own(mx);
+  }
+
+  // numpy pairwise sum of get(0..len-1) over the cached leaf tree.
+  template <class F>
+  __device__ double block_pairwise(F &&get, int64_t len, int64_t *lo, int64_t *ln, int nleaf) {
+    for (int k = tid; k < nleaf; k += NT) lf_sum[k] = pw_leaf(get, lo[k], ln[k]);
+    __syncthreads();
+    double s = pw_combine(len, lf_sum);
+    __syncthreads();
+    return s;
+  }
+
+  // Solution.refresh (core.py:173-177): numpy A @ x - b in the OpenBLAS order.
+  __device__ void refresh() {
+    __syncthreads();  // publish cidx
+    if (m == 1) {
+      if (warp == 0) {
+        double y = warp_ddot_skx([&](int64_t j) { return At[j]; },
+                                 [&](int64_t j) { return lv[cidx[j]]; }, n, lane);
+        if (lane == 0) cr[0] = dsub(y, b[0]);
+      }
+    } else {
+      for (int64_t i = tid; i < m; i += NT) {
+        double y = gemv_row([&](int64_t j) { return At[j * m + i]; },
+                            [&](int64_t j) { return lv[cidx[j]]; }, n, gemv_kind(i, m));
+        cr[i] = dsub(y, b[i]);
+      }
+    }
+    __syncthreads();
+    cobj = own_max_abs();
+    ccnt = 0;
+  }
+
+  __device__ void bump_known(double t) {
+    ccnt += 1;
+    if (ccnt >= prm->refresh_period) refresh();
+    else cobj = t;
+  }
+
+  // apply_shift (core.py:208-225) when the new objective is not known yet.
+  __device__ bool apply_shift_reduce(int64_t j, int nl) {
+    const int old = cidx[j];
+    if (nl == old) return false;
+    const double d = dsub(lv[nl], lv[old]);
+    const double *col = At + j * m;
+    double mx = 0.0;
+    for (int64_t i = tid; i < m; i += NT) {
+      double y = dadd(cr[i], dmul(d, __ldg(col + i)));
+      cr[i] = y;
+      mx = fmax(mx, fabs(y));
+    }
+    mx = warp_max(mx);
+    if (lane == 0) sh->redS[warp] = mx;
+    __syncthreads();
+    if (tid == 0) cidx[j] = nl;
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) t = fmax(t, sh->redS[k]);
+    __syncthreads();
+    ccnt += 1;
+    if (ccnt >= prm->refresh_period) refresh();
+    else cobj = t;
+    return true;
+  }
+
+  // ------------------------------------------------------------- one_opt
+  __device__ void set_deltas(int64_t j, int k) {
+    dmv[j] = k > 0 ? dsub(lv[k - 1], lv[k]) : 0.0;
+    dpv[j] = k + 1 < nlev ? dsub(lv[k + 1], lv[k]) : 0.0;
+  }
+
+  // one_opt, localsearch.py:59-88, with the speculative window described in
+  // the file header.  Candidates of columns after the applied one are
+  // re-scored against the updated residual (counted as raw, not reference).
+  __device__ void one_opt() {
+    __syncthreads();
+    for (int64_t j = tid; j < n; j += NT) set_deltas(j, cidx[j]);
+    __syncthreads();
+    int par = 0;
+    for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
+      bool changed = false;
+      int64_t p = 0;
+      while (p < n) {
+        const int wc = (int)(n - p < kWin ? n - p : kWin);
+        double dm[kWin], dp[kWin], v[32];
+#pragma unroll
+        for (int w = 0; w < kWin; ++w) {
+          dm[w] = w < wc ? dmv[p + w] : 0.0;
+          dp[w] = w < wc ? dpv[p + w] : 0.0;
+          v[w] = 0.0;
+          v[w + kWin] = 0.0;
+        }
+        // lane w < wc keeps the level of column p+w for the decision below
+        const int kdec = lane < wc ? cidx[p + lane] : 0;
+        const double *a0 = At + p * m;
+        if (wc == kWin) {
+          for (int64_t i = tid; i < m; i += NT) {
+            const double r = cr[i];
+            double av[kWin];
+#pragma unroll
+            for (int w = 0; w < kWin; ++w) av[w] = __ldg(a0 + w * m + i);
+#pragma unroll
+            for (int w = 0; w < kWin; ++w) {
+              v[w] = fmax(v[w], fabs(dadd(r, dmul(dm[w], av[w]))));
+              v[w + kWin] = fmax(v[w + kWin], fabs(dadd(r, dmul(dp[w], av[w]))));
+            }
+          }
+        } else {
+          for (int64_t i = tid; i < m; i += NT) {
+            const double r = cr[i];
+#pragma unroll
+            for (int w = 0; w < kWin; ++w) {
+              if (w < wc) {
+                double av = __ldg(a0 + w * m + i);
+                v[w] = fmax(v[w], fabs(dadd(r, dmul(dm[w], av))));
+                v[w + kWin] = fmax(v[w + kWin], fabs(dadd(r, dmul(dp[w], av))));
+              }
+            }
+          }
+        }
+        double t = warp_transpose_max32(v, lane);
+        sh->red[par][warp][lane] = t;
+        __syncthreads();
+        t = 0.0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) t = fmax(t, sh->red[par][k][lane]);
+        par ^= 1;
+        const double tp = __shfl_sync(AMVM_FULL, t, (lane + kWin) & 31);
+        int lvl = -1;
+        double bt = cobj;
+        if (lane < wc) {
+          if (kdec - 1 >= 0 && t < bt) { bt = t; lvl = kdec - 1; }
+          if (kdec + 1 < nlev && tp < bt) { bt = tp; lvl = kdec + 1; }
+        }
+        const unsigned imp = __ballot_sync(AMVM_FULL, lvl >= 0);
+        const unsigned vlo = __ballot_sync(AMVM_FULL, lane < wc && kdec > 0);
+        const unsigned vhi = __ballot_sync(AMVM_FULL, lane < wc && kdec + 1 < nlev);
+        mv_raw += __popc(vlo) + __popc(vhi);
+        if (imp) {
+          const int ws = __ffs(imp) - 1;
+          const unsigned upto = ws == 31 ? AMVM_FULL : ((2u << ws) - 1u);
+          mv_ref += __popc(vlo & upto) + __popc(vhi & upto);
+          const int nl = __shfl_sync(AMVM_FULL, lvl, ws);
+          const int old = __shfl_sync(AMVM_FULL, kdec, ws);
+          const double nt = __shfl_sync(AMVM_FULL, bt, ws);
+          const int64_t j = p + ws;
+          const double d = dsub(lv[nl], lv[old]);
+          const double *col = At + j * m;
+          for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
+          if (tid == 0) {
+            cidx[j] = nl;
+            set_deltas(j, nl);
+          }
+          bump_known(nt);
+          changed = true;
+          p = j + 1;
+        } else {
+          mv_ref += __popc(vlo) + __popc(vhi);
+          p += wc;
+        }
+      }
+      if (!changed) break;
+    }
+  }
+
+  // ------------------------------------------------------ find_candidates
+  // Top-k_eps rows of |s| by (value desc, index asc) (localsearch.py:140):
+  // 8-pass radix select of the k-th key, then ties resolved by index.  Only
+  // the SET matters (the filter is an AND over rows); it is then ordered by
+  // key so the tightest rows reject first.  Rows with s = 0 are dropped
+  // (localsearch.py:151).  Returns the number of filter rows.
+  __device__ int select_rows() {
+    const int64_t kk = this->kk;
+    __syncthreads();
+    if (tid == 0) sh->counter = 0;
+    __syncthreads();
+    uint64_t T = 0;
+    int64_t need = 0;
+    if (kk < m) {
+      uint64_t prefix = 0;
+      int64_t remaining = kk;
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int e = tid; e < 256; e += NT) sh->hist[e] = 0;
+        __syncthreads();
+        const uint64_t hm = shift == 56 ? 0ull : (~0ull << (shift + 8));
+        for (int64_t i = tid; i < m; i += NT) {
+          uint64_t key = abs_key(cr[i]);
+          if ((key & hm) == prefix) atomicAdd(&sh->hist[(key >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int64_t cum = 0;
+          int d = 255;
+          for (; d >= 0; --d) {
+            if (cum + sh->hist[d] >= remaining) break;
+            cum += sh->hist[d];
+          }
+          sh->bc_i[0] = d;
+          sh->bc_i[1] = (int)cum;
+        }
+        __syncthreads();
+        prefix |= (uint64_t)sh->bc_i[0] << shift;
+        remaining -= sh->bc_i[1];
+      }
+      T = prefix;
+      need = remaining;
+    }
+    // keys strictly above T (all rows when kk >= m), unordered
+    for (int64_t i = tid; i < m; i += NT) {
+      uint64_t key = abs_key(cr[i]);
+      if (key > T || (kk >= m && key > 0)) {
+        int pos = atomicAdd(&sh->counter, 1);
+        rows[pos] = (int32_t)i;
+      }
+    }
+    __syncthreads();
+    int cnt = sh->counter;
+    __syncthreads();
+    if (kk < m && T > 0 && need > 0) {
+      int64_t base = 0;
+      for (int64_t c0 = 0; c0 < m && base < need; c0 += NT) {
+        const int64_t i = c0 + tid;
+        const bool f = i < m && abs_key(cr[i]) == T;
+        const unsigned bal = __ballot_sync(AMVM_FULL, f);
+        if (lane == 0) sh->wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int k = 0; k < NW; ++k) {
+          if (k < warp) before += sh->wcnt[k];
+          tot += sh->wcnt[k];
+        }
+        const int64_t pos = base + before + __popc(bal & ((1u << lane) - 1u));
+        if (f && pos < need) rows[cnt + pos] = (int32_t)i;
+        base += tot;
+        __syncthreads();
+      }
+      cnt += (int)need;
+    }
+    // order by (|s| desc, index asc) when small (speed only), then eps/sign
+    if (cnt <= 2048) {
+      for (int q = tid; q < cnt; q += NT) ibuf[q] = rows[q];
+      __syncthreads();
+      for (int q = tid; q < cnt; q += NT) {
+        const int32_t rq = ibuf[q];
+        const uint64_t kq = abs_key(cr[rq]);
+        int rank = 0;
+        for (int o = 0; o < cnt; ++o) {
+          const int32_t ro = ibuf[o];
+          const uint64_t ko = abs_key(cr[ro]);
+          rank += (ko > kq) || (ko == kq && ro < rq);
+        }
+        rows[rank] = rq;
+      }
+      __syncthreads();
+    }
+    for (int q = tid; q < cnt; q += NT) {
+      const double s = cr[rows[q]];
+      reps[q] = dsub(cobj, fabs(s));
+      rsgn[q] = s > 0.0;
+    }
+    __syncthreads();
+    return cnt;
+  }
+
+  __device__ static bool cand_less(const Cand &a, const Cand &b) {
+    if (a.d != b.d) return a.d > b.d;
+    if (a.i != b.i) return a.i < b.i;
+    return a.j < b.j;
+  }
+
+  // Block bitonic sort of cbuf[0..cnt) into (-delta, i, j) order.
+  __device__ void sort_cands(int cnt) {
+    int n2 = 1;
+    while (n2 < cnt) n2 <<= 1;
+    for (int e = cnt + tid; e < n2; e += NT) cbuf[e] = Cand{0x7fffffff, 0x7fffffff, -1.0};
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1) {
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        for (int e = tid; e < n2; e += NT) {
+          const int x = e ^ jj;
+          if (x > e) {
+            Cand A = cbuf[e], Bc = cbuf[x];
+            const bool up = (e & k) == 0;
+            if (up ? cand_less(Bc, A) : cand_less(A, Bc)) {
+              cbuf[e] = Bc;
+              cbuf[x] = A;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // find_candidates, localsearch.py:128-169.  Pairs (i, j) with x_i > x_j
+  // (levels are strictly increasing, so idx_i > idx_j) that pass the
+  // one-sided interval test on every selected row.  Returns the count kept
+  // (truncated to max_candidates in (-delta, i, j) order); when
+  // `always_sort`, the kept list is in that order even if not truncated.
+  __device__ int find_candidates(bool always_sort) {
+    const int nr = select_rows();
+    const int g = nr < kG ? nr : kG;
+    for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
+      const int64_t q = e / n, j = e - q * n;
+      ag[e] = __ldg(At + j * m + rows[q]);
+    }
+    if (tab) {
+      for (int e = tid; e < g * nlev * nlev; e += NT) {
+        const int q = e / (int)(nlev * nlev), rem2 = e - q * (int)(nlev * nlev);
+        const int ki = rem2 / (int)nlev, kj = rem2 - ki * (int)nlev;
+        btab[e] = ki > kj ? ddiv(reps[q], dsub(lv[ki], lv[kj])) : 0.0;
+      }
+    }
+    if (tid == 0) sh->counter = 0;
+    __syncthreads();
+    for (int64_t i = warp; i < n; i += NW) {
+      const int ki = cidx[i];
+      if (ki == 0) continue;
+      const double xi = lv[ki];
+      double ai[kG];
+#pragma unroll
+      for (int q = 0; q < kG; ++q) ai[q] = q < g ? ag[q * n + i] : 0.0;
+      for (int64_t jb = 0; jb < n; jb += 32) {
+        const int64_t j = jb + lane;
+        bool alive = false;
+        double delta = 0.0;
+        if (j < n) {
+          const int kj = cidx[j];
+          if (kj < ki) {
+            delta = dsub(xi, lv[kj]);
+            alive = true;
+            for (int q = 0; q < nr && alive; ++q) {
+              double da, bound;
+              if (q < g) {
+                da = dsub(ag[q * n + j], ai[q]);
+                bound = tab ? btab[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta);
+              } else {
+                const int64_t rq = rows[q];
+                da = dsub(__ldg(At + j * m + rq), __ldg(At + i * m + rq));
+                bound = ddiv(reps[q], delta);
+              }
+              alive = rsgn[q] ? (da < bound) : (da > -bound);
+            }
+          }
+        }
+        const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+        if (bal) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&sh->counter, __popc(bal));
+          base = __shfl_sync(AMVM_FULL, base, 0);
+          if (alive) {
+            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+            if (pos < cap) cbuf[pos] = Cand{(int32_t)i, (int32_t)j, delta};
+          }
+        }
+      }
+    }
+    __syncthreads();
+    int cnt = sh->counter;
+    __syncthreads();
+    if (cnt > cap) {
+      fail(AMVM_ERR_UNSUPPORTED);  // survivor buffer too small
+      cnt = (int)cap;
+    }
+    const int maxc = prm->max_candidates;
+    if ((maxc > 0 && cnt > maxc) || (always_sort && cnt > 1)) {
+      sort_cands(cnt);
+      if (maxc > 0 && cnt > maxc) cnt = maxc;
+    }
+    return cnt;
+  }
+
+  // best_swap + _evaluate_chunk, localsearch.py:181-246: lowest post-swap
+  // objective among strictly improving candidates, ties to the smallest
+  // (i, j).  Returns found; the winner is uniform across the CTA.
+  __device__ bool best_swap(int &bi, int &bj, double &bd, double &bt) {
+    if (!(cobj > 0.0)) return false;
+    const int cnt = find_candidates(false);
+    if (cnt == 0) return false;
+    double wt = 0.0, wd = 0.0;
+    int wi = -1, wj = -1;
+    const double t0 = cobj;
+    for (int c = warp; c < cnt; c += NW) {
+      const Cand e = cbuf[c];
+      const double *ci = At + (int64_t)e.i * m;
+      const double *cj = At + (int64_t)e.j * m;
+      double mx = 0.0;
+      int it = 0;
+      for (int64_t r = lane; r < m; r += 32) {
+        const double y = dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r))));
+        mx = fmax(mx, fabs(y));
+        if ((++it & 15) == 0 && __any_sync(AMVM_FULL, mx >= t0)) break;
+      }
+      mx = warp_max(mx);
+      if (mx < t0 && (wi < 0 || mx < wt || (mx == wt && (e.i < wi || (e.i == wi && e.j < wj))))) {
+        wt = mx; wi = e.i; wj = e.j; wd = e.d;
+      }
+    }
+    mv_ref += cnt;
+    mv_raw += cnt;
+    if (lane == 0) {
+      sh->red[0][warp][0] = wt;
+      sh->red[0][warp][1] = wd;
+      sh->red[0][warp][2] = __longlong_as_double(((int64_t)wi << 32) | (uint32_t)wj);
+    }
+    __syncthreads();
+    bool found = false;
+    for (int k = 0; k < NW; ++k) {
+      const int64_t ij = __double_as_longlong(sh->red[0][k][2]);
+      const int ki = (int)(ij >> 32), kj = (int)(uint32_t)ij;
+      if (ki < 0) continue;
+      const double kt = sh->red[0][k][0];
+      if (!found || kt < bt || (kt == bt && (ki < bi || (ki == bi && kj < bj)))) {
+        found = true; bt = kt; bi = ki; bj = kj; bd = sh->red[0][k][1];
+      }
+    }
+    __syncthreads();
+    return found;
+  }
+
+  // apply_swap, core.py:228-245, with the objective predicted by best_swap.
+  __device__ void apply_swap_known(int i, int j, double d, double t) {
+    const double *ci = At + (int64_t)i * m;
+    const double *cj = At + (int64_t)j * m;
+    for (int64_t r = tid; r < m; r += NT) cr[r] = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
+    if (tid == 0) {
+      const int32_t t0 = cidx[i];
+      cidx[i] = cidx[j];
+      cidx[j] = t0;
+    }
+    bump_known(t);
+  }
+
+  // local_search, localsearch.py:249-269
+  __device__ void local_search() {
+    one_opt();
+    for (int rd = 0; rd < prm->ls_max_rounds; ++rd) {
+      int bi = -1, bj = -1;
+      double bd = 0, bt = 0;
+      if (!best_swap(bi, bj, bd, bt)) break;
+      apply_swap_known(bi, bj, bd, bt);
+      one_opt();
+    }
+    __syncthreads();
+  }
+
+  // -------------------------------------------------------- impact scores
+  // impact_scores, operators.py:54-74: d_j = sum_k |s_k| exp((-a (t-|s_k|))/|a_kj|)
+  // summed over k in row order (numpy axis-0), / pairwise sum |s|.  Terms are
+  // computed by the whole CTA into an smem tile, then each column's owner
+  // adds its tile column sequentially.
+  __device__ void impact_scores(double alpha) {
+    __syncthreads();
+    const double t = cobj;
+    const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
+    const double na = -alpha;
+    for (int64_t cb = 0; cb < n; cb += kTC) {
+      const int cols = (int)(n - cb < kTC ? n - cb : kTC);
+      double acc = 0.0;
+      for (int64_t kb = 0; kb < m; kb += kTK) {
+        const int rws = (int)(m - kb < kTK ? m - kb : kTK);
+        for (int e = tid; e < kTC * kTK; e += NT) {
+          const int c = e / kTK, k = e - c * kTK;
+          if (c < cols && k < rws) {
+            const double a = fabs(__ldg(At + (cb + c) * m + kb + k));
+            const double s = fabs(cr[kb + k]);
+            double term = 0.0;
+            if (a > 0.0) term = dmul(s, exp(ddiv(dmul(na, dsub(t, s)), a)));
+            tile[c * (kTK + 1) + k] = term;
+          }
+        }
+        __syncthreads();
+        if (tid < cols)
+          for (int k = 0; k < rws; ++k) acc = dadd(acc, tile[tid * (kTK + 1) + k]);
+        __syncthreads();
+      }
+      if (tid < cols) dbuf[cb + tid] = ddiv(acc, tot);
+    }
+    __syncthreads();
+  }
+
+  // ------------------------------------------------------------- destroy
+  // Generator.choice(pop, r, replace=False) on thread 0 -> out[0..r).
+  __device__ void choice_noreplace(Pcg &g, int64_t pop, int64_t r, int32_t *out) {
+    if (pop > 10000 && r > pop / 50) {  // numpy tail-shuffle path
+      for (int64_t i = 0; i < pop; ++i) ibuf[i] = (int32_t)i;
+      const int64_t first = pop - r > 1 ? pop - r : 1;
+      for (int64_t i = pop - 1; i >= first; --i) {
+        const int64_t jj = (int64_t)pcg_bounded(g, (uint64_t)i);
+        const int32_t t0 = ibuf[i];
+        ibuf[i] = ibuf[jj];
+        ibuf[jj] = t0;
+      }
+      for (int64_t q = 0; q < r; ++q) out[q] = ibuf[pop - r + q];
+      return;
+    }
+    const uint64_t mask = gen_mask((uint64_t)(1.2 * (double)r));
+    for (uint64_t k = 0; k <= mask; ++k) hset[k] = ~0ull;
+    for (int64_t j = pop - r; j < pop; ++j) {
+      const uint64_t val = pcg_bounded(g, (uint64_t)j);
+      uint64_t loc = val & mask;
+      while (hset[loc] != ~0ull && hset[loc] != val) loc = (loc + 1) & mask;
+      if (hset[loc] == ~0ull) {
+        hset[loc] = val;
+        out[j - pop + r] = (int32_t)val;
+      } else {
+        loc = (uint64_t)j & mask;
+        while (hset[loc] != ~0ull) loc = (loc + 1) & mask;
+        hset[loc] = (uint64_t)j;
+        out[j - pop + r] = (int32_t)j;
+      }
+    }
+    for (int64_t i = r - 1; i >= 1; --i) {
+      const int64_t jj = (int64_t)pcg_bounded(g, (uint64_t)i);
+      const int32_t t0 = out[i];
+      out[i] = out[jj];
+      out[jj] = t0;
+    }
+  }
+
+  __device__ static void isort(int32_t *a, int64_t r) {
+    for (int64_t i = 1; i < r; ++i) {
+      const int32_t v = a[i];
+      int64_t k = i - 1;
+      while (k >= 0 && a[k] > v) {
+        a[k + 1] = a[k];
+        --k;
+      }
+      a[k + 1] = v;
+    }
+  }
+
+  // removed = sort(picked), saved = idx[removed]   (operators.py:29-31)
+  __device__ void finish_destroy(int64_t r) {
+    if (tid == 0) {
+      isort(pick, r);
+      for (int64_t q = 0; q < r; ++q) {
+        rem[q] = pick[q];
+        sav[q] = cidx[pick[q]];
+      }
+    }
+    __syncthreads();
+  }
+
+  // random_destroy, operators.py:34-39
+  __device__ void random_destroy(int64_t r) {
+    __syncthreads();
+    if (tid == 0) choice_noreplace(sh->rng, n, r, pick);
+    finish_destroy(r);
+  }
+
+  // worst_remove_destroy, operators.py:77-105
+  __device__ void worst_destroy(int64_t r, double alpha) {
+    if (!(cobj > 0.0)) {
+      random_destroy(r);
+      return;
+    }
+    impact_scores(alpha);
+    auto gd = [&](int64_t k) { return dbuf[k]; };
+    if (block_pairwise(gd, n, lf_lo + nleaf_m, lf_len + nleaf_m, nleaf_n) <= 0.0) {
+      random_destroy(r);
+      return;
+    }
+    for (int64_t q = 0; q < r; ++q) {
+      const double total = block_pairwise(gd, n, lf_lo + nleaf_m, lf_len + nleaf_m, nleaf_n);
+      if (!(total > 0.0)) {
+        // mass exhausted: rng.choice(setdiff1d(arange(n), picked), r - q, False)
+        if (tid == 0) {
+          for (int64_t k = 0; k < n; ++k) ibuf[k] = 0;
+          for (int64_t k = 0; k < q; ++k) ibuf[pick[k]] = 1;
+          int32_t *rest = (int32_t *)pbuf;  // n int32 fit in n doubles
+          int64_t nrest = 0;
+          for (int64_t k = 0; k < n; ++k)
+            if (!ibuf[k]) rest[nrest++] = (int32_t)k;
+          choice_noreplace(sh->rng, nrest, r - q, pick + q);
+          for (int64_t k = q; k < r; ++k) pick[k] = rest[pick[k]];
+        }
+        break;
+      }
+      for (int64_t k = tid; k < n; k += NT) pbuf[k] = ddiv(dbuf[k], total);
+      __syncthreads();
+      if (tid == 0) {
+        // Generator.choice(n, p): cdf = cumsum(p); cdf /= cdf[-1];
+        // searchsorted(cdf, random(), 'right')
+        double acc = 0.0;
+        for (int64_t k = 0; k < n; ++k) {
+          acc = dadd(acc, pbuf[k]);
+          pbuf[k] = acc;
+        }
+        const double last = pbuf[n - 1];
+        const double u = pcg_random(sh->rng);
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+          const int64_t mid = lo + ((hi - lo) >> 1);
+          if (u < ddiv(pbuf[mid], last)) hi = mid;
+          else lo = mid + 1;
+        }
+        pick[q] = (int32_t)lo;
+        dbuf[lo] = 0.0;
+      }
+      __syncthreads();
+    }
+    finish_destroy(r);
+  }
+
+  // ------------------------------------------------------------- repairs
+  // two_nearest, core.py:62-72: first two of a stable argsort of |lv - v|.
+  // Every warp scans redundantly, so the result is uniform without a barrier.
+  __device__ void two_nearest(double v, int &c1, int &c2) {
+    double bd = 0;
+    int bk = 0x7fffffff;
+    for (int k = lane; k < nlev; k += 32) {
+      const double dk = fabs(dsub(lv[k], v));
+      if (bk == 0x7fffffff || dk < bd) { bd = dk; bk = k; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double od = __shfl_xor_sync(AMVM_FULL, bd, o);
+      const int ok = __shfl_xor_sync(AMVM_FULL, bk, o);
+      if (ok != 0x7fffffff && (bk == 0x7fffffff || od < bd || (od == bd && ok < bk))) { bd = od; bk = ok; }
+    }
+    c1 = bk;
+    bk = 0x7fffffff;
+    for (int k = lane; k < nlev; k += 32) {
+      if (k == c1) continue;
+      const double dk = fabs(dsub(lv[k], v));
+      if (bk == 0x7fffffff || dk < bd) { bd = dk; bk = k; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double od = __shfl_xor_sync(AMVM_FULL, bd, o);
+      const int ok = __shfl_xor_sync(AMVM_FULL, bk, o);
+      if (ok != 0x7fffffff && (bk == 0x7fffffff || od < bd || (od == bd && ok < bk))) { bd = od; bk = ok; }
+    }
+    c2 = bk;
+  }
+
+  // random_repair, operators.py:108-117 (all r coins drawn up front: they are
+  // consecutive in the stream — nothing else draws during a repair).
+  __device__ void random_repair(const int32_t *rm, const int32_t *sv, int64_t r) {
+    __syncthreads();
+    if (tid == 0)
+      for (int64_t q = 0; q < r; ++q) coin[q] = (int32_t)pcg_bounded(sh->rng, 1);
+    __syncthreads();
+    for (int64_t q = 0; q < r; ++q) {
+      int c1, c2;
+      two_nearest(lv[sv[q]], c1, c2);
+      apply_shift_reduce(rm[q], coin[q] ? c2 : c1);
+    }
+  }
+
+  // greedy_repair, operators.py:120-138: the exact in-place sequence.
+  __device__ void greedy_repair(const int32_t *rm, const int32_t *sv, int64_t r) {
+    __syncthreads();
+    for (int64_t q = 0; q < r; ++q) {
+      const int64_t j = rm[q];
+      int c1, c2;
+      two_nearest(lv[sv[q]], c1, c2);
+      apply_shift_reduce(j, c1);
+      const double t1 = cobj;
+      apply_shift_reduce(j, c2);
+      const double t2 = cobj;
+      mv_ref += 2;
+      mv_raw += 2;
+      if (t1 < t2 || (t1 == t2 && lv[c1] < lv[c2])) apply_shift_reduce(j, c1);
+    }
+  }
+
+  // ------------------------------------------------------------ controller
+  // accept, controller.py:168-183 (np.linalg.norm = sqrt of OpenBLAS ddot)
+  __device__ bool accept() {
+    if (cobj < uobj) return true;
+    if (prm->l2_tiebreak && cobj <= dadd(uobj, prm->accept_tie_tol)) {
+      __syncthreads();
+      if (warp < 2) {
+        const double *x = warp == 0 ? cr : ur;
+        const double dd = warp_ddot_skx([&](int64_t i) { return x[i]; }, [&](int64_t i) { return x[i]; }, m, lane);
+        if (lane == 0) sh->bc_d[warp] = __dsqrt_rn(dd);
+      }
+      __syncthreads();
+      const bool ok = sh->bc_d[0] < sh->bc_d[1];
+      __syncthreads();
+      return ok;
+    }
+    return false;
+  }
+
+  // select_operators, controller.py:88-90 (thread 0)
+  __device__ int select_pair() {
+    double s = 0.0;
+    for (int k = 0; k < 4; ++k) s = dadd(s, w[k]);  // pairwise_sum, n < 8
+    double cdf[4], acc = 0.0;
+    for (int k = 0; k < 4; ++k) {
+      acc = dadd(acc, ddiv(w[k], s));
+      cdf[k] = acc;
+    }
+    const double u = pcg_random(sh->rng);
+    int lo = 0, hi = 4;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (u < ddiv(cdf[mid], cdf[3])) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  }
+
+  // update_weights, controller.py:99-131 (replicated in every thread)
+  __device__ void update_weights(int pair, int outcome) {
+    const double pts = outcome == 0 ? prm->sigma1 : outcome == 1 ? prm->sigma2 : outcome == 2 ? prm->sigma3 : 0.0;
+    sc[pair] = dadd(sc[pair], pts);
+    seg[pair] += 1;
+    life[pair] += 1;
+    bit += 1;
+    if (bit % prm->n_segment == 0) {
+      const double keep = dsub(1.0, prm->decay);
+      for (int k = 0; k < 4; ++k) {
+        const double nrm = seg[k] > 0 ? ddiv(sc[k], (double)seg[k]) : 0.0;
+        const double v = dadd(dmul(prm->decay, w[k]), dmul(keep, nrm));
+        w[k] = v < prm->weight_floor ? prm->weight_floor : v;
+        sc[k] = 0.0;
+        seg[k] = 0;
+      }
+    }
+  }
+
+  __device__ void cand_from_cur() {
+    for (int64_t i = tid; i < m; i += NT) cr[i] = ur[i];
+    for (int64_t j = tid; j < n; j += NT) cidx[j] = uidx[j];
+    cobj = uobj;
+    ccnt = ucnt;
+    __syncthreads();
+  }
+
+  __device__ void cur_from_cand() {
+    for (int64_t i = tid; i < m; i += NT) ur[i] = cr[i];
+    for (int64_t j = tid; j < n; j += NT) uidx[j] = cidx[j];
+    uobj = cobj;
+    ucnt = ccnt;
+  }
+
+  __device__ void write_best(int64_t inst, const amvm_result &res) {
+    double *br = res.best.residual + inst * m;
+    int32_t *bi = res.best.idx + inst * n;
+    for (int64_t i = tid; i < m; i += NT) br[i] = ur[i];
+    for (int64_t j = tid; j < n; j += NT) bi[j] = uidx[j];
+    bobj = uobj;
+    bcnt = ucnt;
+  }
+
+  __device__ static uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  }
+
+  // ------------------------------------------------------------- set-up
+  __device__ void bind(const KArgs &a, unsigned char *smem, int slot) {
+    tid = threadIdx.x;
+    lane = tid & 31;
+    warp = tid >> 5;
+    m = a.m;
+    n = a.n;
+    nlev = a.nlev;
+    At = a.At;
+    prm = &a.prm;
+    cap = a.cap;
+    tab = a.tab;
+    const SlotLayout L = slot_layout(m, n, a.prm.k_eps, a.prm.r, a.cap);
+    kk = L.kk;
+    unsigned char *base = a.ws + sizeof(WsHeader) + (size_t)slot * a.slot_bytes;
+    status = (int32_t *)a.ws;
+    ur = (double *)(base + L.ur);
+    uidx = (int32_t *)(base + L.uidx);
+    cidx = (int32_t *)(base + L.cidx);
+    dmv = (double *)(base + L.dmv);
+    dpv = (double *)(base + L.dpv);
+    dbuf = (double *)(base + L.dbuf);
+    pbuf = (double *)(base + L.pbuf);
+    lf_lo = (int64_t *)(base + L.lf_lo);
+    lf_len = (int64_t *)(base + L.lf_len);
+    lf_sum = (double *)(base + L.lf_sum);
+    rows = (int32_t *)(base + L.rows);
+    reps = (double *)(base + L.reps);
+    rsgn = (int32_t *)(base + L.rsgn);
+    ag = (double *)(base + L.ag);
+    cbuf = (Cand *)(base + L.cbuf);
+    hset = (uint64_t *)(base + L.hset);
+    rem = (int32_t *)(base + L.rem);
+    sav = (int32_t *)(base + L.sav);
+    pick = (int32_t *)(base + L.pick);
+    coin = (int32_t *)(base + L.coin);
+    ibuf = (int32_t *)(base + L.ibuf);
+    // dynamic smem: Shared | lv | tile | btab | cr
+    size_t o = sizeof(Shared<NT>);
+    sh = (Shared<NT> *)smem;
+    lv = (double *)(smem + o);
+    o += 8 * ((nlev + 1) & ~1);
+    tile = (double *)(smem + o);
+    o += 8 * kTC * (kTK + 1);
+    btab = (double *)(smem + o);
+    if (tab) o += 8 * kG * nlev * nlev;
+    cr = a.cr_smem ? (double *)(smem + o) : (double *)(base + L.crg);
+    // leaf trees for m and n (fixed per problem)
+    if (tid == 0) {
+      nleaf_m = pw_leaves(m, lf_lo, lf_len, (int)L.nleaf);
+      sh->bc_i[2] = nleaf_m;
+      sh->bc_i[3] = pw_leaves(n, lf_lo + nleaf_m, lf_len + nleaf_m, (int)(2 * L.nleaf - nleaf_m));
+    }
+    __syncthreads();
+    nleaf_m = sh->bc_i[2];
+    nleaf_n = sh->bc_i[3];
+    __syncthreads();
+  }
+
+  __device__ void load_levels(const KArgs &a, int64_t inst) {
+    b = a.B + inst * m;
+    for (int64_t k = tid; k < nlev; k += NT) lv[k] = a.levels[inst * nlev + k];
+    __syncthreads();
+  }
+
+  __device__ void load_rng(const amvm_pcg64 *st) {
+    if (tid == 0) {
+      sh->rng.s = ((unsigned __int128)st->state_hi << 64) | st->state_lo;
+      sh->rng.inc = ((unsigned __int128)st->inc_hi << 64) | st->inc_lo;
+      sh->rng.has32 = st->has_uint32;
+      sh->rng.u32 = st->uinteger;
+    }
+  }
+
+  __device__ void store_rng(amvm_pcg64 *st) {
+    if (tid == 0) {
+      st->state_hi = (uint64_t)(sh->rng.s >> 64);
+      st->state_lo = (uint64_t)sh->rng.s;
+      st->inc_hi = (uint64_t)(sh->rng.inc >> 64);
+      st->inc_lo = (uint64_t)sh->rng.inc;
+      st->has_uint32 = sh->rng.has32;
+      st->uinteger = sh->rng.u32;
+    }
+  }
+
+  // ------------------------------------------------------- solve (one inst)
+  // solve, controller.py:211-286, from the host-computed initial solution.
+  __device__ void solve_instance(const KArgs &a, int64_t inst) {
+    load_levels(a, inst);
+    const amvm_result &res = a.res;
+    for (int64_t i = tid; i < m; i += NT) ur[i] = a.s_r[inst * m + i];
+    for (int64_t j = tid; j < n; j += NT) uidx[j] = a.s_idx[inst * n + j];
+    uobj = a.s_obj[inst];
+    ucnt = a.s_cnt[inst];
+    __syncthreads();
+    write_best(inst, res);
+    load_rng(&a.rng[inst]);
+    for (int k = 0; k < 4; ++k) {
+      w[k] = 1.0; sc[k] = 0.0; seg[k] = 0; life[k] = 0;
+    }
+    bit = 0;
+    mv_ref = mv_raw = 0;
+    const int64_t r = a.prm.r;
+    const int T = a.prm.max_iters;
+    const uint64_t t_start = gtimer();
+    bool cand_is_cur = false;
+    int it = 0;
+    while (it < T) {
+      if (bobj == 0.0) break;
+      if (tid == 0) {
+        int stop = 0;
+        if (a.time_budget_ns >= 0 && (int64_t)(gtimer() - t_start) > a.time_budget_ns) stop = 1;
+        sh->bc_i[0] = stop;
+        sh->bc_i[1] = stop ? 0 : select_pair();
+      }
+      __syncthreads();
+      const int stop = sh->bc_i[0], pair = sh->bc_i[1];
+      __syncthreads();
+      if (stop) break;
+      ++it;
+      if (!cand_is_cur) cand_from_cur();
+      cand_is_cur = false;
+      if (pair < 2) random_destroy(r);
+      else worst_destroy(r, a.prm.alpha);
+      if (pair & 1) greedy_repair(rem, sav, r);
+      else random_repair(rem, sav, r);
+      local_search();
+      const bool acc = accept();
+      int outcome;
+      if (acc && cobj < bobj) outcome = 0;
+      else if (acc && cobj < uobj) outcome = 1;
+      else if (acc) outcome = 2;
+      else outcome = 3;
+      if (acc) {
+        cur_from_cand();
+        cand_is_cur = true;
+        __syncthreads();
+        if (uobj < bobj) write_best(inst, res);
+      }
+      update_weights(pair, outcome);
+      if (tid == 0 && res.trace_current_t) {
+        const int64_t o = inst * (int64_t)T + it - 1;
+        res.trace_current_t[o] = uobj;
+        res.trace_best_t[o] = bobj;
+        res.trace_pair[o] = (uint8_t)pair;
+        res.trace_accepted[o] = (uint8_t)acc;
+      }
+    }
+    if (tid == 0) {
+      res.best.objective[inst] = bobj;
+      res.best.updates[inst] = bcnt;
+      res.initial_objective[inst] = a.s_obj[inst];
+      res.iterations[inst] = it;
+      for (int k = 0; k < 4; ++k) res.operator_uses[inst * 4 + k] = life[k];
+      if (res.moves_scored) {
+        res.moves_scored[2 * inst] = mv_ref;
+        res.moves_scored[2 * inst + 1] = mv_raw;
+      }
+    }
+    store_rng(&a.rng[inst]);
+    __syncthreads();
+  }
+
+  // ------------------------------------------------- component operations
+  __device__ void load_sol(const KArgs &a) {
+    load_levels(a, 0);
+    for (int64_t i = tid; i < m; i += NT) cr[i] = a.s_r[i];
+    for (int64_t j = tid; j < n; j += NT) cidx[j] = a.s_idx[j];
+    cobj = a.s_obj[0];
+    ccnt = a.s_cnt[0];
+    mv_ref = mv_raw = 0;
+    __syncthreads();
+  }
+
+  __device__ void store_sol(const KArgs &a) {
+    __syncthreads();
+    for (int64_t i = tid; i < m; i += NT) a.s_r[i] = cr[i];
+    for (int64_t j = tid; j < n; j += NT) a.s_idx[j] = cidx[j];
+    if (tid == 0) {
+      a.s_obj[0] = cobj;
+      a.s_cnt[0] = ccnt;
+    }
+  }
+
+  __device__ void run_op(const KArgs &a) {
+    load_sol(a);
+    switch (a.op) {
+      case OP_ONE_OPT:
+        one_opt();
+        store_sol(a);
+        break;
+      case OP_LOCAL_SEARCH:
+        local_search();
+        store_sol(a);
+        break;
+      case OP_FIND_CAND: {
+        const int cnt = cobj > 0.0 ? find_candidates(true) : 0;
+        const int k = cnt < a.x_cap ? cnt : a.x_cap;
+        for (int q = tid; q < k; q += NT) {
+          a.x_i[q] = cbuf[q].i;
+          a.x_j[q] = cbuf[q].j;
+          a.x_d[q] = cbuf[q].d;
+        }
+        if (tid == 0) *a.x_cnt = k;
+        break;
+      }
+      case OP_BEST_SWAP: {
+        int bi = -1, bj = -1;
+        double bd = 0, bt = 0;
+        const bool f = best_swap(bi, bj, bd, bt);
+        if (tid == 0) {
+          a.x_out4[0] = f ? bi : -1;
+          a.x_out4[1] = f ? bj : -1;
+          a.x_out4[2] = f ? bd : 0.0;
+          a.x_out4[3] = f ? bt : 0.0;
+        }
+        break;
+      }
+      case OP_IMPACT:
+        impact_scores(a.prm.alpha);
+        for (int64_t j = tid; j < n; j += NT) a.x_d[j] = dbuf[j];
+        break;
+      case OP_DESTROY:
+        load_rng(a.rng);
+        if (a.kind == 0) random_destroy(a.prm.r);
+        else worst_destroy(a.prm.r, a.prm.alpha);
+        for (int64_t q = tid; q < a.prm.r; q += NT) a.x_i[q] = rem[q];
+        store_rng(a.rng);
+        break;
+      case OP_REPAIR:
+        load_rng(a.rng);
+        if (a.kind == 0) random_repair(a.x_i, a.x_saved, a.x_r);
+        else greedy_repair(a.x_i, a.x_saved, a.x_r);
+        store_rng(a.rng);
+        store_sol(a);
+        break;
+      default:
+        fail(AMVM_ERR_INVALID);
+    }
+  }
+};
+
+}  // namespace amvm
