@@ -172,6 +172,21 @@ AMVM_API int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int k
 AMVM_API int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol,
                           void *stream);
 
+/* PTQ front end for one layer sharing X (= A, m calibration rows x n inputs;
+ * builders.py:355-372 semantics with a shared X, controller.py:157-165):
+ * for each weight row k of W (count x n, device), levels[k] = numpy
+ * linspace(min w_k, max w_k, nlev) (range widened by 0.5 when it collapses),
+ * idx[k] = nearest level of w_k (ties to the lower level), B[k] = X @ w_k in
+ * numpy's BLAS order.  Follow with amvm_compute_residual for the start.    */
+AMVM_API int amvm_ptq_prepare(int64_t m, int64_t n, int64_t count, int64_t nlev,
+                              const double *At, const double *W, double *B,
+                              double *levels, int32_t *idx, void *stream);
+
+/* HOST helper: numpy default_rng(seed).bit_generator.state for each seed
+ * (SeedSequence -> PCG64), so per-instance seeds need no Python loop.      */
+AMVM_API int amvm_seed_pcg64(const uint64_t *seeds_host, int64_t count,
+                             amvm_pcg64 *out_host);
+
 /* Waits for `stream`, then returns the device-side status the last call on
  * this workspace left in its header (AMVM_OK, or e.g. AMVM_ERR_UNSUPPORTED
  * when a swap-candidate buffer overflowed).                                 */

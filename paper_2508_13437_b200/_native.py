@@ -21,7 +21,8 @@ AMVM_ERR_INVALID = -1
 EXPORTS = (
     "amvm_workspace_bytes", "amvm_solve", "amvm_one_opt", "amvm_local_search",
     "amvm_find_candidates", "amvm_best_swap", "amvm_impact_scores", "amvm_destroy",
-    "amvm_repair", "amvm_compute_residual", "amvm_status", "amvm_strerror", "amvm_abi_version",
+    "amvm_repair", "amvm_compute_residual", "amvm_ptq_prepare", "amvm_seed_pcg64", "amvm_status",
+    "amvm_strerror", "amvm_abi_version",
 )
 
 
@@ -88,6 +89,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_destroy.argtypes = [vp, vp, C.c_int, vp, vp, vp, vp, sz, vp]
     lib.amvm_repair.argtypes = [vp, vp, C.c_int, vp, vp, vp, vp, i32, vp, sz, vp]
     lib.amvm_compute_residual.argtypes = [vp, vp, vp]
+    lib.amvm_ptq_prepare.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]
+    lib.amvm_seed_pcg64.argtypes = [vp, i64, vp]
     lib.amvm_status.argtypes = [vp, vp]
     lib.amvm_strerror.restype = C.c_char_p
     lib.amvm_strerror.argtypes = [C.c_int]
@@ -142,6 +145,16 @@ def pcg_to_state(g) -> dict:
 
 PCG_DTYPE = np.dtype([("state_hi", "<u8"), ("state_lo", "<u8"), ("inc_hi", "<u8"),
                       ("inc_lo", "<u8"), ("has_uint32", "<u4"), ("uinteger", "<u4")])
+
+
+def seed_states(seeds) -> np.ndarray:
+    """numpy default_rng(seed) PCG64 states for many int seeds (host, in libamvm)."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = np.zeros(seeds.size, PCG_DTYPE)
+    rc = load_library().amvm_seed_pcg64(C.c_void_p(seeds.ctypes.data), seeds.size,
+                                        C.c_void_p(out.ctypes.data))
+    check(rc, "amvm_seed_pcg64")
+    return out
 
 
 def pcg_array(states: list[dict]) -> np.ndarray:

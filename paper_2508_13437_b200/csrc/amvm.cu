@@ -49,10 +49,13 @@ __global__ void __launch_bounds__(NT) k_op(KArgs a) {
 constexpr int kRI = 8;
 constexpr int kRJ = 256;
 
+// x_k = levels_k[idx_k] (compute_residual) or, when Xd != nullptr, the dense
+// row Xd[k] (b = X @ w, builders.py:366); B == nullptr skips the "- b".
 template <int NT>
 __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t nlev, int64_t count,
                                                  const double *__restrict__ At, const double *__restrict__ B,
                                                  const double *__restrict__ levels, const int32_t *__restrict__ idx,
+                                                 const double *__restrict__ Xd,
                                                  double *__restrict__ res, double *__restrict__ obj) {
   __shared__ double xs[kRI][kRJ];
   __shared__ double red[kRI][NT / 32];
@@ -78,7 +81,8 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
         for (int e = tid; e < kRI * kRJ; e += NT) {
           const int q = e / kRJ, jj = e - q * kRJ;
           xs[q][jj] = (q < ni && jj < jn)
-                          ? levels[(k0 + q) * nlev + idx[(k0 + q) * n + j0 + jj]]
+                          ? (Xd ? Xd[(k0 + q) * n + j0 + jj]
+                                : levels[(k0 + q) * nlev + idx[(k0 + q) * n + j0 + jj]])
                           : 0.0;
         }
         __syncthreads();
@@ -108,7 +112,8 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
         for (int q = 0; q < ni; ++q) {
           const double *lvq = levels + (k0 + q) * nlev;
           const int32_t *ix = idx + (k0 + q) * n;
-          auto xv = [&](int64_t j) { return lvq[ix[j]]; };
+          const double *xd = Xd + (k0 + q) * n;
+          auto xv = [&](int64_t j) { return Xd ? xd[j] : lvq[ix[j]]; };
           double v = y[q];
           switch (n & 3) {
             case 1: v = amvm::dfma(At[m1 * m + i], xv(m1), v); break;
@@ -119,7 +124,7 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
               break;
             default: break;
           }
-          v = amvm::dsub(v, B[(k0 + q) * m + i]);
+          if (B) v = amvm::dsub(v, B[(k0 + q) * m + i]);
           res[(k0 + q) * m + i] = v;
           mx[q] = fmax(mx[q], fabs(v));
         }
@@ -130,9 +135,10 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
       for (int q = 0; q < ni; ++q) {
         const double *lvq = levels + (k0 + q) * nlev;
         const int32_t *ix = idx + (k0 + q) * n;
-        double v = gemv_row([&](int64_t j) { return At[j * m + i]; }, [&](int64_t j) { return lvq[ix[j]]; }, n,
-                            gemv_kind(i, m));
-        v = amvm::dsub(v, B[(k0 + q) * m + i]);
+        const double *xd = Xd + (k0 + q) * n;
+        double v = gemv_row([&](int64_t j) { return At[j * m + i]; },
+                            [&](int64_t j) { return Xd ? xd[j] : lvq[ix[j]]; }, n, gemv_kind(i, m));
+        if (B) v = amvm::dsub(v, B[(k0 + q) * m + i]);
         res[(k0 + q) * m + i] = v;
         mx[q] = fmax(mx[q], fabs(v));
       }
@@ -141,8 +147,10 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
     const int q = warp;
     const double *lvq = levels + (k0 + q) * nlev;
     const int32_t *ix = idx + (k0 + q) * n;
-    double v = warp_ddot_skx([&](int64_t j) { return At[j]; }, [&](int64_t j) { return lvq[ix[j]]; }, n, lane);
-    v = amvm::dsub(v, B[k0 + q]);
+    const double *xd = Xd + (k0 + q) * n;
+    double v = warp_ddot_skx([&](int64_t j) { return At[j]; },
+                             [&](int64_t j) { return Xd ? xd[j] : lvq[ix[j]]; }, n, lane);
+    if (B) v = amvm::dsub(v, B[k0 + q]);
     if (lane == 0) res[k0 + q] = v;
     mx[q] = fabs(v);
   }
@@ -152,12 +160,122 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
     if (lane == 0) red[q][warp] = v;
   }
   __syncthreads();
-  if (tid < ni) {
+  if (obj && tid < ni) {
     double v = 0.0;
     for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[tid][w]);
     obj[k0 + tid] = v;
   }
 }
+
+// PTQ row preparation (builders.py:366-371 + controller.py:157-165), one CTA
+// per weight row: lo/hi = min/max w (widened by 0.5 if the range collapses),
+// levels = numpy linspace(lo, hi, L) (k*step + lo, last = hi), idx_j = first
+// argmin_k |w_j - levels_k|.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_ptq_prepare(int64_t n, int64_t nlev, const double *__restrict__ W,
+                                                    double *__restrict__ levels, int32_t *__restrict__ idx) {
+  __shared__ double lo_s[NT / 32], hi_s[NT / 32];
+  __shared__ double lvs[1024];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k = blockIdx.x;
+  const double *w = W + k * n;
+  double lo = w[0], hi = w[0];
+  for (int64_t j = tid; j < n; j += NT) {
+    lo = fmin(lo, w[j]);
+    hi = fmax(hi, w[j]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(AMVM_FULL, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(AMVM_FULL, hi, o));
+  }
+  if (lane == 0) { lo_s[warp] = lo; hi_s[warp] = hi; }
+  __syncthreads();
+  lo = lo_s[0];
+  hi = hi_s[0];
+  for (int q = 1; q < NT / 32; ++q) { lo = fmin(lo, lo_s[q]); hi = fmax(hi, hi_s[q]); }
+  if (amvm::dsub(hi, lo) < 1e-12) {
+    lo = amvm::dsub(lo, 0.5);
+    hi = amvm::dadd(hi, 0.5);
+  }
+  if (nlev == 1) {
+    if (tid == 0) lvs[0] = lo;
+  } else {
+    const double step = amvm::ddiv(amvm::dsub(hi, lo), (double)(nlev - 1));
+    for (int64_t q = tid; q < nlev; q += NT)
+      lvs[q] = q == nlev - 1 ? hi : amvm::dadd(amvm::dmul((double)q, step), lo);
+  }
+  __syncthreads();
+  for (int64_t q = tid; q < nlev; q += NT) levels[k * nlev + q] = lvs[q];
+  for (int64_t j = tid; j < n; j += NT) {
+    const double v = w[j];
+    int best = 0;
+    double bd = fabs(amvm::dsub(v, lvs[0]));
+    for (int q = 1; q < nlev; ++q) {
+      const double d = fabs(amvm::dsub(v, lvs[q]));
+      if (d < bd) { bd = d; best = q; }
+    }
+    idx[k * n + j] = best;
+  }
+}
+
+// numpy SeedSequence(seed) -> PCG64 state (numpy/random/bit_generator.pyx,
+// _pcg64.pyx): pool of 4 uint32 via hashmix/mix, generate_state(4, uint64),
+// pcg64_set_seed(state = s[0]:s[1], inc = s[2]:s[3]).
+namespace {
+constexpr uint32_t kInitA = 0x43b0d7e5u, kMultA = 0x931e8875u, kInitB = 0x8b51f9ddu, kMultB = 0x58f38dedu;
+constexpr uint32_t kMixL = 0xca01f9ddu, kMixR = 0x4973f715u;
+
+uint32_t hashmix(uint32_t v, uint32_t &hc) {
+  v ^= hc;
+  hc *= kMultA;
+  v *= hc;
+  v ^= v >> 16;
+  return v;
+}
+uint32_t mixw(uint32_t x, uint32_t y) {
+  uint32_t r = kMixL * x - kMixR * y;
+  return r ^ (r >> 16);
+}
+
+void seed_pcg64(uint64_t seed, amvm_pcg64 *out) {
+  uint32_t ent[2];
+  int ne = 0;
+  ent[ne++] = (uint32_t)seed;
+  if (seed >> 32) ent[ne++] = (uint32_t)(seed >> 32);
+  uint32_t pool[4];
+  uint32_t hc = kInitA;
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < ne ? ent[i] : 0u, hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mixw(pool[d], hashmix(pool[s], hc));
+  uint32_t words[8];
+  uint32_t hb = kInitB;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= kMultB;
+    v *= hb;
+    v ^= v >> 16;
+    words[i] = v;
+  }
+  uint64_t val[4];
+  for (int i = 0; i < 4; ++i) val[i] = (uint64_t)words[2 * i] | ((uint64_t)words[2 * i + 1] << 32);
+  typedef unsigned __int128 u128;
+  const u128 mult = ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
+  const u128 initstate = ((u128)val[0] << 64) | val[1];
+  const u128 initseq = ((u128)val[2] << 64) | val[3];
+  u128 st = 0, inc = (initseq << 1) | 1u;
+  st = st * mult + inc;
+  st += initstate;
+  st = st * mult + inc;
+  out->state_hi = (uint64_t)(st >> 64);
+  out->state_lo = (uint64_t)st;
+  out->inc_hi = (uint64_t)(inc >> 64);
+  out->inc_lo = (uint64_t)inc;
+  out->has_uint32 = 0;
+  out->uinteger = 0;
+}
+}  // namespace
 
 // ---------------------------------------------------------------- planning
 namespace {
@@ -443,12 +561,31 @@ int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol, void *st
   if (prob->m < 1 || prob->n < 1 || prob->count < 1) return AMVM_ERR_INVALID;
   const int64_t blocks = (prob->count + kRI - 1) / kRI;
   k_residual<256><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-      prob->m, prob->n, prob->nlev, prob->count, prob->At, prob->B, prob->levels, sol->idx, sol->residual,
-      sol->objective);
+      prob->m, prob->n, prob->nlev, prob->count, prob->At, prob->B, prob->levels, sol->idx, nullptr,
+      sol->residual, sol->objective);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
   e = cudaMemsetAsync(sol->updates, 0, sizeof(int32_t) * prob->count, (cudaStream_t)stream);
   return cuda_rc(e);
+}
+
+int amvm_ptq_prepare(int64_t m, int64_t n, int64_t count, int64_t nlev, const double *At, const double *W,
+                     double *B, double *levels, int32_t *idx, void *stream) {
+  if (m < 1 || n < 1 || count < 1 || nlev < 1 || nlev > 1024 || !At || !W || !B || !levels || !idx)
+    return AMVM_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_ptq_prepare<256><<<(unsigned)count, 256, 0, st>>>(n, nlev, W, levels, idx);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  const int64_t blocks = (count + kRI - 1) / kRI;
+  k_residual<256><<<(unsigned)blocks, 256, 0, st>>>(m, n, nlev, count, At, nullptr, levels, idx, W, B, nullptr);
+  return cuda_rc(cudaGetLastError());
+}
+
+int amvm_seed_pcg64(const uint64_t *seeds_host, int64_t count, amvm_pcg64 *out_host) {
+  if (!seeds_host || !out_host || count < 0) return AMVM_ERR_INVALID;
+  for (int64_t k = 0; k < count; ++k) seed_pcg64(seeds_host[k], &out_host[k]);
+  return AMVM_OK;
 }
 
 }  // extern "C"

@@ -70,3 +70,14 @@ def test_trivial_solves_need_no_device(monkeypatch):
     rep = P.solve(P.Instance(np.eye(2), np.array([0.3, 0.2]), P.ValueSet([0.0, 1.0])),
                   P.SolverConfig(max_iters=0))
     assert rep.iterations == 0 and rep.initial_objective == rep.best.objective
+
+
+def test_seed_states_match_numpy_seedsequence():
+    from paper_2508_13437_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libamvm.so not built")
+    seeds = np.array([0, 1, 7, 14335, 2**32 + 5, 2**63 + 1], dtype=np.uint64)
+    st = _native.seed_states(seeds)
+    for k, s in enumerate(seeds):
+        assert _native.pcg_to_state(st[k]) == np.random.default_rng(int(s)).bit_generator.state

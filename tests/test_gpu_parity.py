@@ -219,3 +219,57 @@ def test_compute_residual_matches_host_blas_order(amvm, oracle):
         got = R.cpu().numpy()
         np.testing.assert_array_equal(got, want)
         np.testing.assert_array_equal(O.cpu().numpy(), np.abs(want).max(axis=1))
+
+
+# ------------------------------------------------------- shared-X batch (PTQ)
+def test_ptq_prepare_and_batch_solve_match_host(amvm, oracle):
+    """solve_layer == per-row reference semantics (host numpy start + oracle)."""
+    from threadpoolctl import threadpool_limits
+
+    from paper_2508_13437_b200 import ptq
+
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((136, 60))
+    W = rng.standard_normal((37, 60)) * 0.02
+    W[5] = 0.01  # collapsed range -> widened grid (builders.py:367-369)
+    cfg = amvm.SolverConfig(max_iters=25, destroy_rate=0.05)
+    rep = ptq.solve_layer(X, W, bits=4, cfg=cfg, trace=True)
+    prm = oracle.make_params(60, max_iters=25, destroy_rate=0.05)
+    for r in range(W.shape[0]):
+        w = W[r]
+        lo, hi = float(w.min()), float(w.max())
+        if hi - lo < 1e-12:
+            lo, hi = lo - 0.5, hi + 0.5
+        lv = np.linspace(lo, hi, 16)
+        np.testing.assert_array_equal(rep.levels[r], lv)
+        with threadpool_limits(1):
+            b = X @ w
+            idx0 = np.argmin(np.abs(w[:, None] - lv[None, :]), axis=1)
+            r0 = X @ lv[idx0] - b
+        out = oracle.solve(X, b, lv, idx0, r0, float(np.max(np.abs(r0))), 0, prm, oracle.pcg_from_seed(r))
+        assert rep.initial_objective[r] == float(np.max(np.abs(r0)))
+        assert int(rep.iterations[r]) == int(out["iterations"][0])
+        np.testing.assert_array_equal(rep.codes[r], out["best_idx"][0])
+        assert rep.objective[r] == out["best_objective"][0]
+        it = int(rep.iterations[r])
+        np.testing.assert_array_equal(rep.seconds["trace"]["trace_current_t"][r, :it],
+                                      out["trace_current_t"][0, :it])
+
+
+def test_ptq_layer_row_matches_reference_golden(amvm):
+    """Row 0 of the C4-shaped layer through the batch pipeline == dmmv.solve."""
+    from paper_2508_13437_b200 import ptq
+    from tests.golden import recipes
+    from tests.golden_io import sha
+
+    rec = load("solve_c4row")[0]
+    X, W = recipes.ptq_layer(768, 3072)
+    if sha(X) != rec["A_sha"]:
+        pytest.skip("host numpy does not regenerate X bit-exactly")
+    cfg = amvm.SolverConfig(**cfg_kwargs(rec))
+    rep = ptq.solve_layer(X, W[:3], bits=4, cfg=cfg, trace=True)
+    assert rep.initial_objective[0] == rec["initial_objective"]
+    np.testing.assert_array_equal(rep.codes[0], rec["best_idx"])
+    assert rep.objective[0] == rec["best_objective"]
+    it = int(rec["iterations"])
+    np.testing.assert_array_equal(rep.seconds["trace"]["trace_current_t"][0, :it], rec["trace_current_t"])
