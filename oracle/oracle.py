@@ -47,7 +47,8 @@ class Result(C.Structure):
     _fields_ = [("best", Sol), ("initial_objective", C.c_void_p), ("iterations", C.c_void_p),
                 ("operator_uses", C.c_void_p), ("trace_current_t", C.c_void_p),
                 ("trace_best_t", C.c_void_p), ("trace_pair", C.c_void_p),
-                ("trace_accepted", C.c_void_p), ("moves_scored", C.c_void_p)]
+                ("trace_accepted", C.c_void_p), ("moves_scored", C.c_void_p),
+                ("phase_cycles", C.c_void_p)]
 
 
 class Problem(C.Structure):

@@ -62,7 +62,7 @@ class ResultPtrs(C.Structure):
                 ("iterations", C.c_void_p), ("operator_uses", C.c_void_p),
                 ("trace_current_t", C.c_void_p), ("trace_best_t", C.c_void_p),
                 ("trace_pair", C.c_void_p), ("trace_accepted", C.c_void_p),
-                ("moves_scored", C.c_void_p)]
+                ("moves_scored", C.c_void_p), ("phase_cycles", C.c_void_p)]
 
 
 _lib = None

@@ -17,7 +17,7 @@ using namespace amvm;
 // Persistent solve: one CTA per resident slot, instances pulled from a
 // counter so uneven iteration counts balance across SMs.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_solve(KArgs a) {
+__global__ void __launch_bounds__(NT, 2) k_solve(KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   Engine<NT> E;
   E.bind(a, smem, blockIdx.x);
@@ -297,8 +297,7 @@ int64_t pow2ceil(int64_t v) {
 
 template <int NT>
 size_t smem_bytes(int64_t m, int64_t nlev, int cr_smem, int tab) {
-  size_t s = sizeof(Shared<NT>) + 8 * ((nlev + 1) & ~1) + 8 * kTC * (kTK + 1);
-  if (tab) s += 8 * kG * nlev * nlev;
+  size_t s = sizeof(Shared<NT>) + 8 * ((nlev + 1) & ~1) + scratch_bytes(nlev, tab);
   if (cr_smem) s += 8 * m;
   return s;
 }

@@ -25,10 +25,20 @@
 namespace amvm {
 
 constexpr int kWin = 16;       // one_opt speculative window (columns per barrier)
-constexpr int kG = 4;          // filter rows gathered row-major per find_candidates
-constexpr int kTabMaxLev = 32; // bound table in smem when nlev <= this
+constexpr int kG = 8;          // filter rows staged in smem per find_candidates
+constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
+constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = 128;       // impact tile: columns
 constexpr int kTK = 16;        // impact tile: rows
+
+// Phase-shared smem scratch: the impact tile or the find_candidates tiles.
+__host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
+  size_t fc = 8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2);
+  fc = (fc + 15) & ~(size_t)15;
+  if (tab) fc += 8 * kG * nlev * nlev;
+  size_t imp = 8 * kTC * (kTK + 1);
+  return fc > imp ? fc : imp;
+}
 
 struct Cand {
   int32_t i, j;
@@ -119,6 +129,8 @@ template <int NT>
 struct Shared {
   static constexpr int NW = NT / 32;
   double red[2][NW][32];
+  uint32_t redu[2][NW][32];
+  double red2[2][NW];
   double redS[NW];
   double bc_d[8];
   int bc_i[16];
@@ -147,7 +159,8 @@ struct Engine {
   int nleaf_m, nleaf_n;
   int32_t *rows, *rsgn;
   double *reps;
-  double *ag, *btab, *tile;
+  double *ag;
+  unsigned char *scr;
   Cand *cbuf;
   uint64_t *hset;
   int32_t *rem, *sav, *pick, *coin, *ibuf;
@@ -161,6 +174,7 @@ struct Engine {
   double w[4], sc[4];
   int64_t seg[4], life[4], bit;
   int64_t mv_ref, mv_raw;
+  int64_t pc[8];  // phase cycles (thread 0's view), see amvm_result.phase_cycles
   int32_t *status;
 
   // ------------------------------------------------------------ utilities
@@ -254,9 +268,38 @@ struct Engine {
     dpv[j] = k + 1 < nlev ? dsub(lv[k + 1], lv[k]) : 0.0;
   }
 
-  // one_opt, localsearch.py:59-88, with the speculative window described in
-  // the file header.  Candidates of columns after the applied one are
-  // re-scored against the updated residual (counted as raw, not reference).
+  // Exact max_i |cr_i + d*col_i| for both candidates of one column (CTA-wide).
+  __device__ void exact_pair_max(const double *col, double dm, double dp, double &tm, double &tp) {
+    double mm = 0.0, mp = 0.0;
+    for (int64_t i = tid; i < m; i += NT) {
+      const double r = cr[i], a = __ldg(col + i);
+      mm = fmax(mm, fabs(dadd(r, dmul(dm, a))));
+      mp = fmax(mp, fabs(dadd(r, dmul(dp, a))));
+    }
+    mm = warp_max(mm);
+    mp = warp_max(mp);
+    if (lane == 0) {
+      sh->red2[0][warp] = mm;
+      sh->red2[1][warp] = mp;
+    }
+    __syncthreads();
+    tm = 0.0;
+    tp = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      tm = fmax(tm, sh->red2[0][k]);
+      tp = fmax(tp, sh->red2[1][k]);
+    }
+    __syncthreads();
+  }
+
+  // one_opt, localsearch.py:59-88.  Speculative window of kWin columns scored
+  // against one residual.  The scan keeps only the high 32 bits of |y| (an
+  // integer max on the ALU pipe instead of an FP64 compare-select chain): a
+  // candidate whose high word exceeds that of the objective t cannot improve
+  // (|y| > t), so only columns with some candidate at or below it are
+  // re-scored exactly, in ascending order; the first that strictly improves
+  // is applied, exactly like the sequential first-improvement sweep.
   __device__ void one_opt() {
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) set_deltas(j, cidx[j]);
@@ -267,27 +310,25 @@ struct Engine {
       int64_t p = 0;
       while (p < n) {
         const int wc = (int)(n - p < kWin ? n - p : kWin);
-        double dm[kWin], dp[kWin], v[32];
+        double dm[kWin], dp[kWin];
+        uint32_t h[2 * kWin];
 #pragma unroll
         for (int w = 0; w < kWin; ++w) {
           dm[w] = w < wc ? dmv[p + w] : 0.0;
           dp[w] = w < wc ? dpv[p + w] : 0.0;
-          v[w] = 0.0;
-          v[w + kWin] = 0.0;
+          h[w] = 0u;
+          h[w + kWin] = 0u;
         }
-        // lane w < wc keeps the level of column p+w for the decision below
         const int kdec = lane < wc ? cidx[p + lane] : 0;
         const double *a0 = At + p * m;
         if (wc == kWin) {
           for (int64_t i = tid; i < m; i += NT) {
             const double r = cr[i];
-            double av[kWin];
-#pragma unroll
-            for (int w = 0; w < kWin; ++w) av[w] = __ldg(a0 + w * m + i);
 #pragma unroll
             for (int w = 0; w < kWin; ++w) {
-              v[w] = fmax(v[w], fabs(dadd(r, dmul(dm[w], av[w]))));
-              v[w + kWin] = fmax(v[w + kWin], fabs(dadd(r, dmul(dp[w], av[w]))));
+              const double av = __ldg(a0 + w * m + i);
+              h[w] = max(h[w], (uint32_t)__double2hiint(dadd(r, dmul(dm[w], av))) & 0x7fffffffu);
+              h[w + kWin] = max(h[w + kWin], (uint32_t)__double2hiint(dadd(r, dmul(dp[w], av))) & 0x7fffffffu);
             }
           }
         } else {
@@ -296,49 +337,63 @@ struct Engine {
 #pragma unroll
             for (int w = 0; w < kWin; ++w) {
               if (w < wc) {
-                double av = __ldg(a0 + w * m + i);
-                v[w] = fmax(v[w], fabs(dadd(r, dmul(dm[w], av))));
-                v[w + kWin] = fmax(v[w + kWin], fabs(dadd(r, dmul(dp[w], av))));
+                const double av = __ldg(a0 + w * m + i);
+                h[w] = max(h[w], (uint32_t)__double2hiint(dadd(r, dmul(dm[w], av))) & 0x7fffffffu);
+                h[w + kWin] = max(h[w + kWin], (uint32_t)__double2hiint(dadd(r, dmul(dp[w], av))) & 0x7fffffffu);
               }
             }
           }
         }
-        double t = warp_transpose_max32(v, lane);
-        sh->red[par][warp][lane] = t;
-        __syncthreads();
-        t = 0.0;
+        uint32_t mine = 0u;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) t = fmax(t, sh->red[par][k][lane]);
-        par ^= 1;
-        const double tp = __shfl_sync(AMVM_FULL, t, (lane + kWin) & 31);
-        int lvl = -1;
-        double bt = cobj;
-        if (lane < wc) {
-          if (kdec - 1 >= 0 && t < bt) { bt = t; lvl = kdec - 1; }
-          if (kdec + 1 < nlev && tp < bt) { bt = tp; lvl = kdec + 1; }
+        for (int v = 0; v < 2 * kWin; ++v) {
+          const uint32_t rv = __reduce_max_sync(AMVM_FULL, h[v]);
+          if (lane == v) mine = rv;
         }
-        const unsigned imp = __ballot_sync(AMVM_FULL, lvl >= 0);
-        const unsigned vlo = __ballot_sync(AMVM_FULL, lane < wc && kdec > 0);
-        const unsigned vhi = __ballot_sync(AMVM_FULL, lane < wc && kdec + 1 < nlev);
+        sh->redu[par][warp][lane] = mine;
+        __syncthreads();
+        uint32_t hv = 0u;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) hv = max(hv, sh->redu[par][k][lane]);
+        par ^= 1;
+        const uint32_t hp = __shfl_sync(AMVM_FULL, hv, (lane + kWin) & 31);
+        const uint32_t thi = (uint32_t)__double2hiint(cobj) & 0x7fffffffu;
+        const bool vm = lane < wc && kdec > 0;
+        const bool vp = lane < wc && kdec + 1 < nlev;
+        unsigned fl = __ballot_sync(AMVM_FULL, (vm && hv <= thi) || (vp && hp <= thi));
+        const unsigned vlo = __ballot_sync(AMVM_FULL, vm);
+        const unsigned vhi = __ballot_sync(AMVM_FULL, vp);
         mv_raw += __popc(vlo) + __popc(vhi);
-        if (imp) {
-          const int ws = __ffs(imp) - 1;
-          const unsigned upto = ws == 31 ? AMVM_FULL : ((2u << ws) - 1u);
-          mv_ref += __popc(vlo & upto) + __popc(vhi & upto);
-          const int nl = __shfl_sync(AMVM_FULL, lvl, ws);
-          const int old = __shfl_sync(AMVM_FULL, kdec, ws);
-          const double nt = __shfl_sync(AMVM_FULL, bt, ws);
-          const int64_t j = p + ws;
-          const double d = dsub(lv[nl], lv[old]);
-          const double *col = At + j * m;
-          for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
-          if (tid == 0) {
-            cidx[j] = nl;
-            set_deltas(j, nl);
+        int applied = -1;
+        while (fl) {
+          const int w = __ffs(fl) - 1;
+          fl &= fl - 1;
+          const int k = __shfl_sync(AMVM_FULL, kdec, w);
+          const int64_t j = p + w;
+          double tm, tpv;
+          exact_pair_max(At + j * m, dmv[j], dpv[j], tm, tpv);
+          int lvl = -1;
+          double bt = cobj;
+          if (k > 0 && tm < bt) { bt = tm; lvl = k - 1; }
+          if (k + 1 < nlev && tpv < bt) { bt = tpv; lvl = k + 1; }
+          if (lvl >= 0) {
+            applied = w;
+            const double d = dsub(lv[lvl], lv[k]);
+            const double *col = At + j * m;
+            for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
+            if (tid == 0) {
+              cidx[j] = lvl;
+              set_deltas(j, lvl);
+            }
+            bump_known(bt);
+            break;
           }
-          bump_known(nt);
+        }
+        if (applied >= 0) {
+          const unsigned upto = applied == 31 ? AMVM_FULL : ((2u << applied) - 1u);
+          mv_ref += __popc(vlo & upto) + __popc(vhi & upto);
           changed = true;
-          p = j + 1;
+          p = p + applied + 1;
         } else {
           mv_ref += __popc(vlo) + __popc(vhi);
           p += wc;
@@ -478,69 +533,119 @@ struct Engine {
   }
 
   // find_candidates, localsearch.py:128-169.  Pairs (i, j) with x_i > x_j
-  // (levels are strictly increasing, so idx_i > idx_j) that pass the
-  // one-sided interval test on every selected row.  Returns the count kept
-  // (truncated to max_candidates in (-delta, i, j) order); when
-  // `always_sort`, the kept list is in that order even if not truncated.
+  // (levels strictly increase, so idx_i > idx_j) passing the one-sided
+  // interval test on every selected row.  Variables are bucketed by level, so
+  // for each i only the level-sorted positions below idx_i are visited; the
+  // kG tightest rows are staged in smem tiles with the row's sign folded in
+  // (s_k < 0: b = -a, so every row reads  b_j - b_i < eps_k / delta, which is
+  // bitwise the reference's test); rows beyond kG read A directly for the few
+  // pairs that survive the staged ones.  Returns the count kept (truncated
+  // to max_candidates in (-delta, i, j) order); with `always_sort` the kept
+  // list is in that order even when not truncated.
   __device__ int find_candidates(bool always_sort) {
     const int nr = select_rows();
     const int g = nr < kG ? nr : kG;
+    double *tb = (double *)scr;
+    int32_t *tl = (int32_t *)(tb + kG * kTJ);
+    int32_t *tj = tl + kTJ;
+    int32_t *lst = tj + kTJ;
+    int32_t *lfl = lst + (nlev + 1);
+    double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
     for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
       const int64_t q = e / n, j = e - q * n;
-      ag[e] = __ldg(At + j * m + rows[q]);
+      const double a = __ldg(At + j * m + rows[q]);
+      ag[e] = rsgn[q] ? a : -a;
     }
+    for (int64_t k = tid; k <= nlev; k += NT) lfl[k] = 0;
+    __syncthreads();
+    for (int64_t j = tid; j < n; j += NT) atomicAdd(&lfl[cidx[j]], 1);
+    __syncthreads();
+    if (tid == 0) {
+      int32_t acc = 0;
+      for (int64_t k = 0; k < nlev; ++k) {
+        const int32_t c = lfl[k];
+        lst[k] = acc;
+        lfl[k] = acc;
+        acc += c;
+      }
+      lst[nlev] = acc;
+    }
+    __syncthreads();
+    for (int64_t j = tid; j < n; j += NT) ibuf[atomicAdd(&lfl[cidx[j]], 1)] = (int32_t)j;
     if (tab) {
-      for (int e = tid; e < g * nlev * nlev; e += NT) {
-        const int q = e / (int)(nlev * nlev), rem2 = e - q * (int)(nlev * nlev);
-        const int ki = rem2 / (int)nlev, kj = rem2 - ki * (int)nlev;
-        btab[e] = ki > kj ? ddiv(reps[q], dsub(lv[ki], lv[kj])) : 0.0;
+      const int ll = (int)(nlev * nlev);
+      for (int e = tid; e < g * ll; e += NT) {
+        const int q = e / ll, r2 = e - q * ll;
+        const int ki = r2 / (int)nlev, kj = r2 - ki * (int)nlev;
+        bt[e] = ki > kj ? ddiv(reps[q], dsub(lv[ki], lv[kj])) : 0.0;
       }
     }
     if (tid == 0) sh->counter = 0;
     __syncthreads();
-    for (int64_t i = warp; i < n; i += NW) {
-      const int ki = cidx[i];
-      if (ki == 0) continue;
-      const double xi = lv[ki];
-      double ai[kG];
+    const int ll = (int)(nlev * nlev);
+    for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
+      const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
+      for (int64_t e = tid; e < p1 - p0; e += NT) {
+        const int32_t j = ibuf[p0 + e];
+        tj[e] = j;
+        tl[e] = cidx[j];
 #pragma unroll
-      for (int q = 0; q < kG; ++q) ai[q] = q < g ? ag[q * n + i] : 0.0;
-      for (int64_t jb = 0; jb < n; jb += 32) {
-        const int64_t j = jb + lane;
-        bool alive = false;
-        double delta = 0.0;
-        if (j < n) {
-          const int kj = cidx[j];
-          if (kj < ki) {
+        for (int q = 0; q < kG; ++q)
+          if (q < g) tb[q * kTJ + e] = ag[(int64_t)q * n + j];
+      }
+      __syncthreads();
+      for (int64_t i = warp; i < n; i += NW) {
+        const int ki = cidx[i];
+        const int64_t hi = (int64_t)lst[ki] < p1 ? (int64_t)lst[ki] : p1;
+        if (hi <= p0) continue;
+        double bi[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) bi[q] = q < g ? ag[(int64_t)q * n + i] : 0.0;
+        const double xi = lv[ki];
+        for (int64_t base = p0; base < hi; base += 32) {
+          const int64_t pos = base + lane;
+          bool alive = pos < hi;
+          int kj = 0;
+          double delta = 0.0;
+          const int e = (int)(pos - p0);
+          if (alive) {
+            kj = tl[e];
             delta = dsub(xi, lv[kj]);
-            alive = true;
-            for (int q = 0; q < nr && alive; ++q) {
-              double da, bound;
-              if (q < g) {
-                da = dsub(ag[q * n + j], ai[q]);
-                bound = tab ? btab[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta);
-              } else {
-                const int64_t rq = rows[q];
-                da = dsub(__ldg(At + j * m + rq), __ldg(At + i * m + rq));
-                bound = ddiv(reps[q], delta);
-              }
-              alive = rsgn[q] ? (da < bound) : (da > -bound);
+            if (g > 0) {
+              const double b0 = tab ? bt[ki * nlev + kj] : ddiv(reps[0], delta);
+              alive = dsub(tb[e], bi[0]) < b0;
+            }
+            if (alive && g > 1) {
+              const double b1 = tab ? bt[ll + ki * nlev + kj] : ddiv(reps[1], delta);
+              alive = dsub(tb[kTJ + e], bi[1]) < b1;
+            }
+          }
+          for (int q = 2; alive && q < nr; ++q) {
+            if (q < g) {
+              const double bq = tab ? bt[q * ll + ki * nlev + kj] : ddiv(reps[q], delta);
+              alive = dsub(tb[q * kTJ + e], bi[q]) < bq;
+            } else {
+              const int64_t rq = rows[q];
+              const int32_t j = tj[e];
+              const double da = dsub(__ldg(At + (int64_t)j * m + rq), __ldg(At + i * m + rq));
+              const double bq = ddiv(reps[q], delta);
+              alive = rsgn[q] ? (da < bq) : (da > -bq);
+            }
+          }
+          const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+          if (bal) {
+            int bse = 0;
+            if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
+            bse = __shfl_sync(AMVM_FULL, bse, 0);
+            if (alive) {
+              const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
+              if (pos2 < cap) cbuf[pos2] = Cand{(int32_t)i, tj[e], delta};
             }
           }
         }
-        const unsigned bal = __ballot_sync(AMVM_FULL, alive);
-        if (bal) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&sh->counter, __popc(bal));
-          base = __shfl_sync(AMVM_FULL, base, 0);
-          if (alive) {
-            const int pos = base + __popc(bal & ((1u << lane) - 1u));
-            if (pos < cap) cbuf[pos] = Cand{(int32_t)i, (int32_t)j, delta};
-          }
-        }
       }
+      __syncthreads();
     }
-    __syncthreads();
     int cnt = sh->counter;
     __syncthreads();
     if (cnt > cap) {
@@ -560,7 +665,10 @@ struct Engine {
   // (i, j).  Returns found; the winner is uniform across the CTA.
   __device__ bool best_swap(int &bi, int &bj, double &bd, double &bt) {
     if (!(cobj > 0.0)) return false;
+    const long long tf0 = clock64();
     const int cnt = find_candidates(false);
+    const long long tf1 = clock64();
+    pc[5] += tf1 - tf0;
     if (cnt == 0) return false;
     double wt = 0.0, wd = 0.0;
     int wi = -1, wj = -1;
@@ -589,6 +697,7 @@ struct Engine {
       sh->red[0][warp][2] = __longlong_as_double(((int64_t)wi << 32) | (uint32_t)wj);
     }
     __syncthreads();
+    pc[6] += clock64() - tf1;
     bool found = false;
     for (int k = 0; k < NW; ++k) {
       const int64_t ij = __double_as_longlong(sh->red[0][k][2]);
@@ -639,6 +748,7 @@ struct Engine {
     const double t = cobj;
     const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
     const double na = -alpha;
+    double *tile = (double *)scr;
     for (int64_t cb = 0; cb < n; cb += kTC) {
       const int cols = (int)(n - cb < kTC ? n - cb : kTC);
       double acc = 0.0;
@@ -973,15 +1083,13 @@ struct Engine {
     pick = (int32_t *)(base + L.pick);
     coin = (int32_t *)(base + L.coin);
     ibuf = (int32_t *)(base + L.ibuf);
-    // dynamic smem: Shared | lv | tile | btab | cr
+    // dynamic smem: Shared | lv | scratch | cr
     size_t o = sizeof(Shared<NT>);
     sh = (Shared<NT> *)smem;
     lv = (double *)(smem + o);
     o += 8 * ((nlev + 1) & ~1);
-    tile = (double *)(smem + o);
-    o += 8 * kTC * (kTK + 1);
-    btab = (double *)(smem + o);
-    if (tab) o += 8 * kG * nlev * nlev;
+    scr = smem + o;
+    o += scratch_bytes(nlev, tab);
     cr = a.cr_smem ? (double *)(smem + o) : (double *)(base + L.crg);
     // leaf trees for m and n (fixed per problem)
     if (tid == 0) {
@@ -1038,6 +1146,7 @@ struct Engine {
     }
     bit = 0;
     mv_ref = mv_raw = 0;
+    for (int k = 0; k < 8; ++k) pc[k] = 0;
     const int64_t r = a.prm.r;
     const int T = a.prm.max_iters;
     const uint64_t t_start = gtimer();
@@ -1045,6 +1154,7 @@ struct Engine {
     int it = 0;
     while (it < T) {
       if (bobj == 0.0) break;
+      long long tp = clock64(), tq;
       if (tid == 0) {
         int stop = 0;
         if (a.time_budget_ns >= 0 && (int64_t)(gtimer() - t_start) > a.time_budget_ns) stop = 1;
@@ -1058,11 +1168,16 @@ struct Engine {
       ++it;
       if (!cand_is_cur) cand_from_cur();
       cand_is_cur = false;
+      tq = clock64(); pc[0] += tq - tp; tp = tq;
       if (pair < 2) random_destroy(r);
       else worst_destroy(r, a.prm.alpha);
+      tq = clock64(); pc[pair < 2 ? 1 : 2] += tq - tp; tp = tq;
       if (pair & 1) greedy_repair(rem, sav, r);
       else random_repair(rem, sav, r);
+      tq = clock64(); pc[3] += tq - tp; tp = tq;
+      const long long fc0 = pc[5] + pc[6];
       local_search();
+      tq = clock64(); pc[4] += (tq - tp) - (pc[5] + pc[6] - fc0); tp = tq;
       const bool acc = accept();
       int outcome;
       if (acc && cobj < bobj) outcome = 0;
@@ -1083,6 +1198,7 @@ struct Engine {
         res.trace_pair[o] = (uint8_t)pair;
         res.trace_accepted[o] = (uint8_t)acc;
       }
+      pc[7] += clock64() - tp;
     }
     if (tid == 0) {
       res.best.objective[inst] = bobj;
@@ -1094,6 +1210,8 @@ struct Engine {
         res.moves_scored[2 * inst] = mv_ref;
         res.moves_scored[2 * inst + 1] = mv_raw;
       }
+      if (res.phase_cycles)
+        for (int k = 0; k < 8; ++k) res.phase_cycles[8 * inst + k] = pc[k];
     }
     store_rng(&a.rng[inst]);
     __syncthreads();
@@ -1107,6 +1225,7 @@ struct Engine {
     cobj = a.s_obj[0];
     ccnt = a.s_cnt[0];
     mv_ref = mv_raw = 0;
+    for (int k = 0; k < 8; ++k) pc[k] = 0;
     __syncthreads();
   }
 

@@ -112,6 +112,7 @@ class LayerBatch:
             "iterations": torch.empty(c, dtype=torch.int32, device=dev),
             "operator_uses": torch.empty((c, 4), dtype=torch.int64, device=dev),
             "moves_scored": torch.empty((c, 2), dtype=torch.int64, device=dev),
+            "phase_cycles": torch.empty((c, 8), dtype=torch.int64, device=dev),
         }
         tr = [None] * 4
         if trace:
@@ -125,7 +126,7 @@ class LayerBatch:
             N.SolutionPtrs(o["best_idx"].data_ptr(), o["best_residual"].data_ptr(),
                            o["best_objective"].data_ptr(), o["best_updates"].data_ptr()),
             o["initial_objective"].data_ptr(), o["iterations"].data_ptr(), o["operator_uses"].data_ptr(),
-            *tr, o["moves_scored"].data_ptr())
+            *tr, o["moves_scored"].data_ptr(), o["phase_cycles"].data_ptr())
         prm = make_params(cfg, n, time_budget=cfg.time_limit)
         prob = self.problem()
         nbytes = self.lib.amvm_workspace_bytes(N.C.byref(prob), N.C.byref(prm))
