@@ -1,0 +1,320 @@
+"""Benchmark: AMVM candidate-move scoring on the Llama-3-8B-shaped PTQ layer (C5).
+
+Workload (BASELINE.json configs[4]): one 4096->14336 MLP layer,
+int4 per-row grids, 2048 synthetic calibration tokens:
+  X = default_rng(0).standard_normal((2048, 4096))      (shared A of every row)
+  W = default_rng(1).standard_normal((14336, 4096)) * 0.02
+Row r is the instance  min ||X x - X w_r||_inf, x in linspace(min w_r, max w_r, 16)^4096,
+warm start w_r, seed r (builders.py:355-372 semantics, one X for the layer).
+
+A step = one amvm_solve over this rank's block of `--rows` rows for `--iters`
+ALNS iterations each, from the prepared start (the device-resident path; X, B,
+levels and start residuals already in HBM).  Weak scaling: rank k owns rows
+[k*rows, (k+1)*rows).  `value` = reference-equivalent candidate moves scored
+per second (1-OPT neighbours, 2 per greedy variable, filtered
+swap candidates), summed over ranks / max-over-ranks device time.
+`e2e` = the same metric through the public API (ptq.solve_layer) with X and W
+rows in pinned host memory, copies and the result read-back inside the timed
+region.  `--impl reference` times the CPU restatement of the reference
+(oracle/, bit-identical trajectories) with all host threads on the same rows.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_CALIB, D_IN, D_OUT = 2048, 4096, 14336
+METRIC = "candidate moves scored/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="amvm", choices=["amvm", "reference"])
+    ap.add_argument("--rows", type=int, default=1184, help="rows of the layer per GPU per step")
+    ap.add_argument("--iters", type=int, default=2, help="ALNS iterations per row per step")
+    ap.add_argument("--cpu-rows", type=int, default=16, help="rows in the CPU baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def layer_rows(lo: int, hi: int):
+    X = np.random.default_rng(0).standard_normal((M_CALIB, D_IN))
+    W = np.random.default_rng(1).standard_normal((D_OUT, D_IN)) * 0.02
+    return X, W[lo:hi].copy()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self.stop = gpu, [], threading.Event()
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[2 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "amvm" else "gloo"
+        dist.init_process_group(backend)
+    return rank, world
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def cpu_baseline(rows: int, iters: int, threads: int) -> dict:
+    """The oracle (CPU restatement of the reference, bit-identical trajectories)
+    on `rows` rows of the same layer, all host threads."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import oracle as O
+    X, W = layer_rows(0, rows)
+    B, L, I0, R0, OB = [], [], [], [], []
+    with threadpool_limits(1):
+        for w in W:
+            lo, hi = float(w.min()), float(w.max())
+            lv = np.linspace(lo, hi, 16)
+            b = X @ w
+            idx = np.argmin(np.abs(w[:, None] - lv[None, :]), axis=1)
+            r = X @ lv[idx] - b
+            B.append(b); L.append(lv); I0.append(idx); R0.append(r); OB.append(float(np.max(np.abs(r))))
+    prm = O.make_params(D_IN, max_iters=iters)
+    states = [O.pcg_from_seed(r) for r in range(rows)]
+    t0 = time.perf_counter()
+    out = O.solve(X, np.stack(B), np.stack(L), np.stack(I0), np.stack(R0), np.array(OB), np.zeros(rows),
+                  prm, states, threads=threads)
+    dt = time.perf_counter() - t0
+    moves = int(out["moves_scored"][:, 0].sum())
+    return {"value": moves / dt, "unit": "moves/s", "cores": threads, "kind": "port",
+            "sample": f"{rows} rows x {iters} ALNS iterations of the C5 layer (rows 0..{rows - 1}), "
+                      f"{moves} reference-equivalent moves in {dt:.2f} s",
+            "seconds": dt, "moves": moves}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(min(args.cpu_rows, 4), 1, threads)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(args.cpu_rows, args.iters, threads))
+    v = statistics.median([c["value"] for c in vals])
+    ms = statistics.median([c["seconds"] for c in vals]) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "moves/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5: PTQ Llama-3-8B 4096->14336 int4 layer, 2048 calib tokens",
+                       "rows_per_step": args.cpu_rows, "iters_per_row": args.iters},
+            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "moves/s"},
+            "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_amvm(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_13437_b200 import SolverConfig, ptq
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lo = (rank * args.rows) % D_OUT
+    hi = min(lo + args.rows, D_OUT)
+    X, W = layer_rows(lo, hi)
+    cfg = SolverConfig(max_iters=args.iters)
+    lb = ptq.LayerBatch(X, W, bits=4, rows=None, device=dev)
+    lb.rows = np.arange(lo, hi)  # global row ids -> seeds r
+    lb.prepare()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    st = torch.cuda.current_stream()
+
+    def step():
+        o = lb.solve(cfg)
+        return o
+
+    for _ in range(args.warmup):
+        step()
+    lb.check_status()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    moves = 0
+    phase = np.zeros(16)
+    with Clocks(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        outs = []
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(st)
+            o = step()
+            ev[k][1].record(st)
+            outs.append(o)
+        torch.cuda.synchronize()
+    lb.check_status()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    for o in outs:
+        moves += int(o["moves_scored"][:, 0].sum().item())
+        phase += o["phase_cycles"].sum(dim=0).cpu().numpy()
+    t_max = dev_ms
+    tot_moves = moves
+    if world > 1:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+        mv = torch.tensor([moves], dtype=torch.float64, device=dev)
+        dist.all_reduce(mv)
+        tot_moves = int(mv.item())
+    value = tot_moves / (t_max / 1e3)
+    # roofline: scoring reads one A column (8*m bytes) per 2 adjacent-level
+    # candidates (|V_s| = 2); the dominant kernel is k_solve
+    pk = peaks()
+    bytes_per_move = 8 * M_CALIB / 2
+    achieved = moves * bytes_per_move / (dev_ms / 1e3) / 1e9
+    pc = phase[:8]
+    oo_frac = pc[4] / pc.sum() if pc.sum() else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": pk["source"],
+            "kernel": "k_solve (fused ALNS iteration; all phases)",
+            "bytes_per_move": bytes_per_move, "V_s": 2,
+            "one_opt_phase_share": round(float(oo_frac), 4),
+            "one_opt_phase_GBps": achieved / oo_frac if oo_frac else None}
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, X, W, lo, hi, cfg, world)
+    if rank != 0:
+        return
+    clocks = clk.summary()
+    names = ["select+copy", "rand-destroy", "worst-destroy", "repair", "one_opt", "find_candidates",
+             "swap_eval", "accept"]
+    line = {
+        "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5: PTQ Llama-3-8B 4096->14336 int4 layer, 2048 synthetic calib tokens",
+                   "rows_per_gpu": hi - lo, "iters_per_row": args.iters, "m": M_CALIB, "n": D_IN,
+                   "levels": 16, "parallelism": f"rows sharded over {world} GPU(s)",
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "gpu_launches": args.steps,
+        "roofline": roof,
+        "phase_share": {nm: round(float(v / pc.sum()), 4) for nm, v in zip(names, pc)} if pc.sum() else {},
+        "clocks": clocks,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_rows, args.iters, len(os.sched_getaffinity(0)))
+        line["cpu_baseline"].pop("seconds", None)
+        line["cpu_baseline"].pop("moves", None)
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, X, W, lo, hi, cfg, world):
+    """Public API with host inputs: H2D of X and this rank's W rows every step,
+    D2H of the codes and objectives (ptq.solve_layer)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_13437_b200 import ptq
+
+    Xh = torch.from_numpy(X).pin_memory()
+    Wh = torch.from_numpy(W).pin_memory()
+    rows = np.arange(lo, hi)
+    h2d = Xh.numel() * 8 + Wh.numel() * 8
+    for _ in range(max(1, args.warmup // 2)):
+        ptq.solve_layer(Xh, Wh, bits=4, cfg=cfg, seeds=rows)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    moves = 0
+    d2h = 0
+    steps = max(1, args.steps // 2)
+    for _ in range(steps):
+        rep = ptq.solve_layer(Xh, Wh, bits=4, cfg=cfg, seeds=rows)
+        moves += int(rep.moves_scored[:, 0].sum())
+        d2h = rep.codes.nbytes + rep.objective.nbytes + rep.iterations.nbytes + rep.moves_scored.nbytes
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        mv = torch.tensor([moves], dtype=torch.float64, device="cuda")
+        dist.all_reduce(mv)
+        moves = int(mv.item())
+    return {"value": moves / dt, "unit": "moves/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "path": "ptq.solve_layer (host X, W rows -> device prepare + solve -> host codes)"}
+
+
+def main():
+    args = parse()
+    rank, world = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_amvm(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

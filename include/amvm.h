@@ -107,10 +107,14 @@ typedef struct {
   int64_t *moves_scored;    /* count x 2: [0] reference-equivalent candidate
                                moves scored, [1] raw candidates scored
                                (incl. speculative window work); may be NULL   */
-  int64_t *phase_cycles;    /* count x 8 SM-clock cycles per phase: select+
-                               copy, random destroy, impact+worst destroy,
-                               repair, one_opt, find_candidates, swap
-                               evaluation, accept+commit; may be NULL         */
+  int64_t *phase_cycles;    /* count x 16: [0..7] SM-clock cycles per phase
+                               (select+copy, random destroy, impact+worst
+                               destroy, repair, one_opt, find_candidates,
+                               swap evaluation, accept+commit); [8..15] event
+                               counts (find_candidates calls, survivors, swaps
+                               applied, one_opt exact rechecks, one_opt moves,
+                               one_opt windows, impact calls, refreshes);
+                               may be NULL                                    */
 } amvm_result;
 
 /* ---- whole solve: replaces dmmv.solve (controller.py:211-286) ---------- */

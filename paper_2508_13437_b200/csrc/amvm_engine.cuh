@@ -24,7 +24,7 @@
 
 namespace amvm {
 
-constexpr int kWin = 16;       // one_opt speculative window (columns per barrier)
+constexpr int kWin = 8;        // one_opt speculative window (columns per barrier)
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
@@ -114,7 +114,7 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.reps = o; o = al256(o + 8 * L.kk);
   L.rsgn = o; o = al256(o + 4 * L.kk);
   L.ag = o; o = al256(o + 8 * kG * n);
-  L.cbuf = o; o = al256(o + sizeof(Cand) * cap);
+  L.cbuf = o; o = al256(o + sizeof(Cand) * cap + sizeof(int2) * cap);  // candidates + survivor queue
   L.hset = o; o = al256(o + 8 * L.hsz);
   L.rem = o; o = al256(o + 4 * rr);
   L.sav = o; o = al256(o + 4 * rr);
@@ -124,6 +124,67 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.total = o;
   return L;
 }
+
+// Block-uniform engine context, kept in shared memory (not registers): the
+// kernel is one long state machine, so anything live across all phases must
+// not occupy registers the hot loops need.
+struct Ctx {
+  int64_t m, n, nlev, kk, cap;
+  const double *At, *b;
+  double *lv, *cr, *ur;
+  int32_t *cidx, *uidx;
+  double *dmv, *dpv, *dbuf, *pbuf;
+  int64_t *lf_lo, *lf_len;
+  double *lf_sum;
+  int nleaf_m, nleaf_n, tab;
+  int32_t *rows, *rsgn;
+  double *reps, *ag;
+  unsigned char *scr;
+  Cand *cbuf;
+  uint64_t *hset;
+  int32_t *rem, *sav, *pick, *coin, *ibuf;
+  int32_t *status;
+  amvm_params prm;
+  // operator bank (controller.py:71-85) and counters: thread 0 owns these
+  double w[4], sc[4];
+  int64_t seg[4], life[4], bit;
+  int64_t mv_ref, mv_raw;
+  int64_t pc[16];
+};
+
+#define AMVM_LOCALS                                                                        \
+  [[maybe_unused]] const int64_t m = sh->c.m, n = sh->c.n, nlev = sh->c.nlev;             \
+  [[maybe_unused]] const int64_t kk = sh->c.kk, cap = sh->c.cap;                          \
+  [[maybe_unused]] const double *const At = sh->c.At;                                     \
+  [[maybe_unused]] const double *const b = sh->c.b;                                       \
+  [[maybe_unused]] double *const lv = sh->c.lv;                                           \
+  [[maybe_unused]] double *const cr = sh->c.cr;                                           \
+  [[maybe_unused]] double *const ur = sh->c.ur;                                           \
+  [[maybe_unused]] int32_t *const cidx = sh->c.cidx;                                      \
+  [[maybe_unused]] int32_t *const uidx = sh->c.uidx;                                      \
+  [[maybe_unused]] double *const dmv = sh->c.dmv;                                         \
+  [[maybe_unused]] double *const dpv = sh->c.dpv;                                         \
+  [[maybe_unused]] double *const dbuf = sh->c.dbuf;                                       \
+  [[maybe_unused]] double *const pbuf = sh->c.pbuf;                                       \
+  [[maybe_unused]] int64_t *const lf_lo = sh->c.lf_lo;                                    \
+  [[maybe_unused]] int64_t *const lf_len = sh->c.lf_len;                                  \
+  [[maybe_unused]] double *const lf_sum = sh->c.lf_sum;                                   \
+  [[maybe_unused]] const int nleaf_m = sh->c.nleaf_m, nleaf_n = sh->c.nleaf_n;            \
+  [[maybe_unused]] const int tab = sh->c.tab;                                             \
+  [[maybe_unused]] int32_t *const rows = sh->c.rows;                                      \
+  [[maybe_unused]] int32_t *const rsgn = sh->c.rsgn;                                      \
+  [[maybe_unused]] double *const reps = sh->c.reps;                                       \
+  [[maybe_unused]] double *const ag = sh->c.ag;                                           \
+  [[maybe_unused]] unsigned char *const scr = sh->c.scr;                                  \
+  [[maybe_unused]] Cand *const cbuf = sh->c.cbuf;                                         \
+  [[maybe_unused]] uint64_t *const hset = sh->c.hset;                                     \
+  [[maybe_unused]] int32_t *const rem = sh->c.rem;                                        \
+  [[maybe_unused]] int32_t *const sav = sh->c.sav;                                        \
+  [[maybe_unused]] int32_t *const pick = sh->c.pick;                                      \
+  [[maybe_unused]] int32_t *const coin = sh->c.coin;                                      \
+  [[maybe_unused]] int32_t *const ibuf = sh->c.ibuf;                                      \
+  [[maybe_unused]] int32_t *const status = sh->c.status;                                  \
+  [[maybe_unused]] const amvm_params *const prm = &sh->c.prm;
 
 template <int NT>
 struct Shared {
@@ -137,7 +198,9 @@ struct Shared {
   int wcnt[NW];
   unsigned int hist[256];
   int counter;
+  int qcount;
   Pcg rng;
+  Ctx c;
 };
 
 __device__ __forceinline__ uint64_t abs_key(double x) { return (uint64_t)__double_as_longlong(fabs(x)); }
@@ -145,44 +208,20 @@ __device__ __forceinline__ uint64_t abs_key(double x) { return (uint64_t)__doubl
 template <int NT>
 struct Engine {
   static constexpr int NW = NT / 32;
-  // problem
-  int64_t m, n, nlev;
-  const double *At, *b;
-  double *lv;  // smem
-  const amvm_params *prm;
-  // state
-  double *cr, *ur;
-  int32_t *cidx, *uidx;
-  double *dmv, *dpv, *dbuf, *pbuf;
-  int64_t *lf_lo, *lf_len;
-  double *lf_sum;
-  int nleaf_m, nleaf_n;
-  int32_t *rows, *rsgn;
-  double *reps;
-  double *ag;
-  unsigned char *scr;
-  Cand *cbuf;
-  uint64_t *hset;
-  int32_t *rem, *sav, *pick, *coin, *ibuf;
-  int64_t kk, cap;
-  int tab;
   Shared<NT> *sh;
   int tid, lane, warp;
-  // replicated scalars
+  // replicated block-uniform scalars: every thread evolves identical copies
   double cobj, uobj, bobj;
   int ccnt, ucnt, bcnt;
-  double w[4], sc[4];
-  int64_t seg[4], life[4], bit;
-  int64_t mv_ref, mv_raw;
-  int64_t pc[8];  // phase cycles (thread 0's view), see amvm_result.phase_cycles
-  int32_t *status;
 
   // ------------------------------------------------------------ utilities
   __device__ void fail(int code) {
+    AMVM_LOCALS
     if (tid == 0) atomicCAS(status, 0, code);
   }
 
   __device__ double block_max_own(double mx) {
+    AMVM_LOCALS
     mx = warp_max(mx);
     if (lane == 0) sh->redS[warp] = mx;
     __syncthreads();
@@ -194,6 +233,7 @@ struct Engine {
   }
 
   __device__ double own_max_abs() {
+    AMVM_LOCALS
     double mx = 0.0;
     for (int64_t i = tid; i < m; i += NT) mx = fmax(mx, fabs(cr[i]));
     return block_max_own(mx);
@@ -202,6 +242,7 @@ struct Engine {
   // numpy pairwise sum of get(0..len-1) over the cached leaf tree.
   template <class F>
   __device__ double block_pairwise(F &&get, int64_t len, int64_t *lo, int64_t *ln, int nleaf) {
+    AMVM_LOCALS
     for (int k = tid; k < nleaf; k += NT) lf_sum[k] = pw_leaf(get, lo[k], ln[k]);
     __syncthreads();
     double s = pw_combine(len, lf_sum);
@@ -211,6 +252,8 @@ struct Engine {
 
   // Solution.refresh (core.py:173-177): numpy A @ x - b in the OpenBLAS order.
   __device__ void refresh() {
+    AMVM_LOCALS
+    if (tid == 0) sh->c.pc[15] += 1;
     __syncthreads();  // publish cidx
     if (m == 1) {
       if (warp == 0) {
@@ -231,6 +274,7 @@ struct Engine {
   }
 
   __device__ void bump_known(double t) {
+    AMVM_LOCALS
     ccnt += 1;
     if (ccnt >= prm->refresh_period) refresh();
     else cobj = t;
@@ -238,6 +282,7 @@ struct Engine {
 
   // apply_shift (core.py:208-225) when the new objective is not known yet.
   __device__ bool apply_shift_reduce(int64_t j, int nl) {
+    AMVM_LOCALS
     const int old = cidx[j];
     if (nl == old) return false;
     const double d = dsub(lv[nl], lv[old]);
@@ -264,12 +309,14 @@ struct Engine {
 
   // ------------------------------------------------------------- one_opt
   __device__ void set_deltas(int64_t j, int k) {
+    AMVM_LOCALS
     dmv[j] = k > 0 ? dsub(lv[k - 1], lv[k]) : 0.0;
     dpv[j] = k + 1 < nlev ? dsub(lv[k + 1], lv[k]) : 0.0;
   }
 
   // Exact max_i |cr_i + d*col_i| for both candidates of one column (CTA-wide).
   __device__ void exact_pair_max(const double *col, double dm, double dp, double &tm, double &tp) {
+    AMVM_LOCALS
     double mm = 0.0, mp = 0.0;
     for (int64_t i = tid; i < m; i += NT) {
       const double r = cr[i], a = __ldg(col + i);
@@ -301,6 +348,7 @@ struct Engine {
   // re-scored exactly, in ascending order; the first that strictly improves
   // is applied, exactly like the sequential first-improvement sweep.
   __device__ void one_opt() {
+    AMVM_LOCALS
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) set_deltas(j, cidx[j]);
     __syncthreads();
@@ -344,6 +392,7 @@ struct Engine {
             }
           }
         }
+        if (tid == 0) sh->c.pc[13] += 1;
         uint32_t mine = 0u;
 #pragma unroll
         for (int v = 0; v < 2 * kWin; ++v) {
@@ -363,7 +412,7 @@ struct Engine {
         unsigned fl = __ballot_sync(AMVM_FULL, (vm && hv <= thi) || (vp && hp <= thi));
         const unsigned vlo = __ballot_sync(AMVM_FULL, vm);
         const unsigned vhi = __ballot_sync(AMVM_FULL, vp);
-        mv_raw += __popc(vlo) + __popc(vhi);
+        if (tid == 0) sh->c.mv_raw += __popc(vlo) + __popc(vhi);
         int applied = -1;
         while (fl) {
           const int w = __ffs(fl) - 1;
@@ -371,6 +420,7 @@ struct Engine {
           const int k = __shfl_sync(AMVM_FULL, kdec, w);
           const int64_t j = p + w;
           double tm, tpv;
+          if (tid == 0) sh->c.pc[11] += 1;
           exact_pair_max(At + j * m, dmv[j], dpv[j], tm, tpv);
           int lvl = -1;
           double bt = cobj;
@@ -378,6 +428,7 @@ struct Engine {
           if (k + 1 < nlev && tpv < bt) { bt = tpv; lvl = k + 1; }
           if (lvl >= 0) {
             applied = w;
+            if (tid == 0) sh->c.pc[12] += 1;
             const double d = dsub(lv[lvl], lv[k]);
             const double *col = At + j * m;
             for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
@@ -391,11 +442,11 @@ struct Engine {
         }
         if (applied >= 0) {
           const unsigned upto = applied == 31 ? AMVM_FULL : ((2u << applied) - 1u);
-          mv_ref += __popc(vlo & upto) + __popc(vhi & upto);
+          if (tid == 0) sh->c.mv_ref += __popc(vlo & upto) + __popc(vhi & upto);
           changed = true;
           p = p + applied + 1;
         } else {
-          mv_ref += __popc(vlo) + __popc(vhi);
+          if (tid == 0) sh->c.mv_ref += __popc(vlo) + __popc(vhi);
           p += wc;
         }
       }
@@ -410,7 +461,7 @@ struct Engine {
   // key so the tightest rows reject first.  Rows with s = 0 are dropped
   // (localsearch.py:151).  Returns the number of filter rows.
   __device__ int select_rows() {
-    const int64_t kk = this->kk;
+    AMVM_LOCALS
     __syncthreads();
     if (tid == 0) sh->counter = 0;
     __syncthreads();
@@ -502,14 +553,15 @@ struct Engine {
     return cnt;
   }
 
-  __device__ static bool cand_less(const Cand &a, const Cand &b) {
-    if (a.d != b.d) return a.d > b.d;
-    if (a.i != b.i) return a.i < b.i;
-    return a.j < b.j;
+  __device__ static bool cand_less(const Cand &x, const Cand &y) {
+    if (x.d != y.d) return x.d > y.d;
+    if (x.i != y.i) return x.i < y.i;
+    return x.j < y.j;
   }
 
   // Block bitonic sort of cbuf[0..cnt) into (-delta, i, j) order.
   __device__ void sort_cands(int cnt) {
+    AMVM_LOCALS
     int n2 = 1;
     while (n2 < cnt) n2 <<= 1;
     for (int e = cnt + tid; e < n2; e += NT) cbuf[e] = Cand{0x7fffffff, 0x7fffffff, -1.0};
@@ -534,15 +586,37 @@ struct Engine {
 
   // find_candidates, localsearch.py:128-169.  Pairs (i, j) with x_i > x_j
   // (levels strictly increase, so idx_i > idx_j) passing the one-sided
-  // interval test on every selected row.  Variables are bucketed by level, so
-  // for each i only the level-sorted positions below idx_i are visited; the
-  // kG tightest rows are staged in smem tiles with the row's sign folded in
-  // (s_k < 0: b = -a, so every row reads  b_j - b_i < eps_k / delta, which is
-  // bitwise the reference's test); rows beyond kG read A directly for the few
-  // pairs that survive the staged ones.  Returns the count kept (truncated
-  // to max_candidates in (-delta, i, j) order); with `always_sort` the kept
-  // list is in that order even when not truncated.
+  // interval test on every selected row.
+  //   * variables are bucketed by level; i runs over level-sorted groups of 32
+  //     (one per lane, so a warp's lanes almost always share idx_i) and j over
+  //     the level-sorted positions below idx_i, read by broadcast from smem;
+  //   * the kG tightest rows are staged per j-tile with the row's sign folded
+  //     in (s_k < 0: b = -a), so every staged row is  b_j - b_i < eps_k/delta,
+  //     bitwise the reference's test, evaluated branch-free two rows at a
+  //     time with a warp-level early exit;
+  //   * the few pairs alive after the staged rows go to a queue that the whole
+  //     CTA drains against the remaining rows, read from A directly.
+  // Returns the count kept (truncated to max_candidates in (-delta, i, j)
+  // order); with `always_sort` the kept list is in that order regardless.
+  __device__ void fc_append(int32_t i, int32_t j, double delta) {
+    AMVM_LOCALS
+    const int pos = atomicAdd(&sh->counter, 1);
+    if (pos < cap) cbuf[pos] = Cand{i, j, delta};
+  }
+
+  __device__ bool fc_rest(int64_t i, int32_t j, double delta, int nr, int g) {
+    AMVM_LOCALS
+    for (int q = g; q < nr; ++q) {
+      const int64_t rq = rows[q];
+      const double da = dsub(__ldg(At + (int64_t)j * m + rq), __ldg(At + i * m + rq));
+      const double bq = ddiv(reps[q], delta);
+      if (!(rsgn[q] ? (da < bq) : (da > -bq))) return false;
+    }
+    return true;
+  }
+
   __device__ int find_candidates(bool always_sort) {
+    AMVM_LOCALS
     const int nr = select_rows();
     const int g = nr < kG ? nr : kG;
     double *tb = (double *)scr;
@@ -551,11 +625,10 @@ struct Engine {
     int32_t *lst = tj + kTJ;
     int32_t *lfl = lst + (nlev + 1);
     double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
-    for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
-      const int64_t q = e / n, j = e - q * n;
-      const double a = __ldg(At + j * m + rows[q]);
-      ag[e] = rsgn[q] ? a : -a;
-    }
+    int32_t *perm = ibuf;                 // level-sorted position -> variable
+    int2 *que = (int2 *)(cbuf + cap);     // staged-row survivors awaiting the rest
+    const int qcap = (int)cap;
+    // level buckets
     for (int64_t k = tid; k <= nlev; k += NT) lfl[k] = 0;
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) atomicAdd(&lfl[cidx[j]], 1);
@@ -571,81 +644,114 @@ struct Engine {
       lst[nlev] = acc;
     }
     __syncthreads();
-    for (int64_t j = tid; j < n; j += NT) ibuf[atomicAdd(&lfl[cidx[j]], 1)] = (int32_t)j;
+    for (int64_t j = tid; j < n; j += NT) perm[atomicAdd(&lfl[cidx[j]], 1)] = (int32_t)j;
+    __syncthreads();
+    // staged rows in level-sorted order, sign folded: ag[q*n + pos]
+    for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
+      const int64_t q = e / n, ps = e - q * n;
+      const double a = __ldg(At + (int64_t)perm[ps] * m + rows[q]);
+      ag[e] = rsgn[q] ? a : -a;
+    }
+    const int ll = (int)(nlev * nlev);
     if (tab) {
-      const int ll = (int)(nlev * nlev);
       for (int e = tid; e < g * ll; e += NT) {
         const int q = e / ll, r2 = e - q * ll;
         const int ki = r2 / (int)nlev, kj = r2 - ki * (int)nlev;
         bt[e] = ki > kj ? ddiv(reps[q], dsub(lv[ki], lv[kj])) : 0.0;
       }
     }
-    if (tid == 0) sh->counter = 0;
+    if (tid == 0) {
+      sh->counter = 0;
+      sh->qcount = 0;
+    }
     __syncthreads();
-    const int ll = (int)(nlev * nlev);
+    // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
+    // with it every staged row's bound for a given j-bucket) is warp-uniform
+    const int64_t ngrp = (n + 31) / 32 + nlev;
     for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
       const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
       for (int64_t e = tid; e < p1 - p0; e += NT) {
-        const int32_t j = ibuf[p0 + e];
+        const int32_t j = perm[p0 + e];
         tj[e] = j;
         tl[e] = cidx[j];
 #pragma unroll
         for (int q = 0; q < kG; ++q)
-          if (q < g) tb[q * kTJ + e] = ag[(int64_t)q * n + j];
+          if (q < g) tb[q * kTJ + e] = ag[(int64_t)q * n + p0 + e];
       }
       __syncthreads();
-      for (int64_t i = warp; i < n; i += NW) {
-        const int ki = cidx[i];
-        const int64_t hi = (int64_t)lst[ki] < p1 ? (int64_t)lst[ki] : p1;
-        if (hi <= p0) continue;
+      // walk the groups: group index -> (bucket ki, chunk) by a running scan
+      int ki = 0;
+      int64_t gbase = 0;  // first group id of bucket ki
+      for (int64_t grp = warp; grp < ngrp; grp += NW) {
+        while (ki < nlev && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
+          gbase += (lst[ki + 1] - lst[ki] + 31) >> 5;
+          ++ki;
+        }
+        if (ki >= nlev) break;
+        if (ki == 0) continue;  // no level below the lowest
+        const int64_t hw = (int64_t)lst[ki] < p1 ? (int64_t)lst[ki] : p1;
+        if (hw <= p0) continue;
+        const int64_t ip = lst[ki] + (grp - gbase) * 32 + lane;
+        const bool have = ip < lst[ki + 1];
+        const int32_t i = have ? perm[ip] : 0;
         double bi[kG];
 #pragma unroll
-        for (int q = 0; q < kG; ++q) bi[q] = q < g ? ag[(int64_t)q * n + i] : 0.0;
+        for (int q = 0; q < kG; ++q) bi[q] = (have && q < g) ? ag[(int64_t)q * n + ip] : 0.0;
         const double xi = lv[ki];
-        for (int64_t base = p0; base < hi; base += 32) {
-          const int64_t pos = base + lane;
-          bool alive = pos < hi;
-          int kj = 0;
-          double delta = 0.0;
+        int kcur = -1;
+        double bq[kG], delta = 0.0;
+        for (int64_t pos = p0; pos < hw; ++pos) {
           const int e = (int)(pos - p0);
-          if (alive) {
-            kj = tl[e];
+          const int kj = tl[e];
+          if (kj != kcur) {  // warp-uniform: j positions are level-sorted
+            kcur = kj;
             delta = dsub(xi, lv[kj]);
-            if (g > 0) {
-              const double b0 = tab ? bt[ki * nlev + kj] : ddiv(reps[0], delta);
-              alive = dsub(tb[e], bi[0]) < b0;
-            }
-            if (alive && g > 1) {
-              const double b1 = tab ? bt[ll + ki * nlev + kj] : ddiv(reps[1], delta);
-              alive = dsub(tb[kTJ + e], bi[1]) < b1;
-            }
+#pragma unroll
+            for (int q = 0; q < kG; ++q)
+              bq[q] = q < g ? (tab ? bt[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta)) : 0.0;
           }
-          for (int q = 2; alive && q < nr; ++q) {
-            if (q < g) {
-              const double bq = tab ? bt[q * ll + ki * nlev + kj] : ddiv(reps[q], delta);
-              alive = dsub(tb[q * kTJ + e], bi[q]) < bq;
-            } else {
-              const int64_t rq = rows[q];
-              const int32_t j = tj[e];
-              const double da = dsub(__ldg(At + (int64_t)j * m + rq), __ldg(At + i * m + rq));
-              const double bq = ddiv(reps[q], delta);
-              alive = rsgn[q] ? (da < bq) : (da > -bq);
-            }
-          }
+          // all staged rows evaluated independently (no short-circuit): the
+          // loads issue together instead of as a predicated chain
+          bool alive = have;
+#pragma unroll
+          for (int q = 0; q < kG; ++q)
+            if (q < g) alive &= dsub(tb[q * kTJ + e], bi[q]) < bq[q];
           const unsigned bal = __ballot_sync(AMVM_FULL, alive);
           if (bal) {
-            int bse = 0;
-            if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
-            bse = __shfl_sync(AMVM_FULL, bse, 0);
-            if (alive) {
-              const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
-              if (pos2 < cap) cbuf[pos2] = Cand{(int32_t)i, tj[e], delta};
+            if (nr <= g) {
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
+              bse = __shfl_sync(AMVM_FULL, bse, 0);
+              if (alive) {
+                const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
+                if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
+              }
+            } else {
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
+              bse = __shfl_sync(AMVM_FULL, bse, 0);
+              if (alive) {
+                const int qp = bse + __popc(bal & ((1u << lane) - 1u));
+                if (qp < qcap) que[qp] = make_int2(i, tj[e]);
+                else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta);
+              }
             }
           }
         }
       }
       __syncthreads();
+      if (nr > g) {
+        const int qn = sh->qcount < qcap ? sh->qcount : qcap;
+        for (int e = tid; e < qn; e += NT) {
+          const int2 pr = que[e];
+          const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
+          if (fc_rest(pr.x, pr.y, delta, nr, g)) fc_append(pr.x, pr.y, delta);
+        }
+        __syncthreads();
+        if (tid == 0) sh->qcount = 0;
+      }
     }
+    __syncthreads();
     int cnt = sh->counter;
     __syncthreads();
     if (cnt > cap) {
@@ -664,11 +770,14 @@ struct Engine {
   // objective among strictly improving candidates, ties to the smallest
   // (i, j).  Returns found; the winner is uniform across the CTA.
   __device__ bool best_swap(int &bi, int &bj, double &bd, double &bt) {
+    AMVM_LOCALS
     if (!(cobj > 0.0)) return false;
     const long long tf0 = clock64();
     const int cnt = find_candidates(false);
     const long long tf1 = clock64();
-    pc[5] += tf1 - tf0;
+    if (tid == 0) sh->c.pc[5] += tf1 - tf0;
+    if (tid == 0) sh->c.pc[8] += 1;
+    if (tid == 0) sh->c.pc[9] += cnt;
     if (cnt == 0) return false;
     double wt = 0.0, wd = 0.0;
     int wi = -1, wj = -1;
@@ -689,15 +798,15 @@ struct Engine {
         wt = mx; wi = e.i; wj = e.j; wd = e.d;
       }
     }
-    mv_ref += cnt;
-    mv_raw += cnt;
+    if (tid == 0) sh->c.mv_ref += cnt;
+    if (tid == 0) sh->c.mv_raw += cnt;
     if (lane == 0) {
       sh->red[0][warp][0] = wt;
       sh->red[0][warp][1] = wd;
       sh->red[0][warp][2] = __longlong_as_double(((int64_t)wi << 32) | (uint32_t)wj);
     }
     __syncthreads();
-    pc[6] += clock64() - tf1;
+    if (tid == 0) sh->c.pc[6] += clock64() - tf1;
     bool found = false;
     for (int k = 0; k < NW; ++k) {
       const int64_t ij = __double_as_longlong(sh->red[0][k][2]);
@@ -714,6 +823,7 @@ struct Engine {
 
   // apply_swap, core.py:228-245, with the objective predicted by best_swap.
   __device__ void apply_swap_known(int i, int j, double d, double t) {
+    AMVM_LOCALS
     const double *ci = At + (int64_t)i * m;
     const double *cj = At + (int64_t)j * m;
     for (int64_t r = tid; r < m; r += NT) cr[r] = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
@@ -727,11 +837,13 @@ struct Engine {
 
   // local_search, localsearch.py:249-269
   __device__ void local_search() {
+    AMVM_LOCALS
     one_opt();
     for (int rd = 0; rd < prm->ls_max_rounds; ++rd) {
       int bi = -1, bj = -1;
       double bd = 0, bt = 0;
       if (!best_swap(bi, bj, bd, bt)) break;
+      if (tid == 0) sh->c.pc[10] += 1;
       apply_swap_known(bi, bj, bd, bt);
       one_opt();
     }
@@ -744,6 +856,7 @@ struct Engine {
   // computed by the whole CTA into an smem tile, then each column's owner
   // adds its tile column sequentially.
   __device__ void impact_scores(double alpha) {
+    AMVM_LOCALS
     __syncthreads();
     const double t = cobj;
     const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
@@ -777,6 +890,7 @@ struct Engine {
   // ------------------------------------------------------------- destroy
   // Generator.choice(pop, r, replace=False) on thread 0 -> out[0..r).
   __device__ void choice_noreplace(Pcg &g, int64_t pop, int64_t r, int32_t *out) {
+    AMVM_LOCALS
     if (pop > 10000 && r > pop / 50) {  // numpy tail-shuffle path
       for (int64_t i = 0; i < pop; ++i) ibuf[i] = (int32_t)i;
       const int64_t first = pop - r > 1 ? pop - r : 1;
@@ -827,6 +941,7 @@ struct Engine {
 
   // removed = sort(picked), saved = idx[removed]   (operators.py:29-31)
   __device__ void finish_destroy(int64_t r) {
+    AMVM_LOCALS
     if (tid == 0) {
       isort(pick, r);
       for (int64_t q = 0; q < r; ++q) {
@@ -839,6 +954,7 @@ struct Engine {
 
   // random_destroy, operators.py:34-39
   __device__ void random_destroy(int64_t r) {
+    AMVM_LOCALS
     __syncthreads();
     if (tid == 0) choice_noreplace(sh->rng, n, r, pick);
     finish_destroy(r);
@@ -846,11 +962,13 @@ struct Engine {
 
   // worst_remove_destroy, operators.py:77-105
   __device__ void worst_destroy(int64_t r, double alpha) {
+    AMVM_LOCALS
     if (!(cobj > 0.0)) {
       random_destroy(r);
       return;
     }
     impact_scores(alpha);
+    if (tid == 0) sh->c.pc[14] += 1;
     auto gd = [&](int64_t k) { return dbuf[k]; };
     if (block_pairwise(gd, n, lf_lo + nleaf_m, lf_len + nleaf_m, nleaf_n) <= 0.0) {
       random_destroy(r);
@@ -902,6 +1020,7 @@ struct Engine {
   // two_nearest, core.py:62-72: first two of a stable argsort of |lv - v|.
   // Every warp scans redundantly, so the result is uniform without a barrier.
   __device__ void two_nearest(double v, int &c1, int &c2) {
+    AMVM_LOCALS
     double bd = 0;
     int bk = 0x7fffffff;
     for (int k = lane; k < nlev; k += 32) {
@@ -931,6 +1050,7 @@ struct Engine {
   // random_repair, operators.py:108-117 (all r coins drawn up front: they are
   // consecutive in the stream — nothing else draws during a repair).
   __device__ void random_repair(const int32_t *rm, const int32_t *sv, int64_t r) {
+    AMVM_LOCALS
     __syncthreads();
     if (tid == 0)
       for (int64_t q = 0; q < r; ++q) coin[q] = (int32_t)pcg_bounded(sh->rng, 1);
@@ -944,6 +1064,7 @@ struct Engine {
 
   // greedy_repair, operators.py:120-138: the exact in-place sequence.
   __device__ void greedy_repair(const int32_t *rm, const int32_t *sv, int64_t r) {
+    AMVM_LOCALS
     __syncthreads();
     for (int64_t q = 0; q < r; ++q) {
       const int64_t j = rm[q];
@@ -953,8 +1074,8 @@ struct Engine {
       const double t1 = cobj;
       apply_shift_reduce(j, c2);
       const double t2 = cobj;
-      mv_ref += 2;
-      mv_raw += 2;
+      if (tid == 0) sh->c.mv_ref += 2;
+      if (tid == 0) sh->c.mv_raw += 2;
       if (t1 < t2 || (t1 == t2 && lv[c1] < lv[c2])) apply_shift_reduce(j, c1);
     }
   }
@@ -962,6 +1083,7 @@ struct Engine {
   // ------------------------------------------------------------ controller
   // accept, controller.py:168-183 (np.linalg.norm = sqrt of OpenBLAS ddot)
   __device__ bool accept() {
+    AMVM_LOCALS
     if (cobj < uobj) return true;
     if (prm->l2_tiebreak && cobj <= dadd(uobj, prm->accept_tie_tol)) {
       __syncthreads();
@@ -980,11 +1102,12 @@ struct Engine {
 
   // select_operators, controller.py:88-90 (thread 0)
   __device__ int select_pair() {
+    AMVM_LOCALS
     double s = 0.0;
-    for (int k = 0; k < 4; ++k) s = dadd(s, w[k]);  // pairwise_sum, n < 8
+    for (int k = 0; k < 4; ++k) s = dadd(s, sh->c.w[k]);  // pairwise_sum, n < 8
     double cdf[4], acc = 0.0;
     for (int k = 0; k < 4; ++k) {
-      acc = dadd(acc, ddiv(w[k], s));
+      acc = dadd(acc, ddiv(sh->c.w[k], s));
       cdf[k] = acc;
     }
     const double u = pcg_random(sh->rng);
@@ -999,24 +1122,27 @@ struct Engine {
 
   // update_weights, controller.py:99-131 (replicated in every thread)
   __device__ void update_weights(int pair, int outcome) {
+    AMVM_LOCALS
+    if (tid != 0) return;
     const double pts = outcome == 0 ? prm->sigma1 : outcome == 1 ? prm->sigma2 : outcome == 2 ? prm->sigma3 : 0.0;
-    sc[pair] = dadd(sc[pair], pts);
-    seg[pair] += 1;
-    life[pair] += 1;
-    bit += 1;
-    if (bit % prm->n_segment == 0) {
+    sh->c.sc[pair] = dadd(sh->c.sc[pair], pts);
+    sh->c.seg[pair] += 1;
+    sh->c.life[pair] += 1;
+    sh->c.bit += 1;
+    if (sh->c.bit % prm->n_segment == 0) {
       const double keep = dsub(1.0, prm->decay);
       for (int k = 0; k < 4; ++k) {
-        const double nrm = seg[k] > 0 ? ddiv(sc[k], (double)seg[k]) : 0.0;
-        const double v = dadd(dmul(prm->decay, w[k]), dmul(keep, nrm));
-        w[k] = v < prm->weight_floor ? prm->weight_floor : v;
-        sc[k] = 0.0;
-        seg[k] = 0;
+        const double nrm = sh->c.seg[k] > 0 ? ddiv(sh->c.sc[k], (double)sh->c.seg[k]) : 0.0;
+        const double v = dadd(dmul(prm->decay, sh->c.w[k]), dmul(keep, nrm));
+        sh->c.w[k] = v < prm->weight_floor ? prm->weight_floor : v;
+        sh->c.sc[k] = 0.0;
+        sh->c.seg[k] = 0;
       }
     }
   }
 
   __device__ void cand_from_cur() {
+    AMVM_LOCALS
     for (int64_t i = tid; i < m; i += NT) cr[i] = ur[i];
     for (int64_t j = tid; j < n; j += NT) cidx[j] = uidx[j];
     cobj = uobj;
@@ -1025,6 +1151,7 @@ struct Engine {
   }
 
   __device__ void cur_from_cand() {
+    AMVM_LOCALS
     for (int64_t i = tid; i < m; i += NT) ur[i] = cr[i];
     for (int64_t j = tid; j < n; j += NT) uidx[j] = cidx[j];
     uobj = cobj;
@@ -1032,6 +1159,7 @@ struct Engine {
   }
 
   __device__ void write_best(int64_t inst, const amvm_result &res) {
+    AMVM_LOCALS
     double *br = res.best.residual + inst * m;
     int32_t *bi = res.best.idx + inst * n;
     for (int64_t i = tid; i < m; i += NT) br[i] = ur[i];
@@ -1051,65 +1179,64 @@ struct Engine {
     tid = threadIdx.x;
     lane = tid & 31;
     warp = tid >> 5;
-    m = a.m;
-    n = a.n;
-    nlev = a.nlev;
-    At = a.At;
-    prm = &a.prm;
-    cap = a.cap;
-    tab = a.tab;
-    const SlotLayout L = slot_layout(m, n, a.prm.k_eps, a.prm.r, a.cap);
-    kk = L.kk;
-    unsigned char *base = a.ws + sizeof(WsHeader) + (size_t)slot * a.slot_bytes;
-    status = (int32_t *)a.ws;
-    ur = (double *)(base + L.ur);
-    uidx = (int32_t *)(base + L.uidx);
-    cidx = (int32_t *)(base + L.cidx);
-    dmv = (double *)(base + L.dmv);
-    dpv = (double *)(base + L.dpv);
-    dbuf = (double *)(base + L.dbuf);
-    pbuf = (double *)(base + L.pbuf);
-    lf_lo = (int64_t *)(base + L.lf_lo);
-    lf_len = (int64_t *)(base + L.lf_len);
-    lf_sum = (double *)(base + L.lf_sum);
-    rows = (int32_t *)(base + L.rows);
-    reps = (double *)(base + L.reps);
-    rsgn = (int32_t *)(base + L.rsgn);
-    ag = (double *)(base + L.ag);
-    cbuf = (Cand *)(base + L.cbuf);
-    hset = (uint64_t *)(base + L.hset);
-    rem = (int32_t *)(base + L.rem);
-    sav = (int32_t *)(base + L.sav);
-    pick = (int32_t *)(base + L.pick);
-    coin = (int32_t *)(base + L.coin);
-    ibuf = (int32_t *)(base + L.ibuf);
-    // dynamic smem: Shared | lv | scratch | cr
-    size_t o = sizeof(Shared<NT>);
     sh = (Shared<NT> *)smem;
-    lv = (double *)(smem + o);
-    o += 8 * ((nlev + 1) & ~1);
-    scr = smem + o;
-    o += scratch_bytes(nlev, tab);
-    cr = a.cr_smem ? (double *)(smem + o) : (double *)(base + L.crg);
-    // leaf trees for m and n (fixed per problem)
     if (tid == 0) {
-      nleaf_m = pw_leaves(m, lf_lo, lf_len, (int)L.nleaf);
-      sh->bc_i[2] = nleaf_m;
-      sh->bc_i[3] = pw_leaves(n, lf_lo + nleaf_m, lf_len + nleaf_m, (int)(2 * L.nleaf - nleaf_m));
+      Ctx &c = sh->c;
+      c.m = a.m;
+      c.n = a.n;
+      c.nlev = a.nlev;
+      c.At = a.At;
+      c.prm = a.prm;
+      c.cap = a.cap;
+      c.tab = a.tab;
+      const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap);
+      c.kk = L.kk;
+      unsigned char *base = a.ws + sizeof(WsHeader) + (size_t)slot * a.slot_bytes;
+      c.status = (int32_t *)a.ws;
+      c.ur = (double *)(base + L.ur);
+      c.uidx = (int32_t *)(base + L.uidx);
+      c.cidx = (int32_t *)(base + L.cidx);
+      c.dmv = (double *)(base + L.dmv);
+      c.dpv = (double *)(base + L.dpv);
+      c.dbuf = (double *)(base + L.dbuf);
+      c.pbuf = (double *)(base + L.pbuf);
+      c.lf_lo = (int64_t *)(base + L.lf_lo);
+      c.lf_len = (int64_t *)(base + L.lf_len);
+      c.lf_sum = (double *)(base + L.lf_sum);
+      c.rows = (int32_t *)(base + L.rows);
+      c.reps = (double *)(base + L.reps);
+      c.rsgn = (int32_t *)(base + L.rsgn);
+      c.ag = (double *)(base + L.ag);
+      c.cbuf = (Cand *)(base + L.cbuf);
+      c.hset = (uint64_t *)(base + L.hset);
+      c.rem = (int32_t *)(base + L.rem);
+      c.sav = (int32_t *)(base + L.sav);
+      c.pick = (int32_t *)(base + L.pick);
+      c.coin = (int32_t *)(base + L.coin);
+      c.ibuf = (int32_t *)(base + L.ibuf);
+      // dynamic smem: Shared | lv | scratch | cr
+      size_t o = sizeof(Shared<NT>);
+      c.lv = (double *)(smem + o);
+      o += 8 * ((a.nlev + 1) & ~1);
+      c.scr = smem + o;
+      o += scratch_bytes(a.nlev, a.tab);
+      c.cr = a.cr_smem ? (double *)(smem + o) : (double *)(base + L.crg);
+      // leaf trees of numpy's pairwise sum for lengths m and n
+      c.nleaf_m = pw_leaves(a.m, c.lf_lo, c.lf_len, (int)L.nleaf);
+      c.nleaf_n = pw_leaves(a.n, c.lf_lo + c.nleaf_m, c.lf_len + c.nleaf_m, (int)(2 * L.nleaf - c.nleaf_m));
     }
-    __syncthreads();
-    nleaf_m = sh->bc_i[2];
-    nleaf_n = sh->bc_i[3];
     __syncthreads();
   }
 
   __device__ void load_levels(const KArgs &a, int64_t inst) {
-    b = a.B + inst * m;
+    AMVM_LOCALS
+    if (tid == 0) sh->c.b = a.B + inst * m;
     for (int64_t k = tid; k < nlev; k += NT) lv[k] = a.levels[inst * nlev + k];
     __syncthreads();
   }
 
   __device__ void load_rng(const amvm_pcg64 *st) {
+    AMVM_LOCALS
     if (tid == 0) {
       sh->rng.s = ((unsigned __int128)st->state_hi << 64) | st->state_lo;
       sh->rng.inc = ((unsigned __int128)st->inc_hi << 64) | st->inc_lo;
@@ -1119,6 +1246,7 @@ struct Engine {
   }
 
   __device__ void store_rng(amvm_pcg64 *st) {
+    AMVM_LOCALS
     if (tid == 0) {
       st->state_hi = (uint64_t)(sh->rng.s >> 64);
       st->state_lo = (uint64_t)sh->rng.s;
@@ -1132,6 +1260,7 @@ struct Engine {
   // ------------------------------------------------------- solve (one inst)
   // solve, controller.py:211-286, from the host-computed initial solution.
   __device__ void solve_instance(const KArgs &a, int64_t inst) {
+    AMVM_LOCALS
     load_levels(a, inst);
     const amvm_result &res = a.res;
     for (int64_t i = tid; i < m; i += NT) ur[i] = a.s_r[inst * m + i];
@@ -1141,12 +1270,16 @@ struct Engine {
     __syncthreads();
     write_best(inst, res);
     load_rng(&a.rng[inst]);
-    for (int k = 0; k < 4; ++k) {
-      w[k] = 1.0; sc[k] = 0.0; seg[k] = 0; life[k] = 0;
+    if (tid == 0) {
+      for (int k = 0; k < 4; ++k) {
+        sh->c.w[k] = 1.0; sh->c.sc[k] = 0.0; sh->c.seg[k] = 0; sh->c.life[k] = 0;
+      }
+      sh->c.bit = 0;
     }
-    bit = 0;
-    mv_ref = mv_raw = 0;
-    for (int k = 0; k < 8; ++k) pc[k] = 0;
+    if (tid == 0) {
+      sh->c.mv_ref = sh->c.mv_raw = 0;
+      for (int k = 0; k < 16; ++k) sh->c.pc[k] = 0;
+    }
     const int64_t r = a.prm.r;
     const int T = a.prm.max_iters;
     const uint64_t t_start = gtimer();
@@ -1168,16 +1301,16 @@ struct Engine {
       ++it;
       if (!cand_is_cur) cand_from_cur();
       cand_is_cur = false;
-      tq = clock64(); pc[0] += tq - tp; tp = tq;
+      tq = clock64(); if (tid == 0) sh->c.pc[0] += tq - tp; tp = tq;
       if (pair < 2) random_destroy(r);
       else worst_destroy(r, a.prm.alpha);
-      tq = clock64(); pc[pair < 2 ? 1 : 2] += tq - tp; tp = tq;
+      tq = clock64(); if (tid == 0) sh->c.pc[pair < 2 ? 1 : 2] += tq - tp; tp = tq;
       if (pair & 1) greedy_repair(rem, sav, r);
       else random_repair(rem, sav, r);
-      tq = clock64(); pc[3] += tq - tp; tp = tq;
-      const long long fc0 = pc[5] + pc[6];
+      tq = clock64(); if (tid == 0) sh->c.pc[3] += tq - tp; tp = tq;
+      const long long fc0 = sh->c.pc[5] + sh->c.pc[6];
       local_search();
-      tq = clock64(); pc[4] += (tq - tp) - (pc[5] + pc[6] - fc0); tp = tq;
+      tq = clock64(); if (tid == 0) sh->c.pc[4] += (tq - tp) - (sh->c.pc[5] + sh->c.pc[6] - fc0); tp = tq;
       const bool acc = accept();
       int outcome;
       if (acc && cobj < bobj) outcome = 0;
@@ -1198,20 +1331,20 @@ struct Engine {
         res.trace_pair[o] = (uint8_t)pair;
         res.trace_accepted[o] = (uint8_t)acc;
       }
-      pc[7] += clock64() - tp;
+      if (tid == 0) sh->c.pc[7] += clock64() - tp;
     }
     if (tid == 0) {
       res.best.objective[inst] = bobj;
       res.best.updates[inst] = bcnt;
       res.initial_objective[inst] = a.s_obj[inst];
       res.iterations[inst] = it;
-      for (int k = 0; k < 4; ++k) res.operator_uses[inst * 4 + k] = life[k];
+      for (int k = 0; k < 4; ++k) res.operator_uses[inst * 4 + k] = sh->c.life[k];
       if (res.moves_scored) {
-        res.moves_scored[2 * inst] = mv_ref;
-        res.moves_scored[2 * inst + 1] = mv_raw;
+        res.moves_scored[2 * inst] = sh->c.mv_ref;
+        res.moves_scored[2 * inst + 1] = sh->c.mv_raw;
       }
       if (res.phase_cycles)
-        for (int k = 0; k < 8; ++k) res.phase_cycles[8 * inst + k] = pc[k];
+        for (int k = 0; k < 16; ++k) res.phase_cycles[16 * inst + k] = sh->c.pc[k];
     }
     store_rng(&a.rng[inst]);
     __syncthreads();
@@ -1219,17 +1352,21 @@ struct Engine {
 
   // ------------------------------------------------- component operations
   __device__ void load_sol(const KArgs &a) {
+    AMVM_LOCALS
     load_levels(a, 0);
     for (int64_t i = tid; i < m; i += NT) cr[i] = a.s_r[i];
     for (int64_t j = tid; j < n; j += NT) cidx[j] = a.s_idx[j];
     cobj = a.s_obj[0];
     ccnt = a.s_cnt[0];
-    mv_ref = mv_raw = 0;
-    for (int k = 0; k < 8; ++k) pc[k] = 0;
+    if (tid == 0) {
+      sh->c.mv_ref = sh->c.mv_raw = 0;
+      for (int k = 0; k < 16; ++k) sh->c.pc[k] = 0;
+    }
     __syncthreads();
   }
 
   __device__ void store_sol(const KArgs &a) {
+    AMVM_LOCALS
     __syncthreads();
     for (int64_t i = tid; i < m; i += NT) a.s_r[i] = cr[i];
     for (int64_t j = tid; j < n; j += NT) a.s_idx[j] = cidx[j];
@@ -1240,6 +1377,7 @@ struct Engine {
   }
 
   __device__ void run_op(const KArgs &a) {
+    AMVM_LOCALS
     load_sol(a);
     switch (a.op) {
       case OP_ONE_OPT:

@@ -54,8 +54,6 @@ class LayerBatch:
             raise ValueError("X and W must be float64")
         if X_t.dim() != 2 or W_t.dim() != 2 or X_t.shape[1] != W_t.shape[1]:
             raise ValueError("X must be calib x d and W rows x d")
-        if not (bool(torch.isfinite(X_t).all()) and bool(torch.isfinite(W_t).all())):
-            raise ValueError("A and b must be finite")
         self.m, self.n = int(X_t.shape[0]), int(X_t.shape[1])
         self.rows = np.arange(W_t.shape[0]) if rows is None else np.asarray(rows)
         self.count = int(self.rows.size)
@@ -67,6 +65,9 @@ class LayerBatch:
         self.At = X_t.to(dev, non_blocking=True).t().contiguous()
         Wsel = W_t if rows is None else W_t[torch.as_tensor(self.rows)]
         self.W = Wsel.to(dev, non_blocking=True).contiguous()
+        # Instance validation (core.py:93-94), done on the device copies
+        if not bool(torch.isfinite(self.At).all() & torch.isfinite(self.W).all()):
+            raise ValueError("A and b must be finite")
         f64, i32 = torch.float64, torch.int32
         self.B = torch.empty((self.count, self.m), dtype=f64, device=dev)
         self.L = torch.empty((self.count, self.nlev), dtype=f64, device=dev)
@@ -112,7 +113,7 @@ class LayerBatch:
             "iterations": torch.empty(c, dtype=torch.int32, device=dev),
             "operator_uses": torch.empty((c, 4), dtype=torch.int64, device=dev),
             "moves_scored": torch.empty((c, 2), dtype=torch.int64, device=dev),
-            "phase_cycles": torch.empty((c, 8), dtype=torch.int64, device=dev),
+            "phase_cycles": torch.empty((c, 16), dtype=torch.int64, device=dev),
         }
         tr = [None] * 4
         if trace:
