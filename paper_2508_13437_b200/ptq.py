@@ -199,7 +199,10 @@ def gather_layer(rep: LayerReport, total_rows: int, group=None) -> LayerReport |
         return out
 
     payload = [
-        pad(rep.rows, 1, torch.int64), pad(rep.codes.astype(np.int16), n, torch.int16),
+        pad(rep.rows, 1, torch.int64),
+        # codes travel as uint8 for <= 256 levels (int4: 58.7 MB for all of C5), else int32
+        (pad(rep.codes.astype(np.uint8), n, torch.uint8) if nlev <= 256
+         else pad(rep.codes.astype(np.int32), n, torch.int32)),
         pad(rep.levels, nlev, torch.float64), pad(rep.objective, 1, torch.float64),
         pad(rep.initial_objective, 1, torch.float64), pad(rep.iterations, 1, torch.int64),
         pad(rep.moves_scored, 2, torch.int64),
