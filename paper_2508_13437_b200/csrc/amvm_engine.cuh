@@ -79,7 +79,7 @@ struct WsHeader {
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
   size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
-      hset, rem, sav, pick, coin, ibuf, total;
+      hset, rem, sav, pick, coin, ibuf, srt, total;
   int64_t nleaf, kk, hsz;
 };
 
@@ -121,6 +121,11 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.pick = o; o = al256(o + 4 * rr);
   L.coin = o; o = al256(o + 4 * rr);
   L.ibuf = o; o = al256(o + 4 * (n > L.kk ? n : L.kk));
+  {
+    int64_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    L.srt = o; o = al256(o + 16 * n2);  // bucket sort: (level, b0, j) per position
+  }
   L.total = o;
   return L;
 }
@@ -143,6 +148,7 @@ struct Ctx {
   Cand *cbuf;
   uint64_t *hset;
   int32_t *rem, *sav, *pick, *coin, *ibuf;
+  unsigned char *srt;
   int32_t *status;
   amvm_params prm;
   // operator bank (controller.py:71-85) and counters: thread 0 owns these
@@ -183,6 +189,7 @@ struct Ctx {
   [[maybe_unused]] int32_t *const pick = sh->c.pick;                                      \
   [[maybe_unused]] int32_t *const coin = sh->c.coin;                                      \
   [[maybe_unused]] int32_t *const ibuf = sh->c.ibuf;                                      \
+  [[maybe_unused]] unsigned char *const srt = sh->c.srt;                                   \
   [[maybe_unused]] int32_t *const status = sh->c.status;                                  \
   [[maybe_unused]] const amvm_params *const prm = &sh->c.prm;
 
@@ -646,6 +653,49 @@ struct Engine {
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) perm[atomicAdd(&lfl[cidx[j]], 1)] = (int32_t)j;
     __syncthreads();
+    // sort every level bucket by the tightest row's folded value b0 (eps_0 = 0:
+    // that row defines t), so each i's row-0 survivors in a bucket are a prefix
+    {
+      int64_t n2 = 1;
+      while (n2 < n) n2 <<= 1;
+      int32_t *sl = (int32_t *)srt;
+      int32_t *sj = sl + n2;
+      double *sb = (double *)(sj + n2);
+      for (int64_t e = tid; e < n2; e += NT) {
+        if (e < n) {
+          const int32_t j = perm[e];
+          const double a = __ldg(At + (int64_t)j * m + rows[0]);
+          sl[e] = cidx[j];
+          sj[e] = j;
+          sb[e] = rsgn[0] ? a : -a;
+        } else {
+          sl[e] = 0x7fffffff;
+          sj[e] = 0;
+          sb[e] = 0.0;
+        }
+      }
+      __syncthreads();
+      for (int64_t k = 2; k <= n2; k <<= 1) {
+        for (int64_t jj = k >> 1; jj > 0; jj >>= 1) {
+          for (int64_t e = tid; e < n2; e += NT) {
+            const int64_t x = e ^ jj;
+            if (x > e) {
+              const int32_t la = sl[e], lb = sl[x];
+              const double ba = sb[e], bb = sb[x];
+              const bool gt = la > lb || (la == lb && (ba > bb || (ba == bb && sj[e] > sj[x])));
+              if (((e & k) == 0) == gt) {
+                sl[e] = lb; sl[x] = la;
+                sb[e] = bb; sb[x] = ba;
+                const int32_t t0 = sj[e]; sj[e] = sj[x]; sj[x] = t0;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int64_t e = tid; e < n; e += NT) perm[e] = sj[e];
+      __syncthreads();
+    }
     // staged rows in level-sorted order, sign folded: ag[q*n + pos]
     for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
       const int64_t q = e / n, ps = e - q * n;
@@ -666,7 +716,8 @@ struct Engine {
     }
     __syncthreads();
     // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
-    // with it every staged row's bound for a given j-bucket) is warp-uniform
+    // with it every staged row's bound for a given j-bucket) is warp-uniform;
+    // within a bucket the lanes' b0 ascend, so their prefixes nest
     const int64_t ngrp = (n + 31) / 32 + nlev;
     for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
       const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
@@ -679,7 +730,6 @@ struct Engine {
           if (q < g) tb[q * kTJ + e] = ag[(int64_t)q * n + p0 + e];
       }
       __syncthreads();
-      // walk the groups: group index -> (bucket ki, chunk) by a running scan
       int ki = 0;
       int64_t gbase = 0;  // first group id of bucket ki
       for (int64_t grp = warp; grp < ngrp; grp += NW) {
@@ -689,8 +739,7 @@ struct Engine {
         }
         if (ki >= nlev) break;
         if (ki == 0) continue;  // no level below the lowest
-        const int64_t hw = (int64_t)lst[ki] < p1 ? (int64_t)lst[ki] : p1;
-        if (hw <= p0) continue;
+        if ((int64_t)lst[ki] <= p0) continue;  // no lower-level position in this tile
         const int64_t ip = lst[ki] + (grp - gbase) * 32 + lane;
         const bool have = ip < lst[ki + 1];
         const int32_t i = have ? perm[ip] : 0;
@@ -698,42 +747,57 @@ struct Engine {
 #pragma unroll
         for (int q = 0; q < kG; ++q) bi[q] = (have && q < g) ? ag[(int64_t)q * n + ip] : 0.0;
         const double xi = lv[ki];
-        int kcur = -1;
-        double bq[kG], delta = 0.0;
-        for (int64_t pos = p0; pos < hw; ++pos) {
-          const int e = (int)(pos - p0);
-          const int kj = tl[e];
-          if (kj != kcur) {  // warp-uniform: j positions are level-sorted
-            kcur = kj;
-            delta = dsub(xi, lv[kj]);
-#pragma unroll
-            for (int q = 0; q < kG; ++q)
-              bq[q] = q < g ? (tab ? bt[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta)) : 0.0;
-          }
-          // all staged rows evaluated independently (no short-circuit): the
-          // loads issue together instead of as a predicated chain
-          bool alive = have;
+        for (int kj = 0; kj < ki; ++kj) {
+          const int64_t s0 = (int64_t)lst[kj] > p0 ? (int64_t)lst[kj] : p0;
+          const int64_t s1 = (int64_t)lst[kj + 1] < p1 ? (int64_t)lst[kj + 1] : p1;
+          if (s0 >= s1) continue;
+          const double delta = dsub(xi, lv[kj]);
+          double bq[kG];
 #pragma unroll
           for (int q = 0; q < kG; ++q)
-            if (q < g) alive &= dsub(tb[q * kTJ + e], bi[q]) < bq[q];
-          const unsigned bal = __ballot_sync(AMVM_FULL, alive);
-          if (bal) {
-            if (nr <= g) {
-              int bse = 0;
-              if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
-              bse = __shfl_sync(AMVM_FULL, bse, 0);
-              if (alive) {
-                const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
-                if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
-              }
-            } else {
-              int bse = 0;
-              if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
-              bse = __shfl_sync(AMVM_FULL, bse, 0);
-              if (alive) {
-                const int qp = bse + __popc(bal & ((1u << lane) - 1u));
-                if (qp < qcap) que[qp] = make_int2(i, tj[e]);
-                else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta);
+            bq[q] = q < g ? (tab ? bt[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta)) : 0.0;
+          // row 0 as a prefix: first position where dsub(b0_j, b0_i) < bq0 fails
+          int64_t lo = s0, hi = s1;
+          if (have) {
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              if (dsub(tb[mid - p0], bi[0]) < bq[0]) lo = mid + 1;
+              else hi = mid;
+            }
+          } else {
+            lo = s0;
+          }
+          const int64_t mine = lo;
+          int64_t wend = mine;
+          for (int o = 16; o; o >>= 1) {
+            const int64_t v = __shfl_xor_sync(AMVM_FULL, wend, o);
+            wend = v > wend ? v : wend;
+          }
+          for (int64_t pos = s0; pos < wend; ++pos) {
+            const int e = (int)(pos - p0);
+            bool alive = pos < mine;
+#pragma unroll
+            for (int q = 1; q < kG; ++q)
+              if (q < g) alive &= dsub(tb[q * kTJ + e], bi[q]) < bq[q];
+            const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+            if (bal) {
+              if (nr <= g) {
+                int bse = 0;
+                if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
+                bse = __shfl_sync(AMVM_FULL, bse, 0);
+                if (alive) {
+                  const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
+                  if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
+                }
+              } else {
+                int bse = 0;
+                if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
+                bse = __shfl_sync(AMVM_FULL, bse, 0);
+                if (alive) {
+                  const int qp = bse + __popc(bal & ((1u << lane) - 1u));
+                  if (qp < qcap) que[qp] = make_int2(i, tj[e]);
+                  else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta);
+                }
               }
             }
           }
@@ -1214,6 +1278,7 @@ struct Engine {
       c.pick = (int32_t *)(base + L.pick);
       c.coin = (int32_t *)(base + L.coin);
       c.ibuf = (int32_t *)(base + L.ibuf);
+      c.srt = base + L.srt;
       // dynamic smem: Shared | lv | scratch | cr
       size_t o = sizeof(Shared<NT>);
       c.lv = (double *)(smem + o);
