@@ -73,6 +73,38 @@ __device__ __forceinline__ uint64_t pcg_bounded(Pcg &g, uint64_t rng) {
   return m >> 32;
 }
 
+
+// ----------------------------------------------------- exp for x <= 0
+// Table-driven exp (Tang, ACM TOMS 15, 1989): x = (32m + j) ln2/32 + r,
+// |r| <= ln2/64, exp(x) = 2^m 2^(j/32) (1 + expm1(r)), 2^(j/32) as hi+lo,
+// expm1 by its degree-6 Taylor polynomial (truncation < 4e-18).  <= ~0.52 ulp,
+// i.e. the same accuracy class as numpy's SIMD exp and libm (neither is
+// bit-reproducible here), at ~1/3 of CUDA's generic exp cost.
+__device__ const double kExpHi[32] = {0x1.0000000000000p+0, 0x1.059b0d3158574p+0, 0x1.0b5586cf9890fp+0, 0x1.11301d0125b51p+0, 0x1.172b83c7d517bp+0, 0x1.1d4873168b9aap+0, 0x1.2387a6e756238p+0, 0x1.29e9df51fdee1p+0, 0x1.306fe0a31b715p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123422p+0, 0x1.44e086061892dp+0, 0x1.4bfdad5362a27p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd485429p+0, 0x1.6247eb03a5585p+0, 0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0, 0x1.8ace5422aa0dbp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f090p+0, 0x1.a5503b23e255dp+0, 0x1.ae89f995ad3adp+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529cp+0, 0x1.cb720dcef9069p+0, 0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0};
+__device__ const double kExpLo[32] = {0x0.0p+0, 0x1.d73e2a475b465p-55, 0x1.8a62e4adc610bp-54, -0x1.6c51039449b3ap-54, -0x1.19041b9d78a76p-55, 0x1.e016e00a2643cp-54, 0x1.9b07eb6c70573p-54, 0x1.612e8afad1255p-55, 0x1.6f46ad23182e4p-55, -0x1.63aeabf42eae2p-54, 0x1.ada0911f09ebcp-55, 0x1.89b7a04ef80d0p-59, 0x1.d4397afec42e2p-56, -0x1.07abe1db13cadp-55, 0x1.6324c054647adp-54, -0x1.383c17e40b497p-54, -0x1.bdd3413b26456p-54, -0x1.16e4786887a99p-55, -0x1.41577ee04992fp-55, -0x1.d4c1dd41532d8p-54, 0x1.6e9f156864b27p-54, -0x1.75fc781b57ebcp-57, 0x1.c7c46b071f2bep-56, -0x1.d2f6edb8d41e1p-54, 0x1.7a1cd345dcc81p-54, -0x1.5584f7e54ac3bp-56, 0x1.11065895048ddp-55, 0x1.503cbd1e949dbp-56, 0x1.2ed02d75b3707p-55, -0x1.1a5cd4f184b5cp-54, -0x1.e9c23179c2893p-54, 0x1.9d3e12dd8a18bp-54};
+
+__device__ __forceinline__ double exp_nonpos(double x) {
+  if (x < -745.1332191019412) return 0.0;  // below the smallest subnormal
+  const double kInv = 0x1.71547652b82fep+5;   // 32/ln2
+  const double kMagic = 0x1.8p52;
+  const double kL1 = 0x1.62e4200000000p-6;    // ln2/32, 20 bits: kd*kL1 exact
+  const double kL2 = 0x1.fdf473de6af28p-27;
+  const double kd = dsub(dadd(dmul(x, kInv), kMagic), kMagic);
+  const int k = (int)kd;
+  double r = dfma(kd, -kL1, x);
+  r = dfma(kd, -kL2, r);
+  double p = dfma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = dfma(p, r, 1.0 / 24.0);
+  p = dfma(p, r, 1.0 / 6.0);
+  p = dfma(p, r, 0.5);
+  p = dfma(dmul(r, r), p, r);  // expm1(r)
+  const int j = k & 31, m = k >> 5;
+  const double th = __ldg(&kExpHi[j]), tl = __ldg(&kExpLo[j]);
+  const double res = dadd(th, dfma(th, p, dfma(tl, p, tl)));
+  if (m >= -1022) return dmul(res, __longlong_as_double((long long)(m + 1023) << 52));
+  return dmul(dmul(res, __longlong_as_double((long long)(m + 600 + 1023) << 52)), 0x1p-600);
+}
+
 // --------------------------------------------------------------- warp ops
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll

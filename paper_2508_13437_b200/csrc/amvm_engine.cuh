@@ -28,7 +28,7 @@ constexpr int kWin = 8;        // one_opt speculative window (columns per barrie
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
-constexpr int kTC = 128;       // impact tile: columns
+constexpr int kTC = 256;       // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
 
 // Phase-shared smem scratch: the impact tile or the find_candidates tiles.
@@ -36,7 +36,7 @@ __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
   size_t fc = 8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2);
   fc = (fc + 15) & ~(size_t)15;
   if (tab) fc += 8 * kG * nlev * nlev;
-  size_t imp = 8 * kTC * (kTK + 1);
+  size_t imp = 8 * kTC * (kTK + 1) + 16 * kTK;
   return fc > imp ? fc : imp;
 }
 
@@ -44,6 +44,11 @@ struct Cand {
   int32_t i, j;
   double d;
 };
+
+// The kernel's dynamic shared memory.  Engine pointers into it are derived
+// from this symbol (not stored), so the compiler keeps them in the shared
+// address space (LDS/STS with immediate offsets instead of generic LD/ST).
+extern __shared__ __align__(16) unsigned char amvm_dyn_smem[];
 
 // Everything a kernel launch needs, passed by value.
 struct KArgs {
@@ -78,7 +83,7 @@ struct WsHeader {
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
-  size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
+  size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, cbk, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
       hset, rem, sav, pick, coin, ibuf, srt, total;
   int64_t nleaf, kk, hsz;
 };
@@ -107,6 +112,7 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.dpv = o; o = al256(o + 8 * n);
   L.dbuf = o; o = al256(o + 8 * n);
   L.pbuf = o; o = al256(o + 8 * n);
+  L.cbk = o; o = al256(o + 8 * ((n + 31) / 32 + 2));
   L.lf_lo = o; o = al256(o + 16 * L.nleaf);
   L.lf_len = o; o = al256(o + 16 * L.nleaf);
   L.lf_sum = o; o = al256(o + 8 * L.nleaf);
@@ -136,15 +142,15 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
 struct Ctx {
   int64_t m, n, nlev, kk, cap;
   const double *At, *b;
-  double *lv, *cr, *ur;
+  double *cr, *ur;
   int32_t *cidx, *uidx;
-  double *dmv, *dpv, *dbuf, *pbuf;
+  double *dmv, *dpv, *dbuf, *pbuf, *cbk;
   int64_t *lf_lo, *lf_len;
   double *lf_sum;
   int nleaf_m, nleaf_n, tab;
   int32_t *rows, *rsgn;
   double *reps, *ag;
-  unsigned char *scr;
+  uint32_t off_lv, off_scr;
   Cand *cbuf;
   uint64_t *hset;
   int32_t *rem, *sav, *pick, *coin, *ibuf;
@@ -163,7 +169,7 @@ struct Ctx {
   [[maybe_unused]] const int64_t kk = sh->c.kk, cap = sh->c.cap;                          \
   [[maybe_unused]] const double *const At = sh->c.At;                                     \
   [[maybe_unused]] const double *const b = sh->c.b;                                       \
-  [[maybe_unused]] double *const lv = sh->c.lv;                                           \
+  [[maybe_unused]] double *const lv = (double *)(amvm_dyn_smem + sh->c.off_lv);            \
   [[maybe_unused]] double *const cr = sh->c.cr;                                           \
   [[maybe_unused]] double *const ur = sh->c.ur;                                           \
   [[maybe_unused]] int32_t *const cidx = sh->c.cidx;                                      \
@@ -172,6 +178,7 @@ struct Ctx {
   [[maybe_unused]] double *const dpv = sh->c.dpv;                                         \
   [[maybe_unused]] double *const dbuf = sh->c.dbuf;                                       \
   [[maybe_unused]] double *const pbuf = sh->c.pbuf;                                       \
+  [[maybe_unused]] double *const cbk = sh->c.cbk;                                         \
   [[maybe_unused]] int64_t *const lf_lo = sh->c.lf_lo;                                    \
   [[maybe_unused]] int64_t *const lf_len = sh->c.lf_len;                                  \
   [[maybe_unused]] double *const lf_sum = sh->c.lf_sum;                                   \
@@ -181,7 +188,7 @@ struct Ctx {
   [[maybe_unused]] int32_t *const rsgn = sh->c.rsgn;                                      \
   [[maybe_unused]] double *const reps = sh->c.reps;                                       \
   [[maybe_unused]] double *const ag = sh->c.ag;                                           \
-  [[maybe_unused]] unsigned char *const scr = sh->c.scr;                                  \
+  [[maybe_unused]] unsigned char *const scr = amvm_dyn_smem + sh->c.off_scr;               \
   [[maybe_unused]] Cand *const cbuf = sh->c.cbuf;                                         \
   [[maybe_unused]] uint64_t *const hset = sh->c.hset;                                     \
   [[maybe_unused]] int32_t *const rem = sh->c.rem;                                        \
@@ -773,32 +780,47 @@ struct Engine {
             const int64_t v = __shfl_xor_sync(AMVM_FULL, wend, o);
             wend = v > wend ? v : wend;
           }
-          for (int64_t pos = s0; pos < wend; ++pos) {
-            const int e = (int)(pos - p0);
-            bool alive = pos < mine;
-#pragma unroll
-            for (int q = 1; q < kG; ++q)
-              if (q < g) alive &= dsub(tb[q * kTJ + e], bi[q]) < bq[q];
+          const int e0 = (int)(s0 - p0), e1 = (int)(wend - p0), emine = (int)(mine - p0);
+          // survivors of the staged rows: straight into the candidate list when
+          // they are all the rows, else into the queue for the remaining rows
+          auto emit = [&](int e, bool alive) {
             const unsigned bal = __ballot_sync(AMVM_FULL, alive);
-            if (bal) {
-              if (nr <= g) {
-                int bse = 0;
-                if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
-                bse = __shfl_sync(AMVM_FULL, bse, 0);
-                if (alive) {
-                  const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
-                  if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
-                }
-              } else {
-                int bse = 0;
-                if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
-                bse = __shfl_sync(AMVM_FULL, bse, 0);
-                if (alive) {
-                  const int qp = bse + __popc(bal & ((1u << lane) - 1u));
-                  if (qp < qcap) que[qp] = make_int2(i, tj[e]);
-                  else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta);
-                }
+            if (!bal) return;
+            if (nr <= g) {
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
+              bse = __shfl_sync(AMVM_FULL, bse, 0);
+              if (alive) {
+                const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
+                if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
               }
+            } else {
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
+              bse = __shfl_sync(AMVM_FULL, bse, 0);
+              if (alive) {
+                const int qp = bse + __popc(bal & ((1u << lane) - 1u));
+                if (qp < qcap) que[qp] = make_int2(i, tj[e]);
+                else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta);
+              }
+            }
+          };
+          if (g == kG) {  // common case: every staged row present, no per-row predicates
+            for (int e = e0; e < e1; ++e) {
+              const double *tq = tb + e;
+              bool alive = e < emine;
+#pragma unroll
+              for (int q = 1; q < kG; ++q) alive &= dsub(tq[q * kTJ], bi[q]) < bq[q];
+              emit(e, alive);
+            }
+          } else {
+            for (int e = e0; e < e1; ++e) {
+              const double *tq = tb + e;
+              bool alive = e < emine;
+#pragma unroll
+              for (int q = 1; q < kG; ++q)
+                if (q < g) alive &= dsub(tq[q * kTJ], bi[q]) < bq[q];
+              emit(e, alive);
             }
           }
         }
@@ -916,37 +938,60 @@ struct Engine {
 
   // -------------------------------------------------------- impact scores
   // impact_scores, operators.py:54-74: d_j = sum_k |s_k| exp((-a (t-|s_k|))/|a_kj|)
-  // summed over k in row order (numpy axis-0), / pairwise sum |s|.  Terms are
-  // computed by the whole CTA into an smem tile, then each column's owner
-  // adds its tile column sequentially.
+  // summed over k in row order (numpy axis-0), / pairwise sum |s|.  A tile of
+  // kTC columns x kTK rows: every thread first loads its kTK/...(independent)
+  // A entries, computes the terms branch-free into smem, then each column's
+  // owner thread adds its kTK terms in row order.  The exp argument uses a
+  // Newton-refined reciprocal (<= 2 ulp) and exp_nonpos (<= 0.51 ulp): the
+  // same tolerance class as numpy's own SIMD exp.
   __device__ void impact_scores(double alpha) {
     AMVM_LOCALS
+    static_assert(kTC == NT, "impact tile: one column per thread");
+    constexpr int kPer = kTC * kTK / NT;  // elements per thread per tile
     __syncthreads();
     const double t = cobj;
     const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
     const double na = -alpha;
-    double *tile = (double *)scr;
+    double *tile = (double *)scr;                      // kTC x (kTK+1)
+    double *rowv = tile + kTC * (kTK + 1);             // kTK x {|s_k|, (-alpha)(t - |s_k|)}
     for (int64_t cb = 0; cb < n; cb += kTC) {
       const int cols = (int)(n - cb < kTC ? n - cb : kTC);
       double acc = 0.0;
       for (int64_t kb = 0; kb < m; kb += kTK) {
         const int rws = (int)(m - kb < kTK ? m - kb : kTK);
-        for (int e = tid; e < kTC * kTK; e += NT) {
-          const int c = e / kTK, k = e - c * kTK;
-          if (c < cols && k < rws) {
-            const double a = fabs(__ldg(At + (cb + c) * m + kb + k));
-            const double s = fabs(cr[kb + k]);
-            double term = 0.0;
-            if (a > 0.0) term = dmul(s, exp(ddiv(dmul(na, dsub(t, s)), a)));
-            tile[c * (kTK + 1) + k] = term;
-          }
+        if (tid < kTK) {
+          const double sv = tid < rws ? fabs(cr[kb + tid]) : 0.0;
+          rowv[2 * tid] = sv;
+          rowv[2 * tid + 1] = dmul(na, dsub(t, sv));
+        }
+        double av[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int e = tid + q * NT, c = e / kTK, k = e - c * kTK;
+          av[q] = (c < cols && k < rws) ? fabs(__ldg(At + (cb + c) * m + kb + k)) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int e = tid + q * NT, c = e / kTK, k = e - c * kTK;
+          const double a = av[q];
+          const double as = a > 0.0 ? a : 1.0;
+          double y;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+          y = dfma(y, dfma(-as, y, 1.0), y);
+          y = dfma(y, dfma(-as, y, 1.0), y);
+          const double x = dmul(rowv[2 * k + 1], y);
+          const double term = dmul(rowv[2 * k], exp_nonpos(x));
+          tile[c * (kTK + 1) + k] = a > 0.0 ? term : 0.0;
         }
         __syncthreads();
         if (tid < cols)
-          for (int k = 0; k < rws; ++k) acc = dadd(acc, tile[tid * (kTK + 1) + k]);
-        __syncthreads();
+#pragma unroll
+          for (int k = 0; k < kTK; ++k)
+            if (k < rws) acc = dadd(acc, tile[tid * (kTK + 1) + k]);
       }
       if (tid < cols) dbuf[cb + tid] = ddiv(acc, tot);
+      __syncthreads();
     }
     __syncthreads();
   }
@@ -1056,24 +1101,52 @@ struct Engine {
       }
       for (int64_t k = tid; k < n; k += NT) pbuf[k] = ddiv(dbuf[k], total);
       __syncthreads();
-      if (tid == 0) {
+      if (warp == 0) {
         // Generator.choice(n, p): cdf = cumsum(p); cdf /= cdf[-1];
-        // searchsorted(cdf, random(), 'right')
+        // searchsorted(cdf, random(), 'right').  The cumsum is numpy's
+        // sequential chain; warp 0 runs it with coalesced loads and
+        // shuffle-broadcast adds (every lane holds the identical running
+        // sum), keeping the value before each 32-element chunk so the search
+        // rescans one chunk instead of storing the whole cdf.
+        const int64_t nch = (n + 31) / 32;
         double acc = 0.0;
-        for (int64_t k = 0; k < n; ++k) {
-          acc = dadd(acc, pbuf[k]);
-          pbuf[k] = acc;
+        for (int64_t c = 0; c < nch; ++c) {
+          const int64_t k = c * 32 + lane;
+          const double pv = k < n ? pbuf[k] : 0.0;
+          if (lane == 0) cbk[c] = acc;
+          const int cnt = (int)(n - c * 32 < 32 ? n - c * 32 : 32);
+          for (int l = 0; l < cnt; ++l) acc = dadd(acc, __shfl_sync(AMVM_FULL, pv, l));
         }
-        const double last = pbuf[n - 1];
-        const double u = pcg_random(sh->rng);
-        int64_t lo = 0, hi = n;
+        const double last = acc;  // cdf[n-1]
+        double u = 0.0;
+        if (lane == 0) u = pcg_random(sh->rng);
+        u = __shfl_sync(AMVM_FULL, u, 0);
+        __syncwarp();
+        // first chunk whose last cdf value normalizes above u (cdf is monotone)
+        int64_t lo = 0, hi = nch - 1;
         while (lo < hi) {
-          const int64_t mid = lo + ((hi - lo) >> 1);
-          if (u < ddiv(pbuf[mid], last)) hi = mid;
+          const int64_t mid = (lo + hi) >> 1;
+          const double end = mid + 1 < nch ? cbk[mid + 1] : last;
+          if (u < ddiv(end, last)) hi = mid;
           else lo = mid + 1;
         }
-        pick[q] = (int32_t)lo;
-        dbuf[lo] = 0.0;
+        const int64_t k0 = lo * 32;
+        const double pv = k0 + lane < n ? pbuf[k0 + lane] : 0.0;
+        double a2 = cbk[lo];
+        int64_t pickk = -1;
+        const int cnt = (int)(n - k0 < 32 ? n - k0 : 32);
+        for (int l = 0; l < cnt; ++l) {
+          a2 = dadd(a2, __shfl_sync(AMVM_FULL, pv, l));
+          if (u < ddiv(a2, last)) {
+            pickk = k0 + l;
+            break;
+          }
+        }
+        if (pickk < 0) pickk = n - 1;  // unreachable: cdf[n-1]/cdf[n-1] = 1 > u
+        if (lane == 0) {
+          pick[q] = (int32_t)pickk;
+          dbuf[pickk] = 0.0;
+        }
       }
       __syncthreads();
     }
@@ -1243,7 +1316,8 @@ struct Engine {
     tid = threadIdx.x;
     lane = tid & 31;
     warp = tid >> 5;
-    sh = (Shared<NT> *)smem;
+    sh = (Shared<NT> *)amvm_dyn_smem;
+    (void)smem;
     if (tid == 0) {
       Ctx &c = sh->c;
       c.m = a.m;
@@ -1264,6 +1338,7 @@ struct Engine {
       c.dpv = (double *)(base + L.dpv);
       c.dbuf = (double *)(base + L.dbuf);
       c.pbuf = (double *)(base + L.pbuf);
+      c.cbk = (double *)(base + L.cbk);
       c.lf_lo = (int64_t *)(base + L.lf_lo);
       c.lf_len = (int64_t *)(base + L.lf_len);
       c.lf_sum = (double *)(base + L.lf_sum);
@@ -1281,11 +1356,11 @@ struct Engine {
       c.srt = base + L.srt;
       // dynamic smem: Shared | lv | scratch | cr
       size_t o = sizeof(Shared<NT>);
-      c.lv = (double *)(smem + o);
+      c.off_lv = (uint32_t)o;
       o += 8 * ((a.nlev + 1) & ~1);
-      c.scr = smem + o;
+      c.off_scr = (uint32_t)o;
       o += scratch_bytes(a.nlev, a.tab);
-      c.cr = a.cr_smem ? (double *)(smem + o) : (double *)(base + L.crg);
+      c.cr = a.cr_smem ? (double *)(amvm_dyn_smem + o) : (double *)(base + L.crg);
       // leaf trees of numpy's pairwise sum for lengths m and n
       c.nleaf_m = pw_leaves(a.m, c.lf_lo, c.lf_len, (int)L.nleaf);
       c.nleaf_n = pw_leaves(a.n, c.lf_lo + c.nleaf_m, c.lf_len + c.nleaf_m, (int)(2 * L.nleaf - c.nleaf_m));
