@@ -24,7 +24,9 @@
 
 namespace amvm {
 
-constexpr int kWin = 8;        // one_opt speculative window (columns per barrier)
+constexpr int kWin = 8;        // (legacy) dense one_opt window
+constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
+constexpr int kWS = 32;        // one_opt screened window (columns per barrier)
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
@@ -83,7 +85,7 @@ struct WsHeader {
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
-  size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, cbk, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
+  size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, cbk, gsc, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
       hset, rem, sav, pick, coin, ibuf, srt, total;
   int64_t nleaf, kk, hsz;
 };
@@ -113,6 +115,7 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.dbuf = o; o = al256(o + 8 * n);
   L.pbuf = o; o = al256(o + 8 * n);
   L.cbk = o; o = al256(o + 8 * ((n + 31) / 32 + 2));
+  L.gsc = o; o = al256(o + 8 * kS * n);
   L.lf_lo = o; o = al256(o + 16 * L.nleaf);
   L.lf_len = o; o = al256(o + 16 * L.nleaf);
   L.lf_sum = o; o = al256(o + 8 * L.nleaf);
@@ -144,7 +147,7 @@ struct Ctx {
   const double *At, *b;
   double *cr, *ur;
   int32_t *cidx, *uidx;
-  double *dmv, *dpv, *dbuf, *pbuf, *cbk;
+  double *dmv, *dpv, *dbuf, *pbuf, *cbk, *gsc;
   int64_t *lf_lo, *lf_len;
   double *lf_sum;
   int nleaf_m, nleaf_n, tab;
@@ -179,6 +182,7 @@ struct Ctx {
   [[maybe_unused]] double *const dbuf = sh->c.dbuf;                                       \
   [[maybe_unused]] double *const pbuf = sh->c.pbuf;                                       \
   [[maybe_unused]] double *const cbk = sh->c.cbk;                                         \
+  [[maybe_unused]] double *const gsc = sh->c.gsc;                                         \
   [[maybe_unused]] int64_t *const lf_lo = sh->c.lf_lo;                                    \
   [[maybe_unused]] int64_t *const lf_len = sh->c.lf_len;                                  \
   [[maybe_unused]] double *const lf_sum = sh->c.lf_sum;                                   \
@@ -213,6 +217,11 @@ struct Shared {
   unsigned int hist[256];
   int counter;
   int qcount;
+  int srow[kS];
+  int wpre[kWS + 1];
+  unsigned sflag[NT / 32];
+  uint64_t skey[NT];
+  int sidx[NT];
   Pcg rng;
   Ctx c;
 };
@@ -354,85 +363,106 @@ struct Engine {
     __syncthreads();
   }
 
-  // one_opt, localsearch.py:59-88.  Speculative window of kWin columns scored
-  // against one residual.  The scan keeps only the high 32 bits of |y| (an
-  // integer max on the ALU pipe instead of an FP64 compare-select chain): a
-  // candidate whose high word exceeds that of the objective t cannot improve
-  // (|y| > t), so only columns with some candidate at or below it are
-  // re-scored exactly, in ascending order; the first that strictly improves
-  // is applied, exactly like the sequential first-improvement sweep.
+  // Screening rows for one_opt: each thread's largest |s|, then the kS largest
+  // of those (a block bitonic sort of NT keys).  ANY row subset gives an exact
+  // rejection test; large |s| rows reject almost every non-improving shift.
+  // Gathers gsc[j*kS + s] = A[srow[s], j].
+  __device__ void select_screen() {
+    AMVM_LOCALS
+    uint64_t best = 0;
+    int brow = 0;
+    for (int64_t i = tid; i < m; i += NT) {
+      const uint64_t key = abs_key(cr[i]);
+      if (key > best || i == tid) { best = key; brow = (int)i; }
+    }
+    sh->skey[tid] = tid < m ? best : 0;
+    sh->sidx[tid] = tid < m ? brow : 0;
+    __syncthreads();
+    for (int k = 2; k <= NT; k <<= 1) {
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        const int x = tid ^ jj;
+        if (x > tid) {
+          const uint64_t ka = sh->skey[tid], kb = sh->skey[x];
+          const bool desc = (tid & k) == 0;
+          if (desc ? ka < kb : ka > kb) {
+            sh->skey[tid] = kb; sh->skey[x] = ka;
+            const int t0 = sh->sidx[tid]; sh->sidx[tid] = sh->sidx[x]; sh->sidx[x] = t0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid < kS) sh->srow[tid] = sh->sidx[tid < m ? tid : 0];
+    __syncthreads();
+    for (int64_t e = tid; e < n * kS; e += NT) {
+      const int64_t j = e / kS, q = e - j * kS;
+      gsc[e] = __ldg(At + j * m + sh->srow[q]);
+    }
+    __syncthreads();
+  }
+
+  // one_opt, localsearch.py:59-88, exact and in the reference's order, with a
+  // row screen: a shift can only improve if EVERY row stays below t, so one
+  // screening row with |s_r + d*a_rj| >= t proves the candidate does not
+  // improve.  Per window of kWS columns each warp screens 4 columns (lane =
+  // screening row x candidate); columns with a surviving candidate are then
+  // scored over all m rows exactly, in ascending order, and the first that
+  // strictly improves is applied (first improvement), scanning resumes after it.
   __device__ void one_opt() {
     AMVM_LOCALS
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) set_deltas(j, cidx[j]);
     __syncthreads();
-    int par = 0;
+    select_screen();
+    const int srow_l = sh->srow[lane];
     for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
       bool changed = false;
       int64_t p = 0;
       while (p < n) {
-        const int wc = (int)(n - p < kWin ? n - p : kWin);
-        double dm[kWin], dp[kWin];
-        uint32_t h[2 * kWin];
+        const int wc = (int)(n - p < kWS ? n - p : kWS);
+        const double rs = cr[srow_l];  // current residual of this lane's screening row
+        const double t = cobj;
+        unsigned mine = 0u;  // bit c: column warp*4+c has a surviving candidate
 #pragma unroll
-        for (int w = 0; w < kWin; ++w) {
-          dm[w] = w < wc ? dmv[p + w] : 0.0;
-          dp[w] = w < wc ? dpv[p + w] : 0.0;
-          h[w] = 0u;
-          h[w + kWin] = 0u;
-        }
-        const int kdec = lane < wc ? cidx[p + lane] : 0;
-        const double *a0 = At + p * m;
-        if (wc == kWin) {
-          for (int64_t i = tid; i < m; i += NT) {
-            const double r = cr[i];
-#pragma unroll
-            for (int w = 0; w < kWin; ++w) {
-              const double av = __ldg(a0 + w * m + i);
-              h[w] = max(h[w], (uint32_t)__double2hiint(dadd(r, dmul(dm[w], av))) & 0x7fffffffu);
-              h[w + kWin] = max(h[w + kWin], (uint32_t)__double2hiint(dadd(r, dmul(dp[w], av))) & 0x7fffffffu);
-            }
-          }
-        } else {
-          for (int64_t i = tid; i < m; i += NT) {
-            const double r = cr[i];
-#pragma unroll
-            for (int w = 0; w < kWin; ++w) {
-              if (w < wc) {
-                const double av = __ldg(a0 + w * m + i);
-                h[w] = max(h[w], (uint32_t)__double2hiint(dadd(r, dmul(dm[w], av))) & 0x7fffffffu);
-                h[w + kWin] = max(h[w + kWin], (uint32_t)__double2hiint(dadd(r, dmul(dp[w], av))) & 0x7fffffffu);
-              }
-            }
+        for (int c = 0; c < kWS / NW; ++c) {
+          const int w = warp * (kWS / NW) + c;
+          if (w < wc) {
+            const int64_t j = p + w;
+            const int k = cidx[j];
+            const double a = gsc[j * kS + lane];
+            const bool rm = k <= 0 || fabs(dadd(rs, dmul(dmv[j], a))) >= t;
+            const bool rp = k + 1 >= nlev || fabs(dadd(rs, dmul(dpv[j], a))) >= t;
+            // a candidate survives only if no screening row rejects it
+            const bool surv = !__any_sync(AMVM_FULL, rm) || !__any_sync(AMVM_FULL, rp);
+            if (surv) mine |= 1u << c;
           }
         }
-        if (tid == 0) sh->c.pc[13] += 1;
-        uint32_t mine = 0u;
+        if (lane == 0) sh->sflag[warp] = mine;
+        if (warp == 0) {  // valid candidates per column before any apply (move count)
+          const int k = lane < wc ? cidx[p + lane] : 0;
+          int v = lane < wc ? (k > 0) + (k + 1 < nlev) : 0;
 #pragma unroll
-        for (int v = 0; v < 2 * kWin; ++v) {
-          const uint32_t rv = __reduce_max_sync(AMVM_FULL, h[v]);
-          if (lane == v) mine = rv;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(AMVM_FULL, v, o);
+            if (lane >= o) v += u;
+          }
+          sh->wpre[lane + 1] = v;
+          if (lane == 0) sh->wpre[0] = 0;
         }
-        sh->redu[par][warp][lane] = mine;
         __syncthreads();
-        uint32_t hv = 0u;
+        unsigned fl = 0u;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) hv = max(hv, sh->redu[par][k][lane]);
-        par ^= 1;
-        const uint32_t hp = __shfl_sync(AMVM_FULL, hv, (lane + kWin) & 31);
-        const uint32_t thi = (uint32_t)__double2hiint(cobj) & 0x7fffffffu;
-        const bool vm = lane < wc && kdec > 0;
-        const bool vp = lane < wc && kdec + 1 < nlev;
-        unsigned fl = __ballot_sync(AMVM_FULL, (vm && hv <= thi) || (vp && hp <= thi));
-        const unsigned vlo = __ballot_sync(AMVM_FULL, vm);
-        const unsigned vhi = __ballot_sync(AMVM_FULL, vp);
-        if (tid == 0) sh->c.mv_raw += __popc(vlo) + __popc(vhi);
+        for (int k = 0; k < NW; ++k) fl |= sh->sflag[k] << (k * (kWS / NW));
+        const int upto_cnt_all = sh->wpre[wc];
+        __syncthreads();
+        // reference-equivalent count: both neighbours of every column, as
+        // the sequential sweep evaluates them up to the applied column
         int applied = -1;
         while (fl) {
           const int w = __ffs(fl) - 1;
           fl &= fl - 1;
-          const int k = __shfl_sync(AMVM_FULL, kdec, w);
           const int64_t j = p + w;
+          const int k = cidx[j];
           double tm, tpv;
           if (tid == 0) sh->c.pc[11] += 1;
           exact_pair_max(At + j * m, dmv[j], dpv[j], tm, tpv);
@@ -446,21 +476,26 @@ struct Engine {
             const double d = dsub(lv[lvl], lv[k]);
             const double *col = At + j * m;
             for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
+            __syncthreads();  // all reads of cidx[j] / dmv done; residual published
             if (tid == 0) {
               cidx[j] = lvl;
               set_deltas(j, lvl);
             }
             bump_known(bt);
+            __syncthreads();
             break;
           }
         }
+        if (tid == 0) {
+          const int64_t cnt = applied >= 0 ? sh->wpre[applied + 1] : upto_cnt_all;
+          sh->c.mv_ref += cnt;
+          sh->c.mv_raw += cnt;
+          sh->c.pc[13] += 1;
+        }
         if (applied >= 0) {
-          const unsigned upto = applied == 31 ? AMVM_FULL : ((2u << applied) - 1u);
-          if (tid == 0) sh->c.mv_ref += __popc(vlo & upto) + __popc(vhi & upto);
           changed = true;
           p = p + applied + 1;
         } else {
-          if (tid == 0) sh->c.mv_ref += __popc(vlo) + __popc(vhi);
           p += wc;
         }
       }
@@ -1339,6 +1374,7 @@ struct Engine {
       c.dbuf = (double *)(base + L.dbuf);
       c.pbuf = (double *)(base + L.pbuf);
       c.cbk = (double *)(base + L.cbk);
+      c.gsc = (double *)(base + L.gsc);
       c.lf_lo = (int64_t *)(base + L.lf_lo);
       c.lf_len = (int64_t *)(base + L.lf_len);
       c.lf_sum = (double *)(base + L.lf_sum);
