@@ -1,0 +1,55 @@
+"""Wall time of the named BASELINE configs on the GPU vs the reference's CPU
+times, through the public API, with a parity check against the
+committed goldens (same trajectory => same final l_inf at the same iteration).
+
+  python tools/configs_walltime.py            (on the B200)
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2508_13437_b200 as P  # noqa: E402
+from paper_2508_13437_b200.controller import solve_from  # noqa: E402
+from tests.golden_io import cfg_kwargs, load, named_A  # noqa: E402
+
+# reference CPU seconds per iteration, 1 core, dev container
+REF_S_PER_IT = {"c1": 16.79 / 1000, "c1x": 18.14 / 1000, "c2": 0.110, "c4row": 0.1855, "c5row": 4.12}
+
+
+def main():
+    import torch
+    out = []
+    for name in ["c1", "c1x", "c2", "c4row", "c5row"]:
+        rec = load(f"solve_{name}")[0]
+        A = named_A(name, rec)
+        if A is None:
+            out.append({"config": name, "skipped": "matrix not reproducible on this host"})
+            continue
+        inst = P.Instance(A, rec["b"], P.ValueSet(rec["levels"]), continuous_init=rec.get("continuous_init"))
+        start = P.Solution(rec["idx0"], rec["r0"], rec["obj0"], 0)
+        cfg = P.SolverConfig(**cfg_kwargs(rec))
+        solve_from(inst, start, cfg)  # warm-up (upload + module load)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = solve_from(inst, start, cfg)
+        dt = time.perf_counter() - t0
+        same = (rep.iterations == int(rec["iterations"]) and np.array_equal(rep.best.idx, rec["best_idx"])
+                and rep.best.objective == rec["best_objective"])
+        it = rep.iterations
+        ref_s = REF_S_PER_IT[name] * it
+        out.append({"config": name, "m": int(A.shape[0]), "n": int(A.shape[1]), "levels": int(len(rec["levels"])),
+                    "iterations": it, "gpu_s": round(dt, 4), "ref_cpu_s_1core": round(ref_s, 3),
+                    "speedup_vs_ref": round(ref_s / dt, 1), "final_linf": rep.best.objective,
+                    "reference_final_linf": rec["best_objective"], "bitwise_same_trajectory": bool(same),
+                    "moves_scored_ref": rep.device.get("moves_scored_ref")})
+        print(json.dumps(out[-1]), flush=True)
+
+
+if __name__ == "__main__":
+    main()
