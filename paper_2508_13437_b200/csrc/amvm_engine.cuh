@@ -29,6 +29,7 @@ constexpr int kS = 32;         // one_opt screening rows (exact rejection test),
 constexpr int kWS = 32;        // one_opt screened window (columns per barrier)
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
+constexpr int kRowPasses = 8;  // queue rows drained from an smem-gathered row
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = 256;       // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
@@ -123,7 +124,7 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.reps = o; o = al256(o + 8 * L.kk);
   L.rsgn = o; o = al256(o + 4 * L.kk);
   L.ag = o; o = al256(o + 8 * kG * n);
-  L.cbuf = o; o = al256(o + sizeof(Cand) * cap + sizeof(int2) * cap);  // candidates + survivor queue
+  L.cbuf = o; o = al256(o + sizeof(Cand) * cap + 2 * sizeof(int2) * cap);  // candidates + survivor queue + scratch
   L.hset = o; o = al256(o + 8 * L.hsz);
   L.rem = o; o = al256(o + 4 * rr);
   L.sav = o; o = al256(o + 4 * rr);
@@ -217,6 +218,8 @@ struct Shared {
   unsigned int hist[256];
   int counter;
   int qcount;
+  int gnext;
+  int qnext;
   int srow[kS];
   int wpre[kWS + 1];
   unsigned sflag[NT / 32];
@@ -676,6 +679,7 @@ struct Engine {
     double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
     int32_t *perm = ibuf;                 // level-sorted position -> variable
     int2 *que = (int2 *)(cbuf + cap);     // staged-row survivors awaiting the rest
+    int2 *pr2 = que + cap;                // row-pass scratch
     const int qcap = (int)cap;
     // level buckets
     for (int64_t k = tid; k <= nlev; k += NT) lfl[k] = 0;
@@ -771,10 +775,15 @@ struct Engine {
         for (int q = 0; q < kG; ++q)
           if (q < g) tb[q * kTJ + e] = ag[(int64_t)q * n + p0 + e];
       }
+      if (tid == 0) sh->gnext = 0;
       __syncthreads();
       int ki = 0;
-      int64_t gbase = 0;  // first group id of bucket ki
-      for (int64_t grp = warp; grp < ngrp; grp += NW) {
+      int64_t gbase = 0;  // first group id of bucket ki (groups are claimed in increasing order)
+      for (;;) {
+        int64_t grp = 0;
+        if (lane == 0) grp = atomicAdd(&sh->gnext, 1);
+        grp = __shfl_sync(AMVM_FULL, grp, 0);
+        if (grp >= ngrp) break;
         while (ki < nlev && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
           gbase += (lst[ki + 1] - lst[ki] + 31) >> 5;
           ++ki;
@@ -862,11 +871,41 @@ struct Engine {
       }
       __syncthreads();
       if (nr > g) {
-        const int qn = sh->qcount < qcap ? sh->qcount : qcap;
+        // drain the queue row by row: gather row q of A for every variable
+        // into the (now free) tile smem, test all queued pairs against it
+        // (independent loads, full memory parallelism), compact the
+        // survivors, next row; the rare long survivors finish on A directly
+        int qn = sh->qcount < qcap ? sh->qcount : qcap;
+        double *rowbuf = pbuf;  // n doubles (pbuf is idle during find_candidates)
+        const bool fits = true;
+        int q = g;
+        for (; fits && q < nr && q < g + kRowPasses && qn > 0; ++q) {
+          const int64_t rq = rows[q];
+          for (int64_t j = tid; j < n; j += NT) rowbuf[j] = __ldg(At + j * m + rq);
+          if (tid == 0) sh->qnext = 0;
+          __syncthreads();
+          const double eq = reps[q];
+          const bool pos = rsgn[q] != 0;
+          for (int e = tid; e < qn; e += NT) {
+            const int2 pr = que[e];
+            const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
+            const double da = dsub(rowbuf[pr.y], rowbuf[pr.x]);
+            const double bq = ddiv(eq, delta);
+            pr2[e] = (pos ? (da < bq) : (da > -bq)) ? pr : make_int2(-1, -1);
+          }
+          __syncthreads();
+          for (int e = tid; e < qn; e += NT) {
+            const int2 pr = pr2[e];
+            if (pr.x >= 0) que[atomicAdd(&sh->qnext, 1)] = pr;
+          }
+          __syncthreads();
+          qn = sh->qnext;
+          __syncthreads();
+        }
         for (int e = tid; e < qn; e += NT) {
           const int2 pr = que[e];
           const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
-          if (fc_rest(pr.x, pr.y, delta, nr, g)) fc_append(pr.x, pr.y, delta);
+          if (fc_rest(pr.x, pr.y, delta, nr, q)) fc_append(pr.x, pr.y, delta);
         }
         __syncthreads();
         if (tid == 0) sh->qcount = 0;
