@@ -466,6 +466,20 @@ struct Engine {
           fl &= fl - 1;
           const int64_t j = p + w;
           const int k = cidx[j];
+          {
+            // second screen: every thread tests one of the CTA's per-thread
+            // maximum rows (sorted by select_screen); one load each, one
+            // barrier per candidate, before any full-column pass
+            const int rA = sh->sidx[tid];
+            const double aA = __ldg(At + j * m + rA);
+            const double rr = cr[rA];
+            const double t2 = cobj;
+            const bool em = k <= 0 || fabs(dadd(rr, dmul(dmv[j], aA))) >= t2;
+            const bool ep = k + 1 >= nlev || fabs(dadd(rr, dmul(dpv[j], aA))) >= t2;
+            const bool rej_m = __syncthreads_or(em);
+            const bool rej_p = __syncthreads_or(ep);
+            if (rej_m && rej_p) continue;
+          }
           double tm, tpv;
           if (tid == 0) sh->c.pc[11] += 1;
           exact_pair_max(At + j * m, dmv[j], dpv[j], tm, tpv);
@@ -773,7 +787,7 @@ struct Engine {
         tl[e] = cidx[j];
 #pragma unroll
         for (int q = 0; q < kG; ++q)
-          if (q < g) tb[q * kTJ + e] = ag[(int64_t)q * n + p0 + e];
+          if (q < g) tb[e * kG + q] = ag[(int64_t)q * n + p0 + e];
       }
       if (tid == 0) sh->gnext = 0;
       __syncthreads();
@@ -812,7 +826,7 @@ struct Engine {
           if (have) {
             while (lo < hi) {
               const int64_t mid = (lo + hi) >> 1;
-              if (dsub(tb[mid - p0], bi[0]) < bq[0]) lo = mid + 1;
+              if (dsub(tb[(mid - p0) * kG], bi[0]) < bq[0]) lo = mid + 1;
               else hi = mid;
             }
           } else {
@@ -849,21 +863,44 @@ struct Engine {
               }
             }
           };
-          if (g == kG) {  // common case: every staged row present, no per-row predicates
-            for (int e = e0; e < e1; ++e) {
-              const double *tq = tb + e;
+          if (g == kG) {
+            // common case: every staged row present; the tile is row-
+            // interleaved per position (one 64-byte broadcast record), two
+            // positions per iteration for independent dependency chains
+            int e = e0;
+            for (; e + 1 < e1; e += 2) {
+              const double2 *ta = reinterpret_cast<const double2 *>(tb + e * kG);
+              const double2 *tc = reinterpret_cast<const double2 *>(tb + (e + 1) * kG);
+              double va[kG], vc[kG];
+#pragma unroll
+              for (int h = 0; h < kG / 2; ++h) {
+                const double2 x = ta[h], y = tc[h];
+                va[2 * h] = x.x; va[2 * h + 1] = x.y;
+                vc[2 * h] = y.x; vc[2 * h + 1] = y.y;
+              }
+              bool aa = e < emine, ac = e + 1 < emine;
+#pragma unroll
+              for (int q = 1; q < kG; ++q) {
+                aa &= dsub(va[q], bi[q]) < bq[q];
+                ac &= dsub(vc[q], bi[q]) < bq[q];
+              }
+              emit(e, aa);
+              emit(e + 1, ac);
+            }
+            if (e < e1) {
+              const double *tq = tb + e * kG;
               bool alive = e < emine;
 #pragma unroll
-              for (int q = 1; q < kG; ++q) alive &= dsub(tq[q * kTJ], bi[q]) < bq[q];
+              for (int q = 1; q < kG; ++q) alive &= dsub(tq[q], bi[q]) < bq[q];
               emit(e, alive);
             }
           } else {
             for (int e = e0; e < e1; ++e) {
-              const double *tq = tb + e;
+              const double *tq = tb + e * kG;
               bool alive = e < emine;
 #pragma unroll
               for (int q = 1; q < kG; ++q)
-                if (q < g) alive &= dsub(tq[q * kTJ], bi[q]) < bq[q];
+                if (q < g) alive &= dsub(tq[q], bi[q]) < bq[q];
               emit(e, alive);
             }
           }
