@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libamvm.so")
+LIB_PATH = os.environ.get("AMVM_LIBRARY") or os.path.join(HERE, "libamvm.so")  # override for A/B builds
 
 AMVM_OK = 0
 AMVM_ERR_INVALID = -1

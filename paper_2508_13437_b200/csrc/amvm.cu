@@ -17,7 +17,7 @@ using namespace amvm;
 // Persistent solve: one CTA per resident slot, instances pulled from a
 // counter so uneven iteration counts balance across SMs.
 template <int NT>
-__global__ void __launch_bounds__(NT, 2) k_solve(KArgs a) {
+__global__ void __launch_bounds__(NT, AMVM_MIN_BLOCKS) k_solve(KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   Engine<NT> E;
   E.bind(a, smem, blockIdx.x);
@@ -339,8 +339,13 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   P->cr_smem = p->m * 8 <= 96 * 1024;
   const int64_t n = p->n;
   const int64_t maxc = prm->max_candidates;
-  int64_t cap = maxc > 0 ? std::max<int64_t>(std::max<int64_t>(2 * maxc, maxc + n), 1024)
-                         : std::max<int64_t>(n * (n - 1) / 2, 1024);
+  // swap-candidate survivor buffer: batches get room for 2x max_candidates
+  // (C4/C5 keep < 100 per call); small batches (single instances) get room for
+  // every pair up to 4M, which covers the filter's worst cases on tomography
+  // (SURVEY.md §8a row 17); beyond it the call reports AMVM_ERR_UNSUPPORTED.
+  const int64_t all_pairs = n * (n - 1) / 2;
+  int64_t cap = maxc > 0 ? std::max<int64_t>(std::max<int64_t>(2 * maxc, maxc + n), 1024) : std::max<int64_t>(all_pairs, 1024);
+  if (p->count <= 16) cap = std::max<int64_t>(cap, std::min<int64_t>(all_pairs, (int64_t)1 << 22));
   cap = pow2ceil(cap);
   if (cap > ((int64_t)1 << 30)) return AMVM_ERR_UNSUPPORTED;
   P->cap = (int)cap;

@@ -24,6 +24,12 @@
 
 namespace amvm {
 
+#ifndef AMVM_FC_UNROLL2
+#define AMVM_FC_UNROLL2 1
+#endif
+#ifndef AMVM_MIN_BLOCKS
+#define AMVM_MIN_BLOCKS 2
+#endif
 constexpr int kWin = 8;        // (legacy) dense one_opt window
 constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
 constexpr int kWS = 32;        // one_opt screened window (columns per barrier)
@@ -863,7 +869,7 @@ struct Engine {
               }
             }
           };
-          if (g == kG) {
+          if (g == kG && AMVM_FC_UNROLL2) {
             // common case: every staged row present; the tile is row-
             // interleaved per position (one 64-byte broadcast record), two
             // positions per iteration for independent dependency chains

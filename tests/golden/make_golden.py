@@ -144,13 +144,36 @@ def component_cases() -> list[dict]:
     return out
 
 
+def c3_scaled() -> None:
+    """Tomography (C3 family) at 64^2 x 45 angles, 3 grey levels: A stored as
+    CSR in the fixture (the GPU box has no reference builder)."""
+    angles = np.arange(45) * np.pi / 45
+    A = dmmv.parallel_beam_matrix(64, angles)
+    eta = 0.05 * float(A.sum(axis=1).max())
+    spec = dmmv.TomoSpec(side=64, gray_levels=(0.0, 1.0, 2.0), n_angles=45, noise=eta, phantom="squares",
+                         sirt_iters=100, seed=0)
+    inst, _ = dmmv.build_tomo(spec)
+    rec = solve_record(inst, dmmv.SolverConfig(max_iters=4, seed=0), store_A=False)
+    Ac = inst.A
+    nz = np.nonzero(Ac)
+    rec["A_shape"] = np.array(Ac.shape)
+    rec["A_rows"] = nz[0].astype(np.int32)
+    rec["A_cols"] = nz[1].astype(np.int32)
+    rec["A_vals"] = Ac[nz]
+    save("solve_c3s", [rec])
+
+
 def main() -> None:
     assert os.environ.get("OPENBLAS_NUM_THREADS") == "1"
+    if "--c3s" in sys.argv:
+        c3_scaled()
+        return
     save("components", component_cases())
     save("small_solves", small_solves())
     save("refresh_solves", refresh_solves())
     for name, recs in named_solves().items():
         save(f"solve_{name}", recs)
+    c3_scaled()
 
 
 if __name__ == "__main__":

@@ -44,3 +44,10 @@ def named_A(name: str, rec: dict):
     if sha(data["A"]) != rec["A_sha"]:
         return None
     return data["A"]
+
+
+def stored_A(rec: dict) -> np.ndarray:
+    """Dense A of a fixture that stores it sparsely (A_shape/A_rows/A_cols/A_vals)."""
+    A = np.zeros(tuple(int(x) for x in rec["A_shape"]))
+    A[rec["A_rows"], rec["A_cols"]] = rec["A_vals"]
+    return A

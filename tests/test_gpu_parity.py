@@ -6,7 +6,7 @@ tolerance below).  Run on a B200: ``pytest -m gpu``.
 import numpy as np
 import pytest
 
-from tests.golden_io import cfg_kwargs, load, named_A
+from tests.golden_io import cfg_kwargs, load, named_A, stored_A
 
 pytestmark = pytest.mark.gpu
 
@@ -74,6 +74,12 @@ def test_named_solves_match_reference(amvm, name):
     if A is None:
         pytest.skip("host numpy does not regenerate the reference matrix bit-exactly")
     _check_report(_solve_from_golden(amvm, A, rec), rec)
+
+
+def test_tomography_scaled_matches_reference(amvm):
+    """C3 family at 64^2 x 45 angles: many filter survivors (adaptive buffer)."""
+    rec = load("solve_c3s")[0]
+    _check_report(_solve_from_golden(amvm, stored_A(rec), rec), rec)
 
 
 def test_public_solve_matches_oracle(amvm, oracle):

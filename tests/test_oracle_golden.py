@@ -9,7 +9,7 @@ may differ by an ulp from numpy's SIMD exp (tolerance stated below).
 import numpy as np
 import pytest
 
-from tests.golden_io import cfg_kwargs, load, named_A
+from tests.golden_io import cfg_kwargs, load, named_A, stored_A
 
 IMPACT_RTOL = 1e-13  # libm exp vs numpy SIMD exp (<= 1 ulp per term)
 
@@ -59,6 +59,13 @@ def test_named_solves_bitwise(oracle, name):
     if A is None:
         pytest.skip("host numpy does not regenerate the reference matrix bit-exactly")
     _check_solve(oracle, A, rec)
+
+
+def test_tomography_scaled_bitwise(oracle):
+    """C3 family (64^2 phantom, 45 angles, 3 grey levels; A built by the
+    reference's own projector): 152K swap-filter survivors at the start."""
+    rec = load("solve_c3s")[0]
+    _check_solve(oracle, stored_A(rec), rec)
 
 
 def _sol(rec, prefix):
