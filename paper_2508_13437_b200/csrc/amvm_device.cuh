@@ -112,29 +112,6 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-__device__ __forceinline__ int warp_sum_i(int v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(AMVM_FULL, v, o);
-  return v;
-}
-
-// Transpose-reduce: on entry each lane holds v[0..31]; on exit v[0] of lane
-// l is the max over the warp of everybody's v[l] (31 shuffles, not 160).
-__device__ __forceinline__ double warp_transpose_max32(double (&v)[32], int lane) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int k = 0; k < s; ++k) {
-      double send = up ? v[k] : v[k + s];
-      double keep = up ? v[k + s] : v[k];
-      double recv = __shfl_xor_sync(AMVM_FULL, send, s);
-      v[k] = fmax(keep, recv);
-    }
-  }
-  return v[0];
-}
-
 // -------------------------------------------------- numpy pairwise summation
 // numpy/_core/src/umath/loops_utils.h pairwise_sum: n < 8 sequential from 0;
 // n <= 128 eight accumulators + ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) + tail;

@@ -30,12 +30,12 @@ namespace amvm {
 #ifndef AMVM_MIN_BLOCKS
 #define AMVM_MIN_BLOCKS 2
 #endif
-constexpr int kWin = 8;        // (legacy) dense one_opt window
 constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
 constexpr int kWS = 32;        // one_opt screened window (columns per barrier)
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
 constexpr int kRowPasses = 8;  // queue rows drained from an smem-gathered row
+constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = 256;       // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
@@ -214,8 +214,7 @@ struct Ctx {
 template <int NT>
 struct Shared {
   static constexpr int NW = NT / 32;
-  double red[2][NW][32];
-  uint32_t redu[2][NW][32];
+  double red[NW][4];  // best_swap per-warp winners
   double red2[2][NW];
   double redS[NW];
   double bc_d[8];
@@ -670,10 +669,10 @@ struct Engine {
   //     CTA drains against the remaining rows, read from A directly.
   // Returns the count kept (truncated to max_candidates in (-delta, i, j)
   // order); with `always_sort` the kept list is in that order regardless.
-  __device__ void fc_append(int32_t i, int32_t j, double delta) {
+  __device__ void fc_append(int32_t i, int32_t j, double delta, bool counting = false) {
     AMVM_LOCALS
     const int pos = atomicAdd(&sh->counter, 1);
-    if (pos < cap) cbuf[pos] = Cand{i, j, delta};
+    if (!counting && pos < cap) cbuf[pos] = Cand{i, j, delta};
   }
 
   __device__ bool fc_rest(int64_t i, int32_t j, double delta, int nr, int g) {
@@ -685,6 +684,206 @@ struct Engine {
       if (!(rsgn[q] ? (da < bq) : (da > -bq))) return false;
     }
     return true;
+  }
+
+  // One enumeration pass over the staged tiles.  mode FC_ALL collects every
+  // survivor; FC_COUNT only counts, FC_CUT collects, the survivors whose key
+  // precedes or equals (fD, fI) in the reference order (-delta, i): delta > fD,
+  // or delta == fD and i <= fI (the exact overflow path, find_candidates).
+  enum { FC_ALL = 0, FC_COUNT = 1, FC_CUT = 2 };
+  template <int MODE>
+  __device__ void fc_pass(int nr, int g, double fD, int64_t fI) {
+    AMVM_LOCALS
+    double *tb = (double *)scr;
+    int32_t *tl = (int32_t *)(tb + kG * kTJ);
+    int32_t *tj = tl + kTJ;
+    int32_t *lst = tj + kTJ;
+    double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
+    int32_t *perm = ibuf;
+    int2 *que = (int2 *)(cbuf + cap);
+    int2 *pr2 = que + cap;
+    const int qcap = (int)cap;
+    const int ll = (int)(nlev * nlev);
+    constexpr bool filt = MODE != FC_ALL;
+    constexpr bool counting = MODE == FC_COUNT;
+    // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
+    // with it every staged row's bound for a given j-bucket) is warp-uniform;
+    // within a bucket the lanes' b0 ascend, so their prefixes nest
+    const int64_t ngrp = (n + 31) / 32 + nlev;
+    for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
+      const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
+      for (int64_t e = tid; e < p1 - p0; e += NT) {
+        const int32_t j = perm[p0 + e];
+        tj[e] = j;
+        tl[e] = cidx[j];
+#pragma unroll
+        for (int q = 0; q < kG; ++q)
+          if (q < g) tb[e * kG + q] = ag[(int64_t)q * n + p0 + e];
+      }
+      if (tid == 0) sh->gnext = 0;
+      __syncthreads();
+      int ki = 0;
+      int64_t gbase = 0;  // first group id of bucket ki (groups are claimed in increasing order)
+      for (;;) {
+        int64_t grp = 0;
+        if (lane == 0) grp = atomicAdd(&sh->gnext, 1);
+        grp = __shfl_sync(AMVM_FULL, grp, 0);
+        if (grp >= ngrp) break;
+        while (ki < nlev && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
+          gbase += (lst[ki + 1] - lst[ki] + 31) >> 5;
+          ++ki;
+        }
+        if (ki >= nlev) break;
+        if (ki == 0) continue;  // no level below the lowest
+        if ((int64_t)lst[ki] <= p0) continue;  // no lower-level position in this tile
+        const int64_t ip = lst[ki] + (grp - gbase) * 32 + lane;
+        const bool have = ip < lst[ki + 1];
+        const int32_t i = have ? perm[ip] : 0;
+        double bi[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) bi[q] = (have && q < g) ? ag[(int64_t)q * n + ip] : 0.0;
+        const double xi = lv[ki];
+        for (int kj = 0; kj < ki; ++kj) {
+          const int64_t s0 = (int64_t)lst[kj] > p0 ? (int64_t)lst[kj] : p0;
+          const int64_t s1 = (int64_t)lst[kj + 1] < p1 ? (int64_t)lst[kj + 1] : p1;
+          if (s0 >= s1) continue;
+          const double delta = dsub(xi, lv[kj]);
+          if (filt && delta < fD) continue;  // whole segment after the cut (uniform)
+          double bq[kG];
+#pragma unroll
+          for (int q = 0; q < kG; ++q)
+            bq[q] = q < g ? (tab ? bt[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta)) : 0.0;
+          // row 0 as a prefix: first position where dsub(b0_j, b0_i) < bq0 fails
+          int64_t lo = s0, hi = s1;
+          if (have) {
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              if (dsub(tb[(mid - p0) * kG], bi[0]) < bq[0]) lo = mid + 1;
+              else hi = mid;
+            }
+          } else {
+            lo = s0;
+          }
+          const int64_t mine = lo;
+          int64_t wend = mine;
+          for (int o = 16; o; o >>= 1) {
+            const int64_t v = __shfl_xor_sync(AMVM_FULL, wend, o);
+            wend = v > wend ? v : wend;
+          }
+          const int e0 = (int)(s0 - p0), e1 = (int)(wend - p0), emine = (int)(mine - p0);
+          // survivors of the staged rows: straight into the candidate list when
+          // they are all the rows, else into the queue for the remaining rows
+          auto emit = [&](int e, bool alive) {
+            if (filt) alive = alive && (delta > fD || (int64_t)i <= fI);
+            const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+            if (!bal) return;
+            if (nr <= g && counting) {
+              if (lane == 0) atomicAdd(&sh->counter, __popc(bal));
+            } else if (nr <= g) {
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
+              bse = __shfl_sync(AMVM_FULL, bse, 0);
+              if (alive) {
+                const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
+                if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
+              }
+            } else {
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
+              bse = __shfl_sync(AMVM_FULL, bse, 0);
+              if (alive) {
+                const int qp = bse + __popc(bal & ((1u << lane) - 1u));
+                if (qp < qcap) que[qp] = make_int2(i, tj[e]);
+                else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta, counting);
+              }
+            }
+          };
+          if (g == kG && AMVM_FC_UNROLL2) {
+            // common case: every staged row present; the tile is row-
+            // interleaved per position (one 64-byte broadcast record), two
+            // positions per iteration for independent dependency chains
+            int e = e0;
+            for (; e + 1 < e1; e += 2) {
+              const double2 *ta = reinterpret_cast<const double2 *>(tb + e * kG);
+              const double2 *tc = reinterpret_cast<const double2 *>(tb + (e + 1) * kG);
+              double va[kG], vc[kG];
+#pragma unroll
+              for (int h = 0; h < kG / 2; ++h) {
+                const double2 x = ta[h], y = tc[h];
+                va[2 * h] = x.x; va[2 * h + 1] = x.y;
+                vc[2 * h] = y.x; vc[2 * h + 1] = y.y;
+              }
+              bool aa = e < emine, ac = e + 1 < emine;
+#pragma unroll
+              for (int q = 1; q < kG; ++q) {
+                aa &= dsub(va[q], bi[q]) < bq[q];
+                ac &= dsub(vc[q], bi[q]) < bq[q];
+              }
+              emit(e, aa);
+              emit(e + 1, ac);
+            }
+            if (e < e1) {
+              const double *tq = tb + e * kG;
+              bool alive = e < emine;
+#pragma unroll
+              for (int q = 1; q < kG; ++q) alive &= dsub(tq[q], bi[q]) < bq[q];
+              emit(e, alive);
+            }
+          } else {
+            for (int e = e0; e < e1; ++e) {
+              const double *tq = tb + e * kG;
+              bool alive = e < emine;
+#pragma unroll
+              for (int q = 1; q < kG; ++q)
+                if (q < g) alive &= dsub(tq[q], bi[q]) < bq[q];
+              emit(e, alive);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (nr > g) {
+        // drain the queue row by row: gather row q of A for every variable
+        // into the (now free) tile smem, test all queued pairs against it
+        // (independent loads, full memory parallelism), compact the
+        // survivors, next row; the rare long survivors finish on A directly
+        int qn = sh->qcount < qcap ? sh->qcount : qcap;
+        double *rowbuf = pbuf;  // n doubles (pbuf is idle during find_candidates)
+        const bool fits = true;
+        int q = g;
+        for (; fits && q < nr && q < g + kRowPasses && qn > 0; ++q) {
+          const int64_t rq = rows[q];
+          for (int64_t j = tid; j < n; j += NT) rowbuf[j] = __ldg(At + j * m + rq);
+          if (tid == 0) sh->qnext = 0;
+          __syncthreads();
+          const double eq = reps[q];
+          const bool pos = rsgn[q] != 0;
+          for (int e = tid; e < qn; e += NT) {
+            const int2 pr = que[e];
+            const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
+            const double da = dsub(rowbuf[pr.y], rowbuf[pr.x]);
+            const double bq = ddiv(eq, delta);
+            pr2[e] = (pos ? (da < bq) : (da > -bq)) ? pr : make_int2(-1, -1);
+          }
+          __syncthreads();
+          for (int e = tid; e < qn; e += NT) {
+            const int2 pr = pr2[e];
+            if (pr.x >= 0) que[atomicAdd(&sh->qnext, 1)] = pr;
+          }
+          __syncthreads();
+          qn = sh->qnext;
+          __syncthreads();
+        }
+        for (int e = tid; e < qn; e += NT) {
+          const int2 pr = que[e];
+          const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
+          if (fc_rest(pr.x, pr.y, delta, nr, q)) fc_append(pr.x, pr.y, delta, counting);
+        }
+        __syncthreads();
+        if (tid == 0) sh->qcount = 0;
+      }
+    }
+    __syncthreads();
   }
 
   __device__ int find_candidates(bool always_sort) {
@@ -781,190 +980,88 @@ struct Engine {
       sh->qcount = 0;
     }
     __syncthreads();
-    // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
-    // with it every staged row's bound for a given j-bucket) is warp-uniform;
-    // within a bucket the lanes' b0 ascend, so their prefixes nest
-    const int64_t ngrp = (n + 31) / 32 + nlev;
-    for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
-      const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
-      for (int64_t e = tid; e < p1 - p0; e += NT) {
-        const int32_t j = perm[p0 + e];
-        tj[e] = j;
-        tl[e] = cidx[j];
-#pragma unroll
-        for (int q = 0; q < kG; ++q)
-          if (q < g) tb[e * kG + q] = ag[(int64_t)q * n + p0 + e];
-      }
-      if (tid == 0) sh->gnext = 0;
-      __syncthreads();
-      int ki = 0;
-      int64_t gbase = 0;  // first group id of bucket ki (groups are claimed in increasing order)
-      for (;;) {
-        int64_t grp = 0;
-        if (lane == 0) grp = atomicAdd(&sh->gnext, 1);
-        grp = __shfl_sync(AMVM_FULL, grp, 0);
-        if (grp >= ngrp) break;
-        while (ki < nlev && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
-          gbase += (lst[ki + 1] - lst[ki] + 31) >> 5;
-          ++ki;
-        }
-        if (ki >= nlev) break;
-        if (ki == 0) continue;  // no level below the lowest
-        if ((int64_t)lst[ki] <= p0) continue;  // no lower-level position in this tile
-        const int64_t ip = lst[ki] + (grp - gbase) * 32 + lane;
-        const bool have = ip < lst[ki + 1];
-        const int32_t i = have ? perm[ip] : 0;
-        double bi[kG];
-#pragma unroll
-        for (int q = 0; q < kG; ++q) bi[q] = (have && q < g) ? ag[(int64_t)q * n + ip] : 0.0;
-        const double xi = lv[ki];
-        for (int kj = 0; kj < ki; ++kj) {
-          const int64_t s0 = (int64_t)lst[kj] > p0 ? (int64_t)lst[kj] : p0;
-          const int64_t s1 = (int64_t)lst[kj + 1] < p1 ? (int64_t)lst[kj + 1] : p1;
-          if (s0 >= s1) continue;
-          const double delta = dsub(xi, lv[kj]);
-          double bq[kG];
-#pragma unroll
-          for (int q = 0; q < kG; ++q)
-            bq[q] = q < g ? (tab ? bt[(q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta)) : 0.0;
-          // row 0 as a prefix: first position where dsub(b0_j, b0_i) < bq0 fails
-          int64_t lo = s0, hi = s1;
-          if (have) {
-            while (lo < hi) {
-              const int64_t mid = (lo + hi) >> 1;
-              if (dsub(tb[(mid - p0) * kG], bi[0]) < bq[0]) lo = mid + 1;
-              else hi = mid;
-            }
-          } else {
-            lo = s0;
-          }
-          const int64_t mine = lo;
-          int64_t wend = mine;
-          for (int o = 16; o; o >>= 1) {
-            const int64_t v = __shfl_xor_sync(AMVM_FULL, wend, o);
-            wend = v > wend ? v : wend;
-          }
-          const int e0 = (int)(s0 - p0), e1 = (int)(wend - p0), emine = (int)(mine - p0);
-          // survivors of the staged rows: straight into the candidate list when
-          // they are all the rows, else into the queue for the remaining rows
-          auto emit = [&](int e, bool alive) {
-            const unsigned bal = __ballot_sync(AMVM_FULL, alive);
-            if (!bal) return;
-            if (nr <= g) {
-              int bse = 0;
-              if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
-              bse = __shfl_sync(AMVM_FULL, bse, 0);
-              if (alive) {
-                const int pos2 = bse + __popc(bal & ((1u << lane) - 1u));
-                if (pos2 < cap) cbuf[pos2] = Cand{i, tj[e], delta};
-              }
-            } else {
-              int bse = 0;
-              if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
-              bse = __shfl_sync(AMVM_FULL, bse, 0);
-              if (alive) {
-                const int qp = bse + __popc(bal & ((1u << lane) - 1u));
-                if (qp < qcap) que[qp] = make_int2(i, tj[e]);
-                else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta);
-              }
-            }
-          };
-          if (g == kG && AMVM_FC_UNROLL2) {
-            // common case: every staged row present; the tile is row-
-            // interleaved per position (one 64-byte broadcast record), two
-            // positions per iteration for independent dependency chains
-            int e = e0;
-            for (; e + 1 < e1; e += 2) {
-              const double2 *ta = reinterpret_cast<const double2 *>(tb + e * kG);
-              const double2 *tc = reinterpret_cast<const double2 *>(tb + (e + 1) * kG);
-              double va[kG], vc[kG];
-#pragma unroll
-              for (int h = 0; h < kG / 2; ++h) {
-                const double2 x = ta[h], y = tc[h];
-                va[2 * h] = x.x; va[2 * h + 1] = x.y;
-                vc[2 * h] = y.x; vc[2 * h + 1] = y.y;
-              }
-              bool aa = e < emine, ac = e + 1 < emine;
-#pragma unroll
-              for (int q = 1; q < kG; ++q) {
-                aa &= dsub(va[q], bi[q]) < bq[q];
-                ac &= dsub(vc[q], bi[q]) < bq[q];
-              }
-              emit(e, aa);
-              emit(e + 1, ac);
-            }
-            if (e < e1) {
-              const double *tq = tb + e * kG;
-              bool alive = e < emine;
-#pragma unroll
-              for (int q = 1; q < kG; ++q) alive &= dsub(tq[q], bi[q]) < bq[q];
-              emit(e, alive);
-            }
-          } else {
-            for (int e = e0; e < e1; ++e) {
-              const double *tq = tb + e * kG;
-              bool alive = e < emine;
-#pragma unroll
-              for (int q = 1; q < kG; ++q)
-                if (q < g) alive &= dsub(tq[q], bi[q]) < bq[q];
-              emit(e, alive);
-            }
-          }
-        }
-      }
-      __syncthreads();
-      if (nr > g) {
-        // drain the queue row by row: gather row q of A for every variable
-        // into the (now free) tile smem, test all queued pairs against it
-        // (independent loads, full memory parallelism), compact the
-        // survivors, next row; the rare long survivors finish on A directly
-        int qn = sh->qcount < qcap ? sh->qcount : qcap;
-        double *rowbuf = pbuf;  // n doubles (pbuf is idle during find_candidates)
-        const bool fits = true;
-        int q = g;
-        for (; fits && q < nr && q < g + kRowPasses && qn > 0; ++q) {
-          const int64_t rq = rows[q];
-          for (int64_t j = tid; j < n; j += NT) rowbuf[j] = __ldg(At + j * m + rq);
-          if (tid == 0) sh->qnext = 0;
-          __syncthreads();
-          const double eq = reps[q];
-          const bool pos = rsgn[q] != 0;
-          for (int e = tid; e < qn; e += NT) {
-            const int2 pr = que[e];
-            const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
-            const double da = dsub(rowbuf[pr.y], rowbuf[pr.x]);
-            const double bq = ddiv(eq, delta);
-            pr2[e] = (pos ? (da < bq) : (da > -bq)) ? pr : make_int2(-1, -1);
-          }
-          __syncthreads();
-          for (int e = tid; e < qn; e += NT) {
-            const int2 pr = pr2[e];
-            if (pr.x >= 0) que[atomicAdd(&sh->qnext, 1)] = pr;
-          }
-          __syncthreads();
-          qn = sh->qnext;
-          __syncthreads();
-        }
-        for (int e = tid; e < qn; e += NT) {
-          const int2 pr = que[e];
-          const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
-          if (fc_rest(pr.x, pr.y, delta, nr, q)) fc_append(pr.x, pr.y, delta);
-        }
-        __syncthreads();
-        if (tid == 0) sh->qcount = 0;
-      }
-    }
-    __syncthreads();
+    fc_pass<FC_ALL>(nr, g, 0.0, 0);
     int cnt = sh->counter;
     __syncthreads();
-    if (cnt > cap) {
-      fail(AMVM_ERR_UNSUPPORTED);  // survivor buffer too small
-      cnt = (int)cap;
-    }
     const int maxc = prm->max_candidates;
+    if (cnt > cap) {
+      if (maxc > 0) cnt = fc_overflow(nr, g, maxc);
+      else {
+        fail(AMVM_ERR_UNSUPPORTED);  // no cap requested and more survivors than the buffer
+        cnt = (int)cap;
+      }
+    }
     if ((maxc > 0 && cnt > maxc) || (always_sort && cnt > 1)) {
       sort_cands(cnt);
       if (maxc > 0 && cnt > maxc) cnt = maxc;
+    }
+    return cnt;
+  }
+
+  __device__ int fc_count(int nr, int g, double fD, int64_t fI) {
+    if (tid == 0) { sh->counter = 0; sh->qcount = 0; }
+    __syncthreads();
+    fc_pass<FC_COUNT>(nr, g, fD, fI);
+    const int c = sh->counter;
+    __syncthreads();
+    return c;
+  }
+
+  // More survivors than the buffer holds: find the max_candidates-th survivor
+  // of the reference order (-delta, i, j) by counting passes — binary search
+  // over the distinct level differences present, then over i — and collect
+  // only the survivors up to that (delta, i): fewer than max_candidates + n,
+  // which the buffer holds by construction (cap >= max_candidates + n).
+  __device__ int fc_overflow(int nr, int g, int maxc) {
+    AMVM_LOCALS
+    double *dcl = dbuf;  // idle during find_candidates; needs <= kMaxDeltaClasses
+    int32_t *lst = (int32_t *)((double *)scr + kG * kTJ) + 2 * kTJ;
+    if (tid == 0) {
+      int nd = 0, bad = 0;
+      for (int ki = 1; ki < nlev && !bad; ++ki) {
+        if (lst[ki + 1] == lst[ki]) continue;
+        for (int kj = 0; kj < ki && !bad; ++kj) {
+          if (lst[kj + 1] == lst[kj]) continue;
+          const double d = dsub(lv[ki], lv[kj]);
+          int at = 0;
+          while (at < nd && dcl[at] > d) ++at;
+          if (at < nd && dcl[at] == d) continue;
+          if (nd == kMaxDeltaClasses || nd >= n) { bad = 1; break; }
+          for (int q = nd; q > at; --q) dcl[q] = dcl[q - 1];
+          dcl[at] = d;
+          ++nd;
+        }
+      }
+      sh->bc_i[4] = bad ? -1 : nd;
+    }
+    __syncthreads();
+    const int nd = sh->bc_i[4];
+    __syncthreads();
+    if (nd <= 0) {
+      fail(AMVM_ERR_UNSUPPORTED);
+      return (int)cap;
+    }
+    int lo = 0, hi = nd - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (fc_count(nr, g, dcl[mid], INT64_MAX) >= maxc) hi = mid;
+      else lo = mid + 1;
+    }
+    const double dc = dcl[lo];
+    int64_t ilo = 0, ihi = n - 1;
+    while (ilo < ihi) {
+      const int64_t mid = (ilo + ihi) >> 1;
+      if (fc_count(nr, g, dc, mid) >= maxc) ihi = mid;
+      else ilo = mid + 1;
+    }
+    if (tid == 0) { sh->counter = 0; sh->qcount = 0; }
+    __syncthreads();
+    fc_pass<FC_CUT>(nr, g, dc, ilo);
+    int cnt = sh->counter;
+    __syncthreads();
+    if (cnt > cap) {  // impossible: < maxc + n survivors up to the cut
+      fail(AMVM_ERR_UNSUPPORTED);
+      cnt = (int)cap;
     }
     return cnt;
   }
@@ -1004,20 +1101,20 @@ struct Engine {
     if (tid == 0) sh->c.mv_ref += cnt;
     if (tid == 0) sh->c.mv_raw += cnt;
     if (lane == 0) {
-      sh->red[0][warp][0] = wt;
-      sh->red[0][warp][1] = wd;
-      sh->red[0][warp][2] = __longlong_as_double(((int64_t)wi << 32) | (uint32_t)wj);
+      sh->red[warp][0] = wt;
+      sh->red[warp][1] = wd;
+      sh->red[warp][2] = __longlong_as_double(((int64_t)wi << 32) | (uint32_t)wj);
     }
     __syncthreads();
     if (tid == 0) sh->c.pc[6] += clock64() - tf1;
     bool found = false;
     for (int k = 0; k < NW; ++k) {
-      const int64_t ij = __double_as_longlong(sh->red[0][k][2]);
+      const int64_t ij = __double_as_longlong(sh->red[k][2]);
       const int ki = (int)(ij >> 32), kj = (int)(uint32_t)ij;
       if (ki < 0) continue;
-      const double kt = sh->red[0][k][0];
+      const double kt = sh->red[k][0];
       if (!found || kt < bt || (kt == bt && (ki < bi || (ki == bi && kj < bj)))) {
-        found = true; bt = kt; bi = ki; bj = kj; bd = sh->red[0][k][1];
+        found = true; bt = kt; bi = ki; bj = kj; bd = sh->red[k][1];
       }
     }
     __syncthreads();

@@ -279,3 +279,56 @@ def test_ptq_layer_row_matches_reference_golden(amvm):
     assert rep.objective[0] == rec["best_objective"]
     it = int(rec["iterations"])
     np.testing.assert_array_equal(rep.seconds["trace"]["trace_current_t"][0, :it], rec["trace_current_t"])
+
+
+def test_swap_filter_overflow_path_matches_oracle(amvm, oracle):
+    """More filter survivors than a batch slot's buffer (17 instances => the
+    batch cap 1024; n=80 with k_eps=1 keeps ~1500 pairs): the exact overflow
+    path (counting passes + cut) must still return the reference's first
+    max_candidates in (-delta, i, j) order — checked via whole trajectories."""
+    import torch
+
+    from paper_2508_13437_b200 import _native as N
+    from paper_2508_13437_b200.controller import make_params
+
+    rng = np.random.default_rng(21)
+    count, m, n, nlev = 17, 24, 80, 6
+    A = rng.uniform(-1, 1, (m, n))
+    lv = np.sort(rng.uniform(-1, 1, nlev))
+    B = rng.uniform(-1, 1, (count, m))
+    idx0 = rng.integers(0, nlev, (count, n)).astype(np.int32)
+    R0 = np.stack([A @ lv[idx0[k]] - B[k] for k in range(count)])
+    obj0 = np.abs(R0).max(axis=1)
+    cfg = amvm.SolverConfig(max_iters=6, k_eps=1, max_candidates=3, destroy_rate=0.05)
+    prm = make_params(cfg, n)
+    dev = torch.device("cuda")
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
+    At, Bt, Lt = t(A.T, np.float64), t(B, np.float64), t(np.tile(lv, (count, 1)), np.float64)
+    I0, R0t, O0, C0 = t(idx0, np.int32), t(R0, np.float64), t(obj0, np.float64), t(np.zeros(count), np.int32)
+    rngs = t(N.seed_states(np.arange(count)).view(np.uint8), np.uint8)
+    T = cfg.max_iters
+    bi, br = torch.empty((count, n), dtype=torch.int32, device=dev), torch.empty((count, m), dtype=torch.float64, device=dev)
+    bo, bc = torch.empty(count, dtype=torch.float64, device=dev), torch.empty(count, dtype=torch.int32, device=dev)
+    io, it = torch.empty(count, dtype=torch.float64, device=dev), torch.empty(count, dtype=torch.int32, device=dev)
+    ou = torch.empty((count, 4), dtype=torch.int64, device=dev)
+    tc = torch.empty((count, T), dtype=torch.float64, device=dev)
+    tb = torch.empty((count, T), dtype=torch.float64, device=dev)
+    tp = torch.empty((count, T), dtype=torch.uint8, device=dev)
+    ta = torch.empty((count, T), dtype=torch.uint8, device=dev)
+    res = N.ResultPtrs(N.SolutionPtrs(bi.data_ptr(), br.data_ptr(), bo.data_ptr(), bc.data_ptr()),
+                       io.data_ptr(), it.data_ptr(), ou.data_ptr(), tc.data_ptr(), tb.data_ptr(), tp.data_ptr(),
+                       ta.data_ptr(), None, None)
+    prob = N.Problem(m, n, nlev, count, At.data_ptr(), Bt.data_ptr(), Lt.data_ptr())
+    start = N.SolutionPtrs(I0.data_ptr(), R0t.data_ptr(), O0.data_ptr(), C0.data_ptr())
+    lib = N.load_library()
+    nb = lib.amvm_workspace_bytes(N.C.byref(prob), N.C.byref(prm))
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    N.check(lib.amvm_solve(N.C.byref(prob), N.C.byref(prm), N.C.byref(start), N.ptr(rngs), N.C.byref(res),
+                           N.ptr(ws), N.C.c_size_t(nb), N.stream_handle()), "amvm_solve")
+    N.check(lib.amvm_status(N.ptr(ws), N.stream_handle()), "amvm_solve")
+    oprm = oracle.make_params(n, max_iters=T, k_eps=1, max_candidates=3, destroy_rate=0.05)
+    for k in range(count):
+        out = oracle.solve(A, B[k], lv, idx0[k], R0[k], obj0[k], 0, oprm, oracle.pcg_from_seed(k))
+        assert int(it[k].item()) == int(out["iterations"][0])
+        np.testing.assert_array_equal(tc[k].cpu().numpy(), out["trace_current_t"][0])
+        np.testing.assert_array_equal(bi[k].cpu().numpy(), out["best_idx"][0])
