@@ -289,8 +289,11 @@ def run_e2e(args, X, W, lo, hi, cfg, world):
     steps = max(1, args.steps // 2)
     for _ in range(steps):
         rep = ptq.solve_layer(Xh, Wh, bits=4, cfg=cfg, seeds=rows)
+        rep.rows = rows
         moves += int(rep.moves_scored[:, 0].sum())
         d2h = rep.codes.nbytes + rep.objective.nbytes + rep.iterations.nbytes + rep.moves_scored.nbytes
+        if world > 1:  # the one collective of the design: gather every shard's result
+            ptq.gather_layer(rep, world * rows.size)
     dt = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
@@ -301,7 +304,8 @@ def run_e2e(args, X, W, lo, hi, cfg, world):
         moves = int(mv.item())
     return {"value": moves / dt, "unit": "moves/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "path": "ptq.solve_layer (host X, W rows -> device prepare + solve -> host codes)"}
+            "path": "ptq.solve_layer (host X, W rows -> device prepare + solve -> host codes)"
+                    + (" + NCCL all_gather of all shards" if world > 1 else "")}
 
 
 def main():

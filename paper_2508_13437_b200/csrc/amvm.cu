@@ -314,12 +314,12 @@ int occupancy(size_t smem, bool op, int *blocks) {
 
 size_t smem_for(int nt, int64_t m, int64_t nlev, int cr_smem, int tab) {
   (void)nt;
-  return smem_bytes<256>(m, nlev, cr_smem, tab);
+  return smem_bytes<AMVM_NT>(m, nlev, cr_smem, tab);
 }
 
 int occupancy_for(int nt, size_t smem, bool op, int *blocks) {
   (void)nt;
-  return occupancy<256>(smem, op, blocks);
+  return occupancy<AMVM_NT>(smem, op, blocks);
 }
 
 constexpr size_t kSmemMax = 220 * 1024;
@@ -332,8 +332,8 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
       prm->n_segment < 1)
     return AMVM_ERR_INVALID;
   int nt = prm->threads;
-  if (nt == 0) nt = 256;
-  if (nt != 256) return AMVM_ERR_UNSUPPORTED;  // this build instantiates NT = 256
+  if (nt == 0) nt = AMVM_NT;
+  if (nt != AMVM_NT) return AMVM_ERR_UNSUPPORTED;  // this build instantiates one CTA size
   P->nt = nt;
   P->tab = p->nlev <= kTabMaxLev;
   P->cr_smem = p->m * 8 <= 96 * 1024;
@@ -398,8 +398,8 @@ int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
   int rc = occupancy_for(P.nt, P.smem, op, &blocks);  // also sets the smem attribute
   if (rc) return rc;
   const dim3 grid((unsigned)P.slots), block((unsigned)P.nt);
-  if (op) k_op<256><<<grid, block, P.smem, st>>>(a);
-  else k_solve<256><<<grid, block, P.smem, st>>>(a);
+  if (op) k_op<AMVM_NT><<<grid, block, P.smem, st>>>(a);
+  else k_solve<AMVM_NT><<<grid, block, P.smem, st>>>(a);
   return cuda_rc(cudaGetLastError());
 }
 

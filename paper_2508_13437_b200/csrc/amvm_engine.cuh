@@ -27,17 +27,20 @@ namespace amvm {
 #ifndef AMVM_FC_UNROLL2
 #define AMVM_FC_UNROLL2 1
 #endif
+#ifndef AMVM_NT
+#define AMVM_NT 256  // CTA size of the engine kernels
+#endif
 #ifndef AMVM_MIN_BLOCKS
 #define AMVM_MIN_BLOCKS 2
 #endif
 constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
 constexpr int kWS = 32;        // one_opt screened window (columns per barrier)
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
-constexpr int kTJ = 512;       // find_candidates j-tile (level-sorted positions)
+constexpr int kTJ = 2 * AMVM_NT;  // find_candidates j-tile (level-sorted positions)
 constexpr int kRowPasses = 8;  // queue rows drained from an smem-gathered row
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
-constexpr int kTC = 256;       // impact tile: columns (= CTA size: one column per thread)
+constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
 
 // Phase-shared smem scratch: the impact tile or the find_candidates tiles.
