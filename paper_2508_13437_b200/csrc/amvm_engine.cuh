@@ -4,17 +4,18 @@
 // from an atomic counter), so an ALNS iteration — select, destroy, repair,
 // local search, accept, weight update, trace — never leaves the SM
 // (controller.py:233-275).  Inside the CTA:
-//   * thread t owns residual rows i = t + k*NT, so every rank-1/rank-2 update
-//     (core.py:208-245) is thread-local and needs no barrier;
-//   * block-uniform scalars (objectives, refresh counters, operator bank) are
-//     replicated in every thread's registers and evolve identically;
-//   * RNG draws and the few inherently sequential scans (Floyd sampling,
-//     cumsum of the worst-remove cdf) run on thread 0 and are broadcast;
-//   * A is column-major (At), so scoring streams each column once, coalesced
-//     across the CTA (localsearch.py:73-79), and W = 16 columns are scored
-//     per barrier with a speculative window: all columns of the window see
-//     the same residual, the lowest improving column is applied (exactly the
-//     sequential first-improvement of one_opt) and scanning resumes after it.
+//   * thread t owns residual rows i = t + k*NT, so rank-1/rank-2 updates
+//     (core.py:208-245) are thread-local;
+//   * block-uniform scalars (objectives, refresh counters) are replicated in
+//     every thread's registers and evolve identically; cold uniform state
+//     (pointers, params, operator bank, counters) lives in shared memory;
+//   * RNG draws and the inherently sequential scans (Floyd sampling, the
+//     worst-remove cdf) run on thread 0 / warp 0 and are broadcast;
+//   * A is column-major (At): one_opt scores a column only after exact row
+//     screens fail to reject it (see one_opt), then streams it coalesced;
+//   * every decision reproduces the reference's arithmetic bit for bit
+//     (unfused DMUL/DADD, numpy reduction orders, OpenBLAS dot orders), so the
+//     trajectory equals the reference's.
 #pragma once
 
 #include <cstdint>
@@ -25,7 +26,7 @@
 namespace amvm {
 
 #ifndef AMVM_FC_UNROLL2
-#define AMVM_FC_UNROLL2 1
+#define AMVM_FC_UNROLL2 1  // find_candidates: two j positions per iteration
 #endif
 #ifndef AMVM_NT
 #define AMVM_NT 256  // CTA size of the engine kernels
