@@ -707,7 +707,6 @@ struct Engine {
     int2 *que = (int2 *)(cbuf + cap);
     int2 *pr2 = que + cap;
     const int qcap = (int)cap;
-    const int ll = (int)(nlev * nlev);
     constexpr bool filt = MODE != FC_ALL;
     constexpr bool counting = MODE == FC_COUNT;
     // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
@@ -901,9 +900,6 @@ struct Engine {
     int32_t *lfl = lst + (nlev + 1);
     double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
     int32_t *perm = ibuf;                 // level-sorted position -> variable
-    int2 *que = (int2 *)(cbuf + cap);     // staged-row survivors awaiting the rest
-    int2 *pr2 = que + cap;                // row-pass scratch
-    const int qcap = (int)cap;
     // level buckets
     for (int64_t k = tid; k <= nlev; k += NT) lfl[k] = 0;
     __syncthreads();
