@@ -105,6 +105,22 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   return dmul(dmul(res, __longlong_as_double((long long)(m + 600 + 1023) << 52)), 0x1p-600);
 }
 
+// ------------------------------------------------- async global -> smem
+// LDGSTS: 16-byte copy, zero-filled when `valid` is false (src not read).
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // --------------------------------------------------------------- warp ops
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll

@@ -35,7 +35,8 @@ namespace amvm {
 #define AMVM_MIN_BLOCKS 2
 #endif
 constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
-constexpr int kWS = 32;        // one_opt screened window (columns per barrier)
+constexpr int kCW = 16;        // one_opt window: columns per warp (window = NW * kCW)
+constexpr int kB = 8;          // one_opt second screen: flagged columns per batch
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 constexpr int kTJ = 2 * AMVM_NT;  // find_candidates j-tile (level-sorted positions)
 constexpr int kRowPasses = 8;  // queue rows drained from an smem-gathered row
@@ -43,6 +44,8 @@ constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differe
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
+constexpr int kIR = 8;         // impact stream (n >= NT): rows per slice
+constexpr int kIS = 3;         // impact stream: ring stages
 
 // Phase-shared smem scratch: the impact tile or the find_candidates tiles.
 __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
@@ -50,6 +53,8 @@ __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
   fc = (fc + 15) & ~(size_t)15;
   if (tab) fc += 8 * kG * nlev * nlev;
   size_t imp = 8 * kTC * (kTK + 1) + 16 * kTK;
+  const size_t ring = 8 * (size_t)kIS * kTC * kIR;
+  if (ring > imp) imp = ring;
   return fc > imp ? fc : imp;
 }
 
@@ -96,7 +101,7 @@ struct WsHeader {
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
-  size_t ur, crg, uidx, cidx, dmv, dpv, dbuf, pbuf, cbk, gsc, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
+  size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, gsc, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
       hset, rem, sav, pick, coin, ibuf, srt, total;
   int64_t nleaf, kk, hsz;
 };
@@ -121,8 +126,6 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.crg = o; o = al256(o + 8 * m);
   L.uidx = o; o = al256(o + 4 * n);
   L.cidx = o; o = al256(o + 4 * n);
-  L.dmv = o; o = al256(o + 8 * n);
-  L.dpv = o; o = al256(o + 8 * n);
   L.dbuf = o; o = al256(o + 8 * n);
   L.pbuf = o; o = al256(o + 8 * n);
   L.cbk = o; o = al256(o + 8 * ((n + 31) / 32 + 2));
@@ -158,7 +161,7 @@ struct Ctx {
   const double *At, *b;
   double *cr, *ur;
   int32_t *cidx, *uidx;
-  double *dmv, *dpv, *dbuf, *pbuf, *cbk, *gsc;
+  double *dbuf, *pbuf, *cbk, *gsc;
   int64_t *lf_lo, *lf_len;
   double *lf_sum;
   int nleaf_m, nleaf_n, tab;
@@ -188,8 +191,6 @@ struct Ctx {
   [[maybe_unused]] double *const ur = sh->c.ur;                                           \
   [[maybe_unused]] int32_t *const cidx = sh->c.cidx;                                      \
   [[maybe_unused]] int32_t *const uidx = sh->c.uidx;                                      \
-  [[maybe_unused]] double *const dmv = sh->c.dmv;                                         \
-  [[maybe_unused]] double *const dpv = sh->c.dpv;                                         \
   [[maybe_unused]] double *const dbuf = sh->c.dbuf;                                       \
   [[maybe_unused]] double *const pbuf = sh->c.pbuf;                                       \
   [[maybe_unused]] double *const cbk = sh->c.cbk;                                         \
@@ -230,8 +231,10 @@ struct Shared {
   int gnext;
   int qnext;
   int srow[kS];
-  int wpre[kWS + 1];
-  unsigned sflag[NT / 32];
+  int wk[2][NT / 32 * kCW];     // one_opt window: level index per column
+  unsigned sflag[2][NT / 32];   // one_opt window: first-screen survivors per warp
+  int wsum[2][NT / 32];         // one_opt window: valid candidates per warp
+  unsigned rejw[2][2][NT / 32]; // one_opt batch: second-screen rejections per warp
   uint64_t skey[NT];
   int sidx[NT];
   Pcg rng;
@@ -343,12 +346,6 @@ struct Engine {
   }
 
   // ------------------------------------------------------------- one_opt
-  __device__ void set_deltas(int64_t j, int k) {
-    AMVM_LOCALS
-    dmv[j] = k > 0 ? dsub(lv[k - 1], lv[k]) : 0.0;
-    dpv[j] = k + 1 < nlev ? dsub(lv[k + 1], lv[k]) : 0.0;
-  }
-
   // Exact max_i |cr_i + d*col_i| for both candidates of one column (CTA-wide).
   __device__ void exact_pair_max(const double *col, double dm, double dp, double &tm, double &tp) {
     AMVM_LOCALS
@@ -416,108 +413,158 @@ struct Engine {
   // one_opt, localsearch.py:59-88, exact and in the reference's order, with a
   // row screen: a shift can only improve if EVERY row stays below t, so one
   // screening row with |s_r + d*a_rj| >= t proves the candidate does not
-  // improve.  Per window of kWS columns each warp screens 4 columns (lane =
-  // screening row x candidate); columns with a surviving candidate are then
-  // scored over all m rows exactly, in ascending order, and the first that
-  // strictly improves is applied (first improvement), scanning resumes after it.
+  // improve.  A window is NW*kCW columns: each warp screens kCW of them against
+  // the kS largest-|s| rows (lane = row, all loads issued together, one
+  // barrier per window); the flagged columns then get a second screen in
+  // batches of kB (each thread one of the CTA's per-thread-max rows, one
+  // barrier per batch); survivors are scored over all m rows exactly, in
+  // ascending order, and the first that strictly improves is applied (first
+  // improvement); scanning resumes after it.  Window/batch buffers alternate
+  // by parity, so a buffer is rewritten only after every thread has passed
+  // the barrier that follows its last read.
   __device__ void one_opt() {
     AMVM_LOCALS
-    __syncthreads();
-    for (int64_t j = tid; j < n; j += NT) set_deltas(j, cidx[j]);
+    constexpr int WS = NW * kCW;
     __syncthreads();
     select_screen();
     const int srow_l = sh->srow[lane];
+    int wpar = 0, bpar = 0;
     for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
       bool changed = false;
       int64_t p = 0;
       while (p < n) {
-        const int wc = (int)(n - p < kWS ? n - p : kWS);
+        const int wc = (int)(n - p < WS ? n - p : WS);
         const double rs = cr[srow_l];  // current residual of this lane's screening row
         const double t = cobj;
-        unsigned mine = 0u;  // bit c: column warp*4+c has a surviving candidate
+        const int c0 = warp * kCW;
+        const int64_t jb = p + c0;
+        const int kl = (lane < kCW && c0 + lane < wc) ? cidx[jb + lane] : 0;
+        double a[kCW];
 #pragma unroll
-        for (int c = 0; c < kWS / NW; ++c) {
-          const int w = warp * (kWS / NW) + c;
-          if (w < wc) {
-            const int64_t j = p + w;
-            const int k = cidx[j];
-            const double a = gsc[j * kS + lane];
-            const bool rm = k <= 0 || fabs(dadd(rs, dmul(dmv[j], a))) >= t;
-            const bool rp = k + 1 >= nlev || fabs(dadd(rs, dmul(dpv[j], a))) >= t;
-            // a candidate survives only if no screening row rejects it
-            const bool surv = !__any_sync(AMVM_FULL, rm) || !__any_sync(AMVM_FULL, rp);
-            if (surv) mine |= 1u << c;
+        for (int c = 0; c < kCW; ++c) a[c] = c0 + c < wc ? gsc[(jb + c) * kS + lane] : 0.0;
+        unsigned mine = 0u;  // bit c: column c0+c has a candidate no screening row rejects
+#pragma unroll
+        for (int c = 0; c < kCW; ++c) {
+          const int k = __shfl_sync(AMVM_FULL, kl, c);
+          if (c0 + c < wc) {
+            const double lk = lv[k];
+            const bool hm = k > 0, hp = k + 1 < nlev;
+            const double dm = hm ? dsub(lv[k - 1], lk) : 0.0;
+            const double dp = hp ? dsub(lv[k + 1], lk) : 0.0;
+            const bool rm = !hm || fabs(dadd(rs, dmul(dm, a[c]))) >= t;
+            const bool rp = !hp || fabs(dadd(rs, dmul(dp, a[c]))) >= t;
+            if (!__any_sync(AMVM_FULL, rm) || !__any_sync(AMVM_FULL, rp)) mine |= 1u << c;
           }
         }
-        if (lane == 0) sh->sflag[warp] = mine;
-        if (warp == 0) {  // valid candidates per column before any apply (move count)
-          const int k = lane < wc ? cidx[p + lane] : 0;
-          int v = lane < wc ? (k > 0) + (k + 1 < nlev) : 0;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int u = __shfl_up_sync(AMVM_FULL, v, o);
-            if (lane >= o) v += u;
-          }
-          sh->wpre[lane + 1] = v;
-          if (lane == 0) sh->wpre[0] = 0;
+        // valid candidates per column (reference-equivalent move count)
+        const int v = (lane < kCW && c0 + lane < wc) ? (kl > 0) + (kl + 1 < nlev) : 0;
+        const int vsum = __reduce_add_sync(AMVM_FULL, v);
+        if (lane < kCW) sh->wk[wpar][c0 + lane] = kl;
+        if (lane == 0) {
+          sh->sflag[wpar][warp] = mine;
+          sh->wsum[wpar][warp] = vsum;
         }
         __syncthreads();
-        unsigned fl = 0u;
+        unsigned fm[WS / 32];
 #pragma unroll
-        for (int k = 0; k < NW; ++k) fl |= sh->sflag[k] << (k * (kWS / NW));
-        const int upto_cnt_all = sh->wpre[wc];
-        __syncthreads();
-        // reference-equivalent count: both neighbours of every column, as
-        // the sequential sweep evaluates them up to the applied column
+        for (int q = 0; q < WS / 32; ++q) fm[q] = 0u;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) fm[(w * kCW) / 32] |= sh->sflag[wpar][w] << ((w * kCW) % 32);
         int applied = -1;
-        while (fl) {
-          const int w = __ffs(fl) - 1;
-          fl &= fl - 1;
-          const int64_t j = p + w;
-          const int k = cidx[j];
-          {
-            // second screen: every thread tests one of the CTA's per-thread
-            // maximum rows (sorted by select_screen); one load each, one
-            // barrier per candidate, before any full-column pass
-            const int rA = sh->sidx[tid];
-            const double aA = __ldg(At + j * m + rA);
-            const double rr = cr[rA];
-            const double t2 = cobj;
-            const bool em = k <= 0 || fabs(dadd(rr, dmul(dmv[j], aA))) >= t2;
-            const bool ep = k + 1 >= nlev || fabs(dadd(rr, dmul(dpv[j], aA))) >= t2;
-            const bool rej_m = __syncthreads_or(em);
-            const bool rej_p = __syncthreads_or(ep);
-            if (rej_m && rej_p) continue;
-          }
-          double tm, tpv;
-          if (tid == 0) sh->c.pc[11] += 1;
-          exact_pair_max(At + j * m, dmv[j], dpv[j], tm, tpv);
-          int lvl = -1;
-          double bt = cobj;
-          if (k > 0 && tm < bt) { bt = tm; lvl = k - 1; }
-          if (k + 1 < nlev && tpv < bt) { bt = tpv; lvl = k + 1; }
-          if (lvl >= 0) {
-            applied = w;
-            if (tid == 0) sh->c.pc[12] += 1;
-            const double d = dsub(lv[lvl], lv[k]);
-            const double *col = At + j * m;
-            for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
-            __syncthreads();  // all reads of cidx[j] / dmv done; residual published
-            if (tid == 0) {
-              cidx[j] = lvl;
-              set_deltas(j, lvl);
+        int q = 0;
+        const int rA = sh->sidx[tid];
+        for (;;) {
+          int cols[kB];
+          int nb = 0;
+#pragma unroll
+          for (int e = 0; e < kB; ++e) {
+            while (q < WS / 32 && fm[q] == 0u) ++q;
+            cols[e] = 0;
+            if (q < WS / 32) {
+              cols[e] = q * 32 + __ffs(fm[q]) - 1;
+              fm[q] &= fm[q] - 1u;
+              nb = e + 1;
             }
-            bump_known(bt);
-            __syncthreads();
-            break;
           }
+          if (nb == 0) break;
+          // second screen: one load per thread per flagged column, all issued
+          // together, then one barrier for the batch
+          const double rr = cr[rA];
+          double av[kB];
+#pragma unroll
+          for (int e = 0; e < kB; ++e) av[e] = e < nb ? __ldg(At + (p + cols[e]) * m + rA) : 0.0;
+          unsigned em = 0u, ep = 0u;
+#pragma unroll
+          for (int e = 0; e < kB; ++e) {
+            if (e < nb) {
+              const int k = sh->wk[wpar][cols[e]];
+              const double lk = lv[k];
+              const bool hm = k > 0, hp = k + 1 < nlev;
+              const double dm = hm ? dsub(lv[k - 1], lk) : 0.0;
+              const double dp = hp ? dsub(lv[k + 1], lk) : 0.0;
+              if (!hm || fabs(dadd(rr, dmul(dm, av[e]))) >= t) em |= 1u << e;
+              if (!hp || fabs(dadd(rr, dmul(dp, av[e]))) >= t) ep |= 1u << e;
+            }
+          }
+          em = __reduce_or_sync(AMVM_FULL, em);
+          ep = __reduce_or_sync(AMVM_FULL, ep);
+          if (lane == 0) {
+            sh->rejw[bpar][0][warp] = em;
+            sh->rejw[bpar][1][warp] = ep;
+          }
+          __syncthreads();
+          unsigned rjm = 0u, rjp = 0u;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            rjm |= sh->rejw[bpar][0][w];
+            rjp |= sh->rejw[bpar][1][w];
+          }
+          bpar ^= 1;
+          for (int e = 0; e < nb; ++e) {
+            if ((rjm >> e) & (rjp >> e) & 1u) continue;
+            const int w = cols[e];
+            const int64_t j = p + w;
+            const int k = sh->wk[wpar][w];
+            const double lk = lv[k];
+            const double dm = k > 0 ? dsub(lv[k - 1], lk) : 0.0;
+            const double dp = k + 1 < nlev ? dsub(lv[k + 1], lk) : 0.0;
+            double tm, tpv;
+            if (tid == 0) sh->c.pc[11] += 1;
+            exact_pair_max(At + j * m, dm, dp, tm, tpv);
+            int lvl = -1;
+            double bt = cobj;
+            if (k > 0 && tm < bt) { bt = tm; lvl = k - 1; }
+            if (k + 1 < nlev && tpv < bt) { bt = tpv; lvl = k + 1; }
+            if (lvl >= 0) {
+              applied = w;
+              if (tid == 0) sh->c.pc[12] += 1;
+              const double d = dsub(lv[lvl], lk);
+              const double *col = At + j * m;
+              for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
+              __syncthreads();  // all reads of cidx[j] done; residual published
+              if (tid == 0) cidx[j] = lvl;
+              bump_known(bt);
+              __syncthreads();
+              break;
+            }
+          }
+          if (applied >= 0) break;
         }
         if (tid == 0) {
-          const int64_t cnt = applied >= 0 ? sh->wpre[applied + 1] : upto_cnt_all;
+          int64_t cnt = 0;
+          if (applied >= 0) {
+            for (int c = 0; c <= applied; ++c) {
+              const int k = sh->wk[wpar][c];
+              cnt += (k > 0) + (k + 1 < nlev);
+            }
+          } else {
+            for (int w = 0; w < NW; ++w) cnt += sh->wsum[wpar][w];
+          }
           sh->c.mv_ref += cnt;
           sh->c.mv_raw += cnt;
           sh->c.pc[13] += 1;
         }
+        wpar ^= 1;
         if (applied >= 0) {
           changed = true;
           p = p + applied + 1;
@@ -1166,6 +1213,10 @@ struct Engine {
     const double t = cobj;
     const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
     const double na = -alpha;
+    if (n >= NT) {
+      impact_stream(na, t, tot);
+      return;
+    }
     double *tile = (double *)scr;                      // kTC x (kTK+1)
     double *rowv = tile + kTC * (kTK + 1);             // kTK x {|s_k|, (-alpha)(t - |s_k|)}
     for (int64_t cb = 0; cb < n; cb += kTC) {
@@ -1206,6 +1257,78 @@ struct Engine {
       }
       if (tid < cols) dbuf[cb + tid] = ddiv(acc, tot);
       __syncthreads();
+    }
+    __syncthreads();
+  }
+
+  // Wide instances (n >= NT): thread tid owns column cb + tid outright and
+  // adds its terms in row order straight from a kIS-stage cp.async ring of
+  // kIR-row slices of its own column (16-byte chunks XOR-swizzled by tid, so
+  // the ring is bank-conflict free).  Every thread only reads what it copied,
+  // so the stream needs no barrier: kIS - 1 slices are always in flight while
+  // one is scored.  Same operations in the same order as the tiled path.
+  __device__ void impact_stream(double na, double t, double tot) {
+    AMVM_LOCALS
+    double *const ring = (double *)scr;  // kIS stages x NT threads x kIR doubles
+    const bool vec = (m & 1) == 0 && (((uintptr_t)At) & 15) == 0;
+    const int64_t ntile = (m + kIR - 1) / kIR;
+    const int sw = tid & 3;
+    double *const mine = ring + tid * kIR;
+    for (int64_t cb = 0; cb < n; cb += NT) {
+      const int64_t c = cb + tid;
+      const bool col_ok = c < n;
+      const double *colp = At + (col_ok ? c : 0) * m;
+      auto issue = [&](int64_t tix) {
+        if (tix < ntile) {
+          double *dst = mine + (tix % kIS) * (NT * kIR);
+          const int64_t kb = tix * kIR;
+          if (vec) {
+#pragma unroll
+            for (int p = 0; p < kIR / 2; ++p) {
+              const bool v = col_ok && kb + 2 * p < m;
+              cp_async16(dst + 2 * (p ^ sw), v ? colp + kb + 2 * p : At, v);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < kIR; ++k) {
+              const bool v = col_ok && kb + k < m;
+              cp_async8(dst + 2 * ((k >> 1) ^ sw) + (k & 1), v ? colp + kb + k : At, v);
+            }
+          }
+        }
+        cp_async_commit();  // one group per slice (empty past the end)
+      };
+#pragma unroll 1
+      for (int s0 = 0; s0 < kIS; ++s0) issue(s0);
+      double acc = 0.0;
+#pragma unroll 1
+      for (int64_t tix = 0; tix < ntile; ++tix) {
+        cp_async_wait<kIS - 1>();  // slice tix has landed
+        const double *src = mine + (tix % kIS) * (NT * kIR);
+        const int64_t kb = tix * kIR;
+        const int rws = (int)(m - kb < kIR ? m - kb : kIR);
+        double av[kIR];
+#pragma unroll
+        for (int k = 0; k < kIR; ++k) av[k] = fabs(src[2 * ((k >> 1) ^ sw) + (k & 1)]);
+#pragma unroll
+        for (int k = 0; k < kIR; ++k) {
+          if (k < rws) {
+            const double sv = fabs(cr[kb + k]);
+            const double w = dmul(na, dsub(t, sv));
+            const double a = av[k];
+            const double as = a > 0.0 ? a : 1.0;
+            double y;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+            y = dfma(y, dfma(-as, y, 1.0), y);
+            y = dfma(y, dfma(-as, y, 1.0), y);
+            const double term = dmul(sv, exp_nonpos(dmul(w, y)));
+            acc = dadd(acc, a > 0.0 ? term : 0.0);
+          }
+        }
+        issue(tix + kIS);  // into the stage just consumed (its values are in registers)
+      }
+      cp_async_wait<0>();
+      if (col_ok) dbuf[c] = ddiv(acc, tot);
     }
     __syncthreads();
   }
@@ -1548,8 +1671,6 @@ struct Engine {
       c.ur = (double *)(base + L.ur);
       c.uidx = (int32_t *)(base + L.uidx);
       c.cidx = (int32_t *)(base + L.cidx);
-      c.dmv = (double *)(base + L.dmv);
-      c.dpv = (double *)(base + L.dpv);
       c.dbuf = (double *)(base + L.dbuf);
       c.pbuf = (double *)(base + L.pbuf);
       c.cbk = (double *)(base + L.cbk);
