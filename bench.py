@@ -255,6 +255,8 @@ def run_amvm(args, rank, world):
         "gpu_launches": args.steps,
         "roofline": roof,
         "phase_share": {nm: round(float(v / pc.sum()), 4) for nm, v in zip(names, pc)} if pc.sum() else {},
+        "busy_gcycles_per_step": round(float(pc.sum()) / 1e9 / args.steps, 3),
+        "ms_steps": [round(a.elapsed_time(b), 2) for a, b in ev],
         "clocks": clocks,
     }
     if e2e:

@@ -25,9 +25,6 @@
 
 namespace amvm {
 
-#ifndef AMVM_FC_UNROLL2
-#define AMVM_FC_UNROLL2 1  // find_candidates: two j positions per iteration
-#endif
 #ifndef AMVM_NT
 #define AMVM_NT 256  // CTA size of the engine kernels
 #endif
@@ -48,9 +45,12 @@ constexpr int kIR = 8;         // impact stream (n >= NT): rows per slice
 constexpr int kIS = 3;         // impact stream: ring stages
 
 // Phase-shared smem scratch: the impact tile or the find_candidates tiles.
+// find_candidates scratch: level-bucket bounds first (live across the bucket
+// sort, which reuses everything after them), then the staged tiles.
+__host__ __device__ inline size_t fc_tb_off(int64_t nlev) { return ((size_t)8 * (nlev + 2) + 15) & ~(size_t)15; }
+
 __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
-  size_t fc = 8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2);
-  fc = (fc + 15) & ~(size_t)15;
+  size_t fc = fc_tb_off(nlev) + 8 * kG * kTJ + 4 * 2 * kTJ;
   if (tab) fc += 8 * kG * nlev * nlev;
   size_t imp = 8 * kTC * (kTK + 1) + 16 * kTK;
   const size_t ring = 8 * (size_t)kIS * kTC * kIR;
@@ -291,7 +291,9 @@ struct Engine {
   // Solution.refresh (core.py:173-177): numpy A @ x - b in the OpenBLAS order.
   __device__ void refresh() {
     AMVM_LOCALS
+#ifndef AMVM_FC_STATS
     if (tid == 0) sh->c.pc[15] += 1;
+#endif
     __syncthreads();  // publish cidx
     if (m == 1) {
       if (warp == 0) {
@@ -470,20 +472,33 @@ struct Engine {
         for (int q = 0; q < WS / 32; ++q) fm[q] = 0u;
 #pragma unroll
         for (int w = 0; w < NW; ++w) fm[(w * kCW) / 32] |= sh->sflag[wpar][w] << ((w * kCW) % 32);
+        // smallest flagged column >= c (WS if none); unrolled so fm stays in registers
+        auto next_flag = [&](int c) {
+          int r = WS;
+#pragma unroll
+          for (int w4 = WS / 32 - 1; w4 >= 0; --w4) {
+            unsigned word = fm[w4];
+            if (c >= w4 * 32 + 32) word = 0u;
+            else if (c > w4 * 32) word &= ~0u << (c - w4 * 32);
+            if (word) r = w4 * 32 + __ffs(word) - 1;
+          }
+          return r;
+        };
         int applied = -1;
-        int q = 0;
+        int cnext = 0;
         const int rA = sh->sidx[tid];
         for (;;) {
           int cols[kB];
           int nb = 0;
 #pragma unroll
           for (int e = 0; e < kB; ++e) {
-            while (q < WS / 32 && fm[q] == 0u) ++q;
-            cols[e] = 0;
-            if (q < WS / 32) {
-              cols[e] = q * 32 + __ffs(fm[q]) - 1;
-              fm[q] &= fm[q] - 1u;
+            const int cf = next_flag(cnext);
+            cols[e] = cf < WS ? cf : 0;
+            if (cf < WS) {
               nb = e + 1;
+              cnext = cf + 1;
+            } else {
+              cnext = WS;
             }
           }
           if (nb == 0) break;
@@ -529,7 +544,9 @@ struct Engine {
             const double dm = k > 0 ? dsub(lv[k - 1], lk) : 0.0;
             const double dp = k + 1 < nlev ? dsub(lv[k + 1], lk) : 0.0;
             double tm, tpv;
+#ifndef AMVM_FC_STATS
             if (tid == 0) sh->c.pc[11] += 1;
+#endif
             exact_pair_max(At + j * m, dm, dp, tm, tpv);
             int lvl = -1;
             double bt = cobj;
@@ -537,7 +554,9 @@ struct Engine {
             if (k + 1 < nlev && tpv < bt) { bt = tpv; lvl = k + 1; }
             if (lvl >= 0) {
               applied = w;
+#ifndef AMVM_FC_STATS
               if (tid == 0) sh->c.pc[12] += 1;
+#endif
               const double d = dsub(lv[lvl], lk);
               const double *col = At + j * m;
               for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
@@ -745,11 +764,12 @@ struct Engine {
   template <int MODE>
   __device__ void fc_pass(int nr, int g, double fD, int64_t fI) {
     AMVM_LOCALS
-    double *tb = (double *)scr;
+    // scratch: [lst, lfl | tb | tl | tj | bt] (fc_scr_off)
+    int32_t *lst = (int32_t *)scr;
+    double *tb = (double *)(scr + fc_tb_off(nlev));
     int32_t *tl = (int32_t *)(tb + kG * kTJ);
     int32_t *tj = tl + kTJ;
-    int32_t *lst = tj + kTJ;
-    double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
+    double *bt = (double *)(tj + kTJ);
     int32_t *perm = ibuf;
     int2 *que = (int2 *)(cbuf + cap);
     int2 *pr2 = que + cap;
@@ -821,6 +841,13 @@ struct Engine {
             wend = v > wend ? v : wend;
           }
           const int e0 = (int)(s0 - p0), e1 = (int)(wend - p0), emine = (int)(mine - p0);
+#ifdef AMVM_FC_STATS
+          if (lane == 0) atomicAdd((unsigned long long *)&sh->c.pc[14], (unsigned long long)(e1 - e0));
+          {
+            const int u = __reduce_add_sync(AMVM_FULL, emine - e0);
+            if (lane == 0) atomicAdd((unsigned long long *)&sh->c.pc[15], (unsigned long long)u);
+          }
+#endif
           // survivors of the staged rows: straight into the candidate list when
           // they are all the rows, else into the queue for the remaining rows
           auto emit = [&](int e, bool alive) {
@@ -840,6 +867,9 @@ struct Engine {
             } else {
               int bse = 0;
               if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
+#ifdef AMVM_FC_STATS
+              if (lane == 0) atomicAdd((unsigned long long *)&sh->c.pc[11], (unsigned long long)__popc(bal));
+#endif
               bse = __shfl_sync(AMVM_FULL, bse, 0);
               if (alive) {
                 const int qp = bse + __popc(bal & ((1u << lane) - 1u));
@@ -848,36 +878,75 @@ struct Engine {
               }
             }
           };
-          if (g == kG && AMVM_FC_UNROLL2) {
+          if (g == kG) {
             // common case: every staged row present; the tile is row-
             // interleaved per position (one 64-byte broadcast record), two
-            // positions per iteration for independent dependency chains
-            int e = e0;
-            for (; e + 1 < e1; e += 2) {
-              const double2 *ta = reinterpret_cast<const double2 *>(tb + e * kG);
-              const double2 *tc = reinterpret_cast<const double2 *>(tb + (e + 1) * kG);
-              double va[kG], vc[kG];
+            // positions per iteration for independent dependency chains;
+            // alive bits collect in a 32-position mask flushed with one scan
+            // and one atomic per warp (survivors are ~1% of the pairs)
+            const bool lane_ok = !filt || delta > fD || (int64_t)i <= fI;
+            for (int cb = e0; cb < e1; cb += 32) {
+              const int ce = e1 - cb < 32 ? e1 - cb : 32;
+              unsigned msk = 0u;
+              int u = 0;
+              for (; u + 1 < ce; u += 2) {
+                const double2 *ta = reinterpret_cast<const double2 *>(tb + (cb + u) * kG);
+                const double2 *tc = reinterpret_cast<const double2 *>(tb + (cb + u + 1) * kG);
+                double va[kG], vc[kG];
 #pragma unroll
-              for (int h = 0; h < kG / 2; ++h) {
-                const double2 x = ta[h], y = tc[h];
-                va[2 * h] = x.x; va[2 * h + 1] = x.y;
-                vc[2 * h] = y.x; vc[2 * h + 1] = y.y;
+                for (int h = 0; h < kG / 2; ++h) {
+                  const double2 x = ta[h], y = tc[h];
+                  va[2 * h] = x.x; va[2 * h + 1] = x.y;
+                  vc[2 * h] = y.x; vc[2 * h + 1] = y.y;
+                }
+                bool aa = cb + u < emine, ac = cb + u + 1 < emine;
+#pragma unroll
+                for (int q = 1; q < kG; ++q) {
+                  aa &= dsub(va[q], bi[q]) < bq[q];
+                  ac &= dsub(vc[q], bi[q]) < bq[q];
+                }
+                msk |= ((unsigned)aa | ((unsigned)ac << 1)) << u;
               }
-              bool aa = e < emine, ac = e + 1 < emine;
+              if (u < ce) {
+                const double *tq = tb + (cb + u) * kG;
+                bool alive = cb + u < emine;
 #pragma unroll
-              for (int q = 1; q < kG; ++q) {
-                aa &= dsub(va[q], bi[q]) < bq[q];
-                ac &= dsub(vc[q], bi[q]) < bq[q];
+                for (int q = 1; q < kG; ++q) alive &= dsub(tq[q], bi[q]) < bq[q];
+                msk |= (unsigned)alive << u;
               }
-              emit(e, aa);
-              emit(e + 1, ac);
-            }
-            if (e < e1) {
-              const double *tq = tb + e * kG;
-              bool alive = e < emine;
+              if (!lane_ok) msk = 0u;
+              if (!__any_sync(AMVM_FULL, msk != 0u)) continue;
+              const int c = __popc(msk);
+              int incl = c;
 #pragma unroll
-              for (int q = 1; q < kG; ++q) alive &= dsub(tq[q], bi[q]) < bq[q];
-              emit(e, alive);
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(AMVM_FULL, incl, o);
+                if (lane >= o) incl += y;
+              }
+              const int tot = __shfl_sync(AMVM_FULL, incl, 31);
+              if (nr <= g && counting) {
+                if (lane == 0) atomicAdd(&sh->counter, tot);
+                continue;
+              }
+              int bse = 0;
+              if (lane == 0) bse = atomicAdd(nr <= g ? &sh->counter : &sh->qcount, tot);
+#ifdef AMVM_FC_STATS
+              if (lane == 0 && nr > g) atomicAdd((unsigned long long *)&sh->c.pc[11], (unsigned long long)tot);
+#endif
+              int pos = __shfl_sync(AMVM_FULL, bse, 0) + incl - c;
+              while (msk) {
+                const int uu = __ffs(msk) - 1;
+                msk &= msk - 1u;
+                const int32_t j = tj[cb + uu];
+                if (nr <= g) {
+                  if (pos < cap) cbuf[pos] = Cand{i, j, delta};
+                } else if (pos < qcap) {
+                  que[pos] = make_int2(i, j);
+                } else if (fc_rest(i, j, delta, nr, g)) {
+                  fc_append(i, j, delta, counting);
+                }
+                ++pos;
+              }
             }
           } else {
             for (int e = e0; e < e1; ++e) {
@@ -924,6 +993,9 @@ struct Engine {
           qn = sh->qnext;
           __syncthreads();
         }
+#ifdef AMVM_FC_STATS
+        if (tid == 0) sh->c.pc[12] += qn;
+#endif
         for (int e = tid; e < qn; e += NT) {
           const int2 pr = que[e];
           const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
@@ -940,12 +1012,12 @@ struct Engine {
     AMVM_LOCALS
     const int nr = select_rows();
     const int g = nr < kG ? nr : kG;
-    double *tb = (double *)scr;
+    int32_t *lst = (int32_t *)scr;
+    int32_t *lfl = lst + (nlev + 1);
+    double *tb = (double *)(scr + fc_tb_off(nlev));
     int32_t *tl = (int32_t *)(tb + kG * kTJ);
     int32_t *tj = tl + kTJ;
-    int32_t *lst = tj + kTJ;
-    int32_t *lfl = lst + (nlev + 1);
-    double *bt = (double *)(scr + (((size_t)(8 * kG * kTJ + 4 * 2 * kTJ + 4 * 2 * (nlev + 2)) + 15) & ~(size_t)15));
+    double *bt = (double *)(tj + kTJ);
     int32_t *perm = ibuf;                 // level-sorted position -> variable
     // level buckets
     for (int64_t k = tid; k <= nlev; k += NT) lfl[k] = 0;
@@ -970,28 +1042,63 @@ struct Engine {
     {
       int64_t n2 = 1;
       while (n2 < n) n2 <<= 1;
-      int32_t *sl = (int32_t *)srt;
-      int32_t *sj = sl + n2;
-      double *sb = (double *)(sj + n2);
-      for (int64_t e = tid; e < n2; e += NT) {
-        if (e < n) {
-          const int32_t j = perm[e];
-          const double a = __ldg(At + (int64_t)j * m + rows[0]);
-          sl[e] = cidx[j];
-          sj[e] = j;
-          sb[e] = rsgn[0] ? a : -a;
-        } else {
-          sl[e] = 0x7fffffff;
-          sj[e] = 0;
-          sb[e] = 0.0;
+      if (n2 <= 65536 && nlev <= 32768 && fc_tb_off(nlev) + (size_t)12 * n2 <= scratch_bytes(nlev, tab)) {
+        // in shared memory (after the bucket bounds): key (level << 16 | j)
+        // + b0, one compare-exchange pair per thread per step
+        double *sb = (double *)(scr + fc_tb_off(nlev));
+        uint32_t *sk = (uint32_t *)(sb + n2);
+        for (int64_t e = tid; e < n2; e += NT) {
+          if (e < n) {
+            const int32_t j = perm[e];
+            const double a = __ldg(At + (int64_t)j * m + rows[0]);
+            sk[e] = ((uint32_t)cidx[j] << 16) | (uint32_t)j;
+            sb[e] = rsgn[0] ? a : -a;
+          } else {
+            sk[e] = 0xffffffffu;
+            sb[e] = 0.0;
+          }
         }
-      }
-      __syncthreads();
-      for (int64_t k = 2; k <= n2; k <<= 1) {
-        for (int64_t jj = k >> 1; jj > 0; jj >>= 1) {
-          for (int64_t e = tid; e < n2; e += NT) {
-            const int64_t x = e ^ jj;
-            if (x > e) {
+        __syncthreads();
+        for (int64_t k = 2; k <= n2; k <<= 1) {
+          for (int64_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int64_t t = tid; t < (n2 >> 1); t += NT) {
+              const int64_t e = ((t & ~(jj - 1)) << 1) | (t & (jj - 1)), x = e | jj;
+              const uint32_t ka = sk[e], kb = sk[x];
+              const double ba = sb[e], bb = sb[x];
+              const uint32_t la = ka >> 16, lb = kb >> 16;
+              const bool gt = la > lb || (la == lb && (ba > bb || (ba == bb && ka > kb)));
+              if (((e & k) == 0) == gt) {
+                sk[e] = kb; sk[x] = ka;
+                sb[e] = bb; sb[x] = ba;
+              }
+            }
+            __syncthreads();
+          }
+        }
+        for (int64_t e = tid; e < n; e += NT) perm[e] = (int32_t)(sk[e] & 0xffffu);
+        __syncthreads();
+      } else {
+        int32_t *sl = (int32_t *)srt;
+        int32_t *sj = sl + n2;
+        double *sb = (double *)(sj + n2);
+        for (int64_t e = tid; e < n2; e += NT) {
+          if (e < n) {
+            const int32_t j = perm[e];
+            const double a = __ldg(At + (int64_t)j * m + rows[0]);
+            sl[e] = cidx[j];
+            sj[e] = j;
+            sb[e] = rsgn[0] ? a : -a;
+          } else {
+            sl[e] = 0x7fffffff;
+            sj[e] = 0;
+            sb[e] = 0.0;
+          }
+        }
+        __syncthreads();
+        for (int64_t k = 2; k <= n2; k <<= 1) {
+          for (int64_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int64_t t = tid; t < (n2 >> 1); t += NT) {
+              const int64_t e = ((t & ~(jj - 1)) << 1) | (t & (jj - 1)), x = e | jj;
               const int32_t la = sl[e], lb = sl[x];
               const double ba = sb[e], bb = sb[x];
               const bool gt = la > lb || (la == lb && (ba > bb || (ba == bb && sj[e] > sj[x])));
@@ -1001,12 +1108,12 @@ struct Engine {
                 const int32_t t0 = sj[e]; sj[e] = sj[x]; sj[x] = t0;
               }
             }
+            __syncthreads();
           }
-          __syncthreads();
         }
+        for (int64_t e = tid; e < n; e += NT) perm[e] = sj[e];
+        __syncthreads();
       }
-      for (int64_t e = tid; e < n; e += NT) perm[e] = sj[e];
-      __syncthreads();
     }
     // staged rows in level-sorted order, sign folded: ag[q*n + pos]
     for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
@@ -1062,7 +1169,7 @@ struct Engine {
   __device__ int fc_overflow(int nr, int g, int maxc) {
     AMVM_LOCALS
     double *dcl = dbuf;  // idle during find_candidates; needs <= kMaxDeltaClasses
-    int32_t *lst = (int32_t *)((double *)scr + kG * kTJ) + 2 * kTJ;
+    int32_t *lst = (int32_t *)scr;
     if (tid == 0) {
       int nd = 0, bad = 0;
       for (int ki = 1; ki < nlev && !bad; ++ki) {
@@ -1414,7 +1521,9 @@ struct Engine {
       return;
     }
     impact_scores(alpha);
+#ifndef AMVM_FC_STATS
     if (tid == 0) sh->c.pc[14] += 1;
+#endif
     auto gd = [&](int64_t k) { return dbuf[k]; };
     if (block_pairwise(gd, n, lf_lo + nleaf_m, lf_len + nleaf_m, nleaf_n) <= 0.0) {
       random_destroy(r);
