@@ -10,7 +10,8 @@ warm start w_r, seed r (builders.py:355-372 semantics, one X for the layer).
 A step = one amvm_solve over this rank's block of `--rows` rows for `--iters`
 ALNS iterations each, from the prepared start (the device-resident path; X, B,
 levels and start residuals already in HBM).  Weak scaling: rank k owns rows
-[k*rows, (k+1)*rows).  `value` = reference-equivalent candidate moves scored
+[k*rows, (k+1)*rows); the default 1792 rows per GPU make N = 8 exactly the
+full 14336-row layer.  `value` = reference-equivalent candidate moves scored
 per second (1-OPT neighbours, 2 per greedy variable, filtered
 swap candidates), summed over ranks / max-over-ranks device time.
 `e2e` = the same metric through the public API (ptq.solve_layer) with X and W
@@ -45,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="amvm", choices=["amvm", "reference"])
-    ap.add_argument("--rows", type=int, default=1184, help="rows of the layer per GPU per step")
+    ap.add_argument("--rows", type=int, default=D_OUT // 8,
+                    help="rows of the layer per GPU per step (default 1792: the whole layer at 8 GPUs)")
     ap.add_argument("--iters", type=int, default=2, help="ALNS iterations per row per step")
     ap.add_argument("--cpu-rows", type=int, default=16, help="rows in the CPU baseline sample")
     ap.add_argument("--no-e2e", action="store_true")

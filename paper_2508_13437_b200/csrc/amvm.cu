@@ -22,13 +22,49 @@ __global__ void __launch_bounds__(NT, AMVM_MIN_BLOCKS) k_solve(KArgs a) {
   Engine<NT> E;
   E.bind(a, smem, blockIdx.x);
   WsHeader *hdr = (WsHeader *)a.ws;
+  // Tasks: without chunking, task t = instance t.  Chunked: task t = (chunk
+  // t / count, instance t % count), handed out in order, so every instance's
+  // chunk c is taken before any chunk c + 1 and the batch's tail is one chunk,
+  // not one whole instance.  A task waits for its instance's previous chunk
+  // (taken earlier by a running CTA, so this cannot deadlock; with count >=
+  // resident CTAs it almost never waits).  One call site of solve_instance
+  // keeps the engine inlined.
+  // (loop state lives in shared memory and kernel parameters, not registers:
+  // the engine inlined below needs all of them)
   for (;;) {
-    if (threadIdx.x == 0) E.sh->bc_i[15] = atomicAdd(&hdr->next, 1);
+    if (threadIdx.x == 0) {
+      const int64_t nch = a.chunk_iters > 0 && a.prm.max_iters > 0
+                              ? (a.prm.max_iters + a.chunk_iters - 1) / a.chunk_iters : 1;
+      const unsigned long long t = atomicAdd(&hdr->next_task, 1ull);
+      const int64_t inst = (int64_t)(t % a.count), chunk = (int64_t)(t / a.count);
+      int skip = 0;
+      if (a.chunk_iters > 0 && t < (unsigned long long)a.count * nch) {
+        int32_t *prog = &((InstState *)(a.ist + inst * a.ist_bytes))->progress;
+        int p;
+        while ((p = atomicAdd(prog, 0)) < chunk) __nanosleep(1000);
+        __threadfence();
+        skip = p > chunk;  // finished early: nothing left to run
+      }
+      E.sh->task_live = t < (unsigned long long)a.count * nch;
+      E.sh->task_skip = skip;
+      E.sh->task_inst = inst;
+      E.sh->task_chunk = chunk;
+    }
     __syncthreads();
-    const int64_t inst = E.sh->bc_i[15];
+    const bool live = E.sh->task_live, skip = E.sh->task_skip;
     __syncthreads();
-    if (inst >= a.count) break;
-    E.solve_instance(a, inst);
+    if (!live) break;
+    if (skip) continue;
+    const bool done = E.solve_instance(a, E.sh->task_inst, E.sh->task_chunk);
+    if (a.chunk_iters > 0) {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int64_t nch = a.prm.max_iters > 0 ? (a.prm.max_iters + a.chunk_iters - 1) / a.chunk_iters : 1;
+        atomicExch(&((InstState *)(a.ist + E.sh->task_inst * a.ist_bytes))->progress,
+                   done ? (int)nch : (int)E.sh->task_chunk + 1);
+      }
+    }
   }
 }
 
@@ -286,6 +322,8 @@ struct Plan {
   int cr_smem, tab, cap;
   size_t slot_bytes;
   int64_t slots;
+  size_t ist_bytes;  // per parked instance (chunked solve), 0 otherwise
+  int chunk_iters;
   size_t ws_bytes;
 };
 
@@ -323,6 +361,10 @@ int occupancy_for(int nt, size_t smem, bool op, int *blocks) {
 }
 
 constexpr size_t kSmemMax = 220 * 1024;
+#ifndef AMVM_CHUNK_ITERS
+#define AMVM_CHUNK_ITERS 1
+#endif
+constexpr int kChunkIters = AMVM_CHUNK_ITERS;  // chunked solve: ALNS iterations per task
 
 int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   if (!p || !prm) return AMVM_ERR_INVALID;
@@ -372,7 +414,11 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
     if (blocks < 1) return AMVM_ERR_UNSUPPORTED;
     P->slots = std::min<int64_t>(p->count, (int64_t)blocks * sms);
   }
-  P->ws_bytes = sizeof(WsHeader) + (size_t)P->slots * P->slot_bytes;
+  // more instances than resident CTAs: solve in chunks of kChunkIters
+  // iterations so instances migrate between CTAs and the tail is one chunk
+  P->chunk_iters = (!op && p->count > P->slots && prm->max_iters > kChunkIters) ? kChunkIters : 0;
+  P->ist_bytes = P->chunk_iters ? inst_layout(p->m, p->n).total : 0;
+  P->ws_bytes = sizeof(WsHeader) + (size_t)P->slots * P->slot_bytes + (size_t)p->count * P->ist_bytes;
   return AMVM_OK;
 }
 
@@ -386,6 +432,9 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
   a.prm = *prm;
   a.ws = (unsigned char *)ws;
   a.slot_bytes = P.slot_bytes;
+  a.chunk_iters = P.chunk_iters;
+  a.ist_bytes = P.ist_bytes;
+  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + (size_t)P.slots * P.slot_bytes : nullptr;
   a.cr_smem = P.cr_smem; a.tab = P.tab; a.cap = P.cap;
   a.time_budget_ns = prm->time_limit_s < 0 ? -1 : (int64_t)(prm->time_limit_s * 1e9);
   return a;
@@ -394,6 +443,10 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
 int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(a.ws, 0, sizeof(WsHeader), st);
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  if (a.ist) {  // progress = 0 for every parked instance
+    e = cudaMemset2DAsync(a.ist, a.ist_bytes, 0, sizeof(InstState), (size_t)a.count, st);
+    if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  }
   int blocks = 0;
   int rc = occupancy_for(P.nt, P.smem, op, &blocks);  // also sets the smem attribute
   if (rc) return rc;

@@ -79,8 +79,11 @@ struct KArgs {
   int32_t *s_cnt;
   amvm_pcg64 *rng;
   amvm_result res;
-  unsigned char *ws;  // workspace base (header + slots)
+  unsigned char *ws;  // workspace base (header + slots [+ parked instances])
   size_t slot_bytes;
+  unsigned char *ist;  // parked per-instance state (chunked solve), else null
+  size_t ist_bytes;
+  int chunk_iters;     // iterations per task (0: one task per instance)
   int cr_smem, tab, cap;
   int64_t time_budget_ns;  // < 0: none
   // component-op extras
@@ -96,8 +99,33 @@ enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, O
 struct WsHeader {
   int32_t status;
   int32_t next;
-  int32_t pad[62];
+  unsigned long long next_task;  // chunked solve: (chunk, instance) tasks handed out
+  int32_t pad[60];
 };
+
+// A parked instance between chunks of a chunked solve (the persistent part
+// of the ALNS state: current solution, best objective, operator bank, RNG
+// lives in amvm_solve's rng array).  progress = chunks done; an instance that
+// stops early jumps to the last chunk so later tasks for it are no-ops.
+struct InstState {
+  int32_t progress, it, ucnt, bcnt;
+  double uobj, bobj;
+  double w[4], sc[4];
+  int64_t seg[4], life[4], bit;
+  int64_t mv_ref, mv_raw, elapsed_ns;
+  int64_t pc[16];
+};
+
+struct InstLayout {
+  size_t r, idx, total;
+};
+__host__ __device__ inline InstLayout inst_layout(int64_t m, int64_t n) {
+  InstLayout L;
+  L.r = (sizeof(InstState) + 255) & ~(size_t)255;
+  L.idx = L.r + (((size_t)8 * m + 255) & ~(size_t)255);
+  L.total = L.idx + (((size_t)4 * n + 255) & ~(size_t)255);
+  return L;
+}
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
@@ -237,6 +265,8 @@ struct Shared {
   unsigned rejw[2][2][NT / 32]; // one_opt batch: second-screen rejections per warp
   uint64_t skey[NT];
   int sidx[NT];
+  int64_t task_inst, task_chunk;  // k_solve: the task being run (kept out of registers)
+  int task_live, task_skip;
   Pcg rng;
   Ctx c;
 };
@@ -1822,11 +1852,12 @@ struct Engine {
 
   __device__ void load_rng(const amvm_pcg64 *st) {
     AMVM_LOCALS
-    if (tid == 0) {
-      sh->rng.s = ((unsigned __int128)st->state_hi << 64) | st->state_lo;
-      sh->rng.inc = ((unsigned __int128)st->inc_hi << 64) | st->inc_lo;
-      sh->rng.has32 = st->has_uint32;
-      sh->rng.u32 = st->uinteger;
+    if (tid == 0) {  // L2 reads: a chunked solve may have parked it from another SM
+      const unsigned long long *q = (const unsigned long long *)st;
+      sh->rng.s = ((unsigned __int128)__ldcg(q) << 64) | __ldcg(q + 1);
+      sh->rng.inc = ((unsigned __int128)__ldcg(q + 2) << 64) | __ldcg(q + 3);
+      sh->rng.has32 = __ldcg(&st->has_uint32);
+      sh->rng.u32 = __ldcg(&st->uinteger);
     }
   }
 
@@ -1844,34 +1875,70 @@ struct Engine {
 
   // ------------------------------------------------------- solve (one inst)
   // solve, controller.py:211-286, from the host-computed initial solution.
-  __device__ void solve_instance(const KArgs &a, int64_t inst) {
+  // With a.chunk_iters = K > 0 the call runs iterations [chunk*K, chunk*K+K)
+  // only, resuming from / parking to the instance's InstState, so instances
+  // migrate between CTAs at iteration boundaries (load balance).  Returns
+  // true when the instance is finished (results written).
+  __device__ bool solve_instance(const KArgs &a, int64_t inst, int64_t chunk = 0) {
     AMVM_LOCALS
     load_levels(a, inst);
     const amvm_result &res = a.res;
-    for (int64_t i = tid; i < m; i += NT) ur[i] = a.s_r[inst * m + i];
-    for (int64_t j = tid; j < n; j += NT) uidx[j] = a.s_idx[inst * n + j];
-    uobj = a.s_obj[inst];
-    ucnt = a.s_cnt[inst];
-    __syncthreads();
-    write_best(inst, res);
-    load_rng(&a.rng[inst]);
-    if (tid == 0) {
-      for (int k = 0; k < 4; ++k) {
-        sh->c.w[k] = 1.0; sh->c.sc[k] = 0.0; sh->c.seg[k] = 0; sh->c.life[k] = 0;
-      }
-      sh->c.bit = 0;
-    }
-    if (tid == 0) {
-      sh->c.mv_ref = sh->c.mv_raw = 0;
-      for (int k = 0; k < 16; ++k) sh->c.pc[k] = 0;
-    }
-    const int64_t r = a.prm.r;
     const int T = a.prm.max_iters;
-    const uint64_t t_start = gtimer();
-    bool cand_is_cur = false;
+    const int K = a.chunk_iters;
+    InstState *st = K > 0 ? (InstState *)(a.ist + inst * a.ist_bytes) : nullptr;
+    const InstLayout IL = inst_layout(m, n);
     int it = 0;
-    while (it < T) {
-      if (bobj == 0.0) break;
+    int64_t elapsed = 0;
+    if (chunk == 0) {
+      for (int64_t i = tid; i < m; i += NT) ur[i] = a.s_r[inst * m + i];
+      for (int64_t j = tid; j < n; j += NT) uidx[j] = a.s_idx[inst * n + j];
+      uobj = a.s_obj[inst];
+      ucnt = a.s_cnt[inst];
+      __syncthreads();
+      write_best(inst, res);
+      if (tid == 0) {
+        for (int k = 0; k < 4; ++k) {
+          sh->c.w[k] = 1.0; sh->c.sc[k] = 0.0; sh->c.seg[k] = 0; sh->c.life[k] = 0;
+        }
+        sh->c.bit = 0;
+        sh->c.mv_ref = sh->c.mv_raw = 0;
+        for (int k = 0; k < 16; ++k) sh->c.pc[k] = 0;
+      }
+    } else {  // resume a parked instance (L2 reads: parked by another SM)
+      const double *sr = (const double *)((const unsigned char *)st + IL.r);
+      const int32_t *si = (const int32_t *)((const unsigned char *)st + IL.idx);
+      for (int64_t i = tid; i < m; i += NT) ur[i] = __ldcg(sr + i);
+      for (int64_t j = tid; j < n; j += NT) uidx[j] = __ldcg(si + j);
+      uobj = __ldcg(&st->uobj);
+      bobj = __ldcg(&st->bobj);
+      ucnt = __ldcg(&st->ucnt);
+      bcnt = __ldcg(&st->bcnt);
+      it = __ldcg(&st->it);
+      elapsed = __ldcg((const long long *)&st->elapsed_ns);
+      if (tid == 0) {
+        for (int k = 0; k < 4; ++k) {
+          sh->c.w[k] = __ldcg(&st->w[k]); sh->c.sc[k] = __ldcg(&st->sc[k]);
+          sh->c.seg[k] = __ldcg((const long long *)&st->seg[k]);
+          sh->c.life[k] = __ldcg((const long long *)&st->life[k]);
+        }
+        sh->c.bit = __ldcg((const long long *)&st->bit);
+        sh->c.mv_ref = __ldcg((const long long *)&st->mv_ref);
+        sh->c.mv_raw = __ldcg((const long long *)&st->mv_raw);
+        for (int k = 0; k < 16; ++k) sh->c.pc[k] = __ldcg((const long long *)&st->pc[k]);
+      }
+      __syncthreads();
+    }
+    load_rng(&a.rng[inst]);
+    const int it_end = K > 0 && (int64_t)T - it > K ? it + K : T;
+    const int64_t r = a.prm.r;
+    const uint64_t t_start = gtimer() - (uint64_t)elapsed;
+    bool cand_is_cur = false;
+    bool finished = false;
+    while (it < it_end) {
+      if (bobj == 0.0) {
+        finished = true;
+        break;
+      }
       long long tp = clock64(), tq;
       if (tid == 0) {
         int stop = 0;
@@ -1882,7 +1949,10 @@ struct Engine {
       __syncthreads();
       const int stop = sh->bc_i[0], pair = sh->bc_i[1];
       __syncthreads();
-      if (stop) break;
+      if (stop) {
+        finished = true;
+        break;
+      }
       ++it;
       if (!cand_is_cur) cand_from_cur();
       cand_is_cur = false;
@@ -1918,6 +1988,25 @@ struct Engine {
       }
       if (tid == 0) sh->c.pc[7] += clock64() - tp;
     }
+    if (!finished && it < T) {  // park for the next chunk
+      double *sr = (double *)((unsigned char *)st + IL.r);
+      int32_t *si = (int32_t *)((unsigned char *)st + IL.idx);
+      for (int64_t i = tid; i < m; i += NT) sr[i] = ur[i];
+      for (int64_t j = tid; j < n; j += NT) si[j] = uidx[j];
+      if (tid == 0) {
+        st->uobj = uobj; st->bobj = bobj; st->ucnt = ucnt; st->bcnt = bcnt; st->it = it;
+        st->elapsed_ns = (int64_t)(gtimer() - t_start);
+        for (int k = 0; k < 4; ++k) {
+          st->w[k] = sh->c.w[k]; st->sc[k] = sh->c.sc[k]; st->seg[k] = sh->c.seg[k]; st->life[k] = sh->c.life[k];
+        }
+        st->bit = sh->c.bit;
+        st->mv_ref = sh->c.mv_ref; st->mv_raw = sh->c.mv_raw;
+        for (int k = 0; k < 16; ++k) st->pc[k] = sh->c.pc[k];
+      }
+      store_rng(&a.rng[inst]);
+      __syncthreads();
+      return false;
+    }
     if (tid == 0) {
       res.best.objective[inst] = bobj;
       res.best.updates[inst] = bcnt;
@@ -1933,6 +2022,7 @@ struct Engine {
     }
     store_rng(&a.rng[inst]);
     __syncthreads();
+    return true;
   }
 
   // ------------------------------------------------- component operations

@@ -281,25 +281,20 @@ def test_ptq_layer_row_matches_reference_golden(amvm):
     np.testing.assert_array_equal(rep.seconds["trace"]["trace_current_t"][0, :it], rec["trace_current_t"])
 
 
-def test_swap_filter_overflow_path_matches_oracle(amvm, oracle):
-    """More filter survivors than a batch slot's buffer (17 instances => the
-    batch cap 1024; n=80 with k_eps=1 keeps ~1500 pairs): the exact overflow
-    path (counting passes + cut) must still return the reference's first
-    max_candidates in (-delta, i, j) order — checked via whole trajectories."""
+def _batch_vs_oracle(amvm, oracle, A, B, lv, idx0, cfg_kw, check=None):
+    """One amvm_solve over a batch sharing A (start = idx0), every checked
+    instance compared with the oracle's solve from the same start and seed."""
     import torch
 
     from paper_2508_13437_b200 import _native as N
     from paper_2508_13437_b200.controller import make_params
 
-    rng = np.random.default_rng(21)
-    count, m, n, nlev = 17, 24, 80, 6
-    A = rng.uniform(-1, 1, (m, n))
-    lv = np.sort(rng.uniform(-1, 1, nlev))
-    B = rng.uniform(-1, 1, (count, m))
-    idx0 = rng.integers(0, nlev, (count, n)).astype(np.int32)
+    count, n = idx0.shape
+    m = A.shape[0]
+    nlev = lv.size
     R0 = np.stack([A @ lv[idx0[k]] - B[k] for k in range(count)])
     obj0 = np.abs(R0).max(axis=1)
-    cfg = amvm.SolverConfig(max_iters=6, k_eps=1, max_candidates=3, destroy_rate=0.05)
+    cfg = amvm.SolverConfig(**cfg_kw)
     prm = make_params(cfg, n)
     dev = torch.device("cuda")
     t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
@@ -326,9 +321,53 @@ def test_swap_filter_overflow_path_matches_oracle(amvm, oracle):
     N.check(lib.amvm_solve(N.C.byref(prob), N.C.byref(prm), N.C.byref(start), N.ptr(rngs), N.C.byref(res),
                            N.ptr(ws), N.C.c_size_t(nb), N.stream_handle()), "amvm_solve")
     N.check(lib.amvm_status(N.ptr(ws), N.stream_handle()), "amvm_solve")
-    oprm = oracle.make_params(n, max_iters=T, k_eps=1, max_candidates=3, destroy_rate=0.05)
-    for k in range(count):
+    okw = {k: v for k, v in cfg_kw.items() if k != "seed"}
+    oprm = oracle.make_params(n, **okw)
+    host = {k: v.cpu().numpy() for k, v in dict(it=it, tc=tc, tb=tb, tp=tp, ta=ta, bi=bi, br=br, bo=bo, ou=ou).items()}
+    for k in (range(count) if check is None else check):
         out = oracle.solve(A, B[k], lv, idx0[k], R0[k], obj0[k], 0, oprm, oracle.pcg_from_seed(k))
-        assert int(it[k].item()) == int(out["iterations"][0])
-        np.testing.assert_array_equal(tc[k].cpu().numpy(), out["trace_current_t"][0])
-        np.testing.assert_array_equal(bi[k].cpu().numpy(), out["best_idx"][0])
+        n_it = int(out["iterations"][0])
+        assert int(host["it"][k]) == n_it, k
+        np.testing.assert_array_equal(host["tc"][k, :n_it], out["trace_current_t"][0, :n_it])
+        np.testing.assert_array_equal(host["tb"][k, :n_it], out["trace_best_t"][0, :n_it])
+        np.testing.assert_array_equal(host["tp"][k, :n_it], out["trace_pair"][0, :n_it])
+        np.testing.assert_array_equal(host["ta"][k, :n_it], out["trace_accepted"][0, :n_it])
+        np.testing.assert_array_equal(host["bi"][k], out["best_idx"][0])
+        np.testing.assert_array_equal(host["br"][k], out["best_residual"][0])
+        assert host["bo"][k] == out["best_objective"][0]
+        np.testing.assert_array_equal(host["ou"][k], out["operator_uses"][0])
+    return host
+
+
+def test_swap_filter_overflow_path_matches_oracle(amvm, oracle):
+    """More filter survivors than a batch slot's buffer (17 instances => the
+    batch cap 1024; n=80 with k_eps=1 keeps ~1500 pairs): the exact overflow
+    path (counting passes + cut) must still return the reference's first
+    max_candidates in (-delta, i, j) order — checked via whole trajectories."""
+    rng = np.random.default_rng(21)
+    count, m, n, nlev = 17, 24, 80, 6
+    A = rng.uniform(-1, 1, (m, n))
+    lv = np.sort(rng.uniform(-1, 1, nlev))
+    B = rng.uniform(-1, 1, (count, m))
+    idx0 = rng.integers(0, nlev, (count, n)).astype(np.int32)
+    _batch_vs_oracle(amvm, oracle, A, B, lv, idx0,
+                     dict(max_iters=6, k_eps=1, max_candidates=3, destroy_rate=0.05))
+
+
+def test_chunked_batch_migrates_bitwise(amvm, oracle):
+    """More instances than resident CTAs: the solve runs one ALNS iteration
+    per task and instances migrate between CTAs (parked state in the
+    workspace).  Trajectories must equal the oracle's; planted instances
+    reach objective 0 mid-run and must stop exactly there."""
+    rng = np.random.default_rng(33)
+    count, m, n, nlev = 700, 18, 14, 5
+    A = rng.integers(-4, 5, (m, n)).astype(float)
+    lv = np.arange(nlev, dtype=float) - 2.0
+    B = rng.integers(-6, 7, (count, m)).astype(float)
+    xs = rng.integers(0, nlev, (count, n))
+    planted = np.arange(count) % 5 == 0
+    B[planted] = np.stack([A @ lv[xs[k]] for k in np.nonzero(planted)[0]])
+    idx0 = rng.integers(0, nlev, (count, n)).astype(np.int32)
+    host = _batch_vs_oracle(amvm, oracle, A, B, lv, idx0, dict(max_iters=9, destroy_rate=0.2),
+                            check=range(0, count, 3))
+    assert (host["it"] < 9).any() and (host["it"] == 9).any()  # both early stops and full runs
