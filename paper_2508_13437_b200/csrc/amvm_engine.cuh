@@ -129,12 +129,16 @@ __host__ __device__ inline InstLayout inst_layout(int64_t m, int64_t n) {
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
-  size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, gsc, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf,
+  size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, gsc, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf, que, rg,
       hset, rem, sav, pick, coin, ibuf, srt, total;
   int64_t nleaf, kk, hsz;
 };
 
 __host__ __device__ inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Survivor queue of find_candidates (pairs alive after the staged rows, all
+// tiles of one call): at least 64K entries; beyond it pairs finish directly.
+__host__ __device__ inline int64_t fc_qcap(int64_t cap) { return cap > 65536 ? cap : 65536; }
 
 __host__ __device__ inline uint64_t gen_mask(uint64_t v) {
   v |= v >> 1; v |= v >> 2; v |= v >> 4; v |= v >> 8; v |= v >> 16; v |= v >> 32;
@@ -165,7 +169,9 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.reps = o; o = al256(o + 8 * L.kk);
   L.rsgn = o; o = al256(o + 4 * L.kk);
   L.ag = o; o = al256(o + 8 * kG * n);
-  L.cbuf = o; o = al256(o + sizeof(Cand) * cap + 2 * sizeof(int2) * cap);  // candidates + survivor queue + scratch
+  L.cbuf = o; o = al256(o + sizeof(Cand) * cap);
+  L.que = o; o = al256(o + 2 * sizeof(Cand) * fc_qcap(cap));  // staged-row survivors, ping-pong
+  L.rg = o; o = al256(o + 8 * kRowPasses * n);                 // rows of the queue passes
   L.hset = o; o = al256(o + 8 * L.hsz);
   L.rem = o; o = al256(o + 4 * rr);
   L.sav = o; o = al256(o + 4 * rr);
@@ -196,7 +202,8 @@ struct Ctx {
   int32_t *rows, *rsgn;
   double *reps, *ag;
   uint32_t off_lv, off_scr;
-  Cand *cbuf;
+  Cand *cbuf, *que;
+  double *rg;
   uint64_t *hset;
   int32_t *rem, *sav, *pick, *coin, *ibuf;
   unsigned char *srt;
@@ -234,6 +241,8 @@ struct Ctx {
   [[maybe_unused]] double *const ag = sh->c.ag;                                           \
   [[maybe_unused]] unsigned char *const scr = amvm_dyn_smem + sh->c.off_scr;               \
   [[maybe_unused]] Cand *const cbuf = sh->c.cbuf;                                         \
+  [[maybe_unused]] Cand *const que = sh->c.que;                                           \
+  [[maybe_unused]] double *const rg = sh->c.rg;                                           \
   [[maybe_unused]] uint64_t *const hset = sh->c.hset;                                     \
   [[maybe_unused]] int32_t *const rem = sh->c.rem;                                        \
   [[maybe_unused]] int32_t *const sav = sh->c.sav;                                        \
@@ -786,6 +795,65 @@ struct Engine {
     return true;
   }
 
+  // Pairs alive after the staged rows (queued by every tile): the next
+  // kRowPasses rows of A are gathered once per call, each pass tests the
+  // whole queue against one row (independent loads) and compacts it (one
+  // atomic per warp) into the other half of the ping-pong queue; the rare
+  // survivors of all passes finish on A directly.
+  __device__ void fc_drain(int nr, int g, bool counting) {
+    AMVM_LOCALS
+    const int qcap = (int)fc_qcap(cap);
+    int qn = sh->qcount < qcap ? sh->qcount : qcap;
+    const int np = nr - g < kRowPasses ? nr - g : kRowPasses;
+    for (int64_t e = tid; e < (int64_t)np * n; e += NT) {
+      const int64_t q = e / n, j = e - q * n;
+      rg[e] = __ldg(At + j * m + rows[g + q]);
+    }
+    if (tid == 0) sh->qnext = 0;
+    __syncthreads();
+    Cand *src = que, *dst = que + qcap;
+    int q = g;
+    int base = 0;  // sh->qnext only grows: pass survivors land at [base, qnext)
+    for (; q < g + np && qn > 0; ++q) {
+      const double *row = rg + (int64_t)(q - g) * n;
+      const double eq = reps[q];
+      const bool pos = rsgn[q] != 0;
+      for (int e0 = warp * 32; e0 < qn; e0 += NT) {
+        const int e = e0 + lane;
+        Cand c{0, 0, 1.0};
+        bool alive = false;
+        if (e < qn) {
+          c = src[e];
+          const double da = dsub(row[c.j], row[c.i]);
+          const double bq = ddiv(eq, c.d);
+          alive = pos ? (da < bq) : (da > -bq);
+        }
+        const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+        if (!bal) continue;
+        int bse = 0;
+        if (lane == 0) bse = atomicAdd(&sh->qnext, __popc(bal));
+        bse = __shfl_sync(AMVM_FULL, bse, 0) - base;
+        if (alive) dst[bse + __popc(bal & ((1u << lane) - 1u))] = c;
+      }
+      __syncthreads();
+      const int tot = sh->qnext;
+      __syncthreads();  // everyone has read it before the next pass adds to it
+      qn = tot - base;
+      base = tot;
+      Cand *t = src; src = dst; dst = t;
+    }
+#ifdef AMVM_FC_STATS
+    if (tid == 0) sh->c.pc[12] += qn;
+#endif
+    for (int e = tid; e < qn; e += NT) {
+      const Cand c = src[e];
+      if (fc_rest(c.i, c.j, c.d, nr, q)) fc_append(c.i, c.j, c.d, counting);
+    }
+    __syncthreads();
+    if (tid == 0) sh->qcount = 0;
+    __syncthreads();
+  }
+
   // One enumeration pass over the staged tiles.  mode FC_ALL collects every
   // survivor; FC_COUNT only counts, FC_CUT collects, the survivors whose key
   // precedes or equals (fD, fI) in the reference order (-delta, i): delta > fD,
@@ -801,9 +869,7 @@ struct Engine {
     int32_t *tj = tl + kTJ;
     double *bt = (double *)(tj + kTJ);
     int32_t *perm = ibuf;
-    int2 *que = (int2 *)(cbuf + cap);
-    int2 *pr2 = que + cap;
-    const int qcap = (int)cap;
+    const int qcap = (int)fc_qcap(cap);
     constexpr bool filt = MODE != FC_ALL;
     constexpr bool counting = MODE == FC_COUNT;
     // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
@@ -903,7 +969,7 @@ struct Engine {
               bse = __shfl_sync(AMVM_FULL, bse, 0);
               if (alive) {
                 const int qp = bse + __popc(bal & ((1u << lane) - 1u));
-                if (qp < qcap) que[qp] = make_int2(i, tj[e]);
+                if (qp < qcap) que[qp] = Cand{i, tj[e], delta};
                 else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta, counting);
               }
             }
@@ -971,7 +1037,7 @@ struct Engine {
                 if (nr <= g) {
                   if (pos < cap) cbuf[pos] = Cand{i, j, delta};
                 } else if (pos < qcap) {
-                  que[pos] = make_int2(i, j);
+                  que[pos] = Cand{i, j, delta};
                 } else if (fc_rest(i, j, delta, nr, g)) {
                   fc_append(i, j, delta, counting);
                 }
@@ -991,50 +1057,8 @@ struct Engine {
         }
       }
       __syncthreads();
-      if (nr > g) {
-        // drain the queue row by row: gather row q of A for every variable
-        // into the (now free) tile smem, test all queued pairs against it
-        // (independent loads, full memory parallelism), compact the
-        // survivors, next row; the rare long survivors finish on A directly
-        int qn = sh->qcount < qcap ? sh->qcount : qcap;
-        double *rowbuf = pbuf;  // n doubles (pbuf is idle during find_candidates)
-        const bool fits = true;
-        int q = g;
-        for (; fits && q < nr && q < g + kRowPasses && qn > 0; ++q) {
-          const int64_t rq = rows[q];
-          for (int64_t j = tid; j < n; j += NT) rowbuf[j] = __ldg(At + j * m + rq);
-          if (tid == 0) sh->qnext = 0;
-          __syncthreads();
-          const double eq = reps[q];
-          const bool pos = rsgn[q] != 0;
-          for (int e = tid; e < qn; e += NT) {
-            const int2 pr = que[e];
-            const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
-            const double da = dsub(rowbuf[pr.y], rowbuf[pr.x]);
-            const double bq = ddiv(eq, delta);
-            pr2[e] = (pos ? (da < bq) : (da > -bq)) ? pr : make_int2(-1, -1);
-          }
-          __syncthreads();
-          for (int e = tid; e < qn; e += NT) {
-            const int2 pr = pr2[e];
-            if (pr.x >= 0) que[atomicAdd(&sh->qnext, 1)] = pr;
-          }
-          __syncthreads();
-          qn = sh->qnext;
-          __syncthreads();
-        }
-#ifdef AMVM_FC_STATS
-        if (tid == 0) sh->c.pc[12] += qn;
-#endif
-        for (int e = tid; e < qn; e += NT) {
-          const int2 pr = que[e];
-          const double delta = dsub(lv[cidx[pr.x]], lv[cidx[pr.y]]);
-          if (fc_rest(pr.x, pr.y, delta, nr, q)) fc_append(pr.x, pr.y, delta, counting);
-        }
-        __syncthreads();
-        if (tid == 0) sh->qcount = 0;
-      }
     }
+    if (nr > g) fc_drain(nr, g, counting);
     __syncthreads();
   }
 
@@ -1822,6 +1846,8 @@ struct Engine {
       c.rsgn = (int32_t *)(base + L.rsgn);
       c.ag = (double *)(base + L.ag);
       c.cbuf = (Cand *)(base + L.cbuf);
+      c.que = (Cand *)(base + L.que);
+      c.rg = (double *)(base + L.rg);
       c.hset = (uint64_t *)(base + L.hset);
       c.rem = (int32_t *)(base + L.rem);
       c.sav = (int32_t *)(base + L.sav);

@@ -101,7 +101,10 @@ class LayerBatch:
             self.prepare()
         dev = self.device
         seeds = self.rows if seeds is None else np.asarray(seeds)
-        self.rng = torch.from_numpy(N.seed_states(seeds).view(np.uint8)).to(dev)
+        # pinned + non_blocking: the upload is stream-ordered and the host does
+        # not wait for earlier work (back-to-back solves stay queued)
+        self._rng_host = torch.from_numpy(N.seed_states(seeds).view(np.uint8)).pin_memory()
+        self.rng = self._rng_host.to(dev, non_blocking=True)
         T = max(int(cfg.max_iters), 1)
         c, m, n = self.count, self.m, self.n
         o = {
