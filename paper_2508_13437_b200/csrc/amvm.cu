@@ -68,6 +68,22 @@ __global__ void __launch_bounds__(NT, AMVM_MIN_BLOCKS) k_solve(KArgs a) {
   }
 }
 
+// Ar[i*n + j] = At[j*m + i]: 32x32 tiles through shared memory, both sides
+// coalesced.  grid (ceil(n/32), ceil(m/32)), block (32, 8).
+__global__ void k_transpose(const double *__restrict__ At, double *__restrict__ Ar, int64_t m, int64_t n) {
+  __shared__ double t[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    t[r][threadIdx.x] = (j < n && i < m) ? At[j * m + i] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    if (i < m && j < n) Ar[i * n + j] = t[threadIdx.x][r];
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_op(KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -418,7 +434,8 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   // iterations so instances migrate between CTAs and the tail is one chunk
   P->chunk_iters = (!op && p->count > P->slots && prm->max_iters > kChunkIters) ? kChunkIters : 0;
   P->ist_bytes = P->chunk_iters ? inst_layout(p->m, p->n).total : 0;
-  P->ws_bytes = sizeof(WsHeader) + (size_t)P->slots * P->slot_bytes + (size_t)p->count * P->ist_bytes;
+  P->ws_bytes = sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + (size_t)P->slots * P->slot_bytes +
+                (size_t)p->count * P->ist_bytes;
   return AMVM_OK;
 }
 
@@ -434,7 +451,9 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
   a.slot_bytes = P.slot_bytes;
   a.chunk_iters = P.chunk_iters;
   a.ist_bytes = P.ist_bytes;
-  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + (size_t)P.slots * P.slot_bytes : nullptr;
+  a.Ar = (const double *)(a.ws + sizeof(WsHeader));
+  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + (size_t)P.slots * P.slot_bytes
+                      : nullptr;
   a.cr_smem = P.cr_smem; a.tab = P.tab; a.cap = P.cap;
   a.time_budget_ns = prm->time_limit_s < 0 ? -1 : (int64_t)(prm->time_limit_s * 1e9);
   return a;
@@ -450,6 +469,10 @@ int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
   int blocks = 0;
   int rc = occupancy_for(P.nt, P.smem, op, &blocks);  // also sets the smem attribute
   if (rc) return rc;
+  {  // row-major copy of A for the row gathers (filter rows, screening rows)
+    const dim3 tg((unsigned)((a.n + 31) / 32), (unsigned)((a.m + 31) / 32)), tb(32, 8);
+    k_transpose<<<tg, tb, 0, st>>>(a.At, (double *)a.Ar, a.m, a.n);
+  }
   const dim3 grid((unsigned)P.slots), block((unsigned)P.nt);
   if (op) k_op<AMVM_NT><<<grid, block, P.smem, st>>>(a);
   else k_solve<AMVM_NT><<<grid, block, P.smem, st>>>(a);

@@ -72,6 +72,7 @@ extern __shared__ __align__(16) unsigned char amvm_dyn_smem[];
 struct KArgs {
   int64_t m, n, nlev, count;
   const double *At, *B, *levels;
+  const double *Ar;  // row-major copy of A (m x n), built in the workspace
   amvm_params prm;
   // start solution (solve) or in/out solution (component ops)
   int32_t *s_idx;
@@ -96,7 +97,7 @@ struct KArgs {
 
 enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR };
 
-struct WsHeader {
+struct WsHeader {  // 256 bytes
   int32_t status;
   int32_t next;
   unsigned long long next_task;  // chunked solve: (chunk, instance) tasks handed out
@@ -116,6 +117,9 @@ struct InstState {
   int64_t pc[16];
 };
 
+// Workspace: [WsHeader | Ar (row-major copy of A) | slots | parked instances]
+__host__ __device__ inline size_t ws_ar_bytes(int64_t m, int64_t n) { return ((size_t)8 * m * n + 255) & ~(size_t)255; }
+
 struct InstLayout {
   size_t r, idx, total;
 };
@@ -129,7 +133,7 @@ __host__ __device__ inline InstLayout inst_layout(int64_t m, int64_t n) {
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
-  size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, gsc, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf, que, rg,
+  size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf, que,
       hset, rem, sav, pick, coin, ibuf, srt, total;
   int64_t nleaf, kk, hsz;
 };
@@ -161,7 +165,6 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.dbuf = o; o = al256(o + 8 * n);
   L.pbuf = o; o = al256(o + 8 * n);
   L.cbk = o; o = al256(o + 8 * ((n + 31) / 32 + 2));
-  L.gsc = o; o = al256(o + 8 * kS * n);
   L.lf_lo = o; o = al256(o + 16 * L.nleaf);
   L.lf_len = o; o = al256(o + 16 * L.nleaf);
   L.lf_sum = o; o = al256(o + 8 * L.nleaf);
@@ -171,7 +174,6 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.ag = o; o = al256(o + 8 * kG * n);
   L.cbuf = o; o = al256(o + sizeof(Cand) * cap);
   L.que = o; o = al256(o + 2 * sizeof(Cand) * fc_qcap(cap));  // staged-row survivors, ping-pong
-  L.rg = o; o = al256(o + 8 * kRowPasses * n);                 // rows of the queue passes
   L.hset = o; o = al256(o + 8 * L.hsz);
   L.rem = o; o = al256(o + 4 * rr);
   L.sav = o; o = al256(o + 4 * rr);
@@ -192,10 +194,10 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
 // not occupy registers the hot loops need.
 struct Ctx {
   int64_t m, n, nlev, kk, cap;
-  const double *At, *b;
+  const double *At, *Ar, *b;
   double *cr, *ur;
   int32_t *cidx, *uidx;
-  double *dbuf, *pbuf, *cbk, *gsc;
+  double *dbuf, *pbuf, *cbk;
   int64_t *lf_lo, *lf_len;
   double *lf_sum;
   int nleaf_m, nleaf_n, tab;
@@ -203,7 +205,6 @@ struct Ctx {
   double *reps, *ag;
   uint32_t off_lv, off_scr;
   Cand *cbuf, *que;
-  double *rg;
   uint64_t *hset;
   int32_t *rem, *sav, *pick, *coin, *ibuf;
   unsigned char *srt;
@@ -220,6 +221,7 @@ struct Ctx {
   [[maybe_unused]] const int64_t m = sh->c.m, n = sh->c.n, nlev = sh->c.nlev;             \
   [[maybe_unused]] const int64_t kk = sh->c.kk, cap = sh->c.cap;                          \
   [[maybe_unused]] const double *const At = sh->c.At;                                     \
+  [[maybe_unused]] const double *const Ar = sh->c.Ar;                                     \
   [[maybe_unused]] const double *const b = sh->c.b;                                       \
   [[maybe_unused]] double *const lv = (double *)(amvm_dyn_smem + sh->c.off_lv);            \
   [[maybe_unused]] double *const cr = sh->c.cr;                                           \
@@ -229,7 +231,6 @@ struct Ctx {
   [[maybe_unused]] double *const dbuf = sh->c.dbuf;                                       \
   [[maybe_unused]] double *const pbuf = sh->c.pbuf;                                       \
   [[maybe_unused]] double *const cbk = sh->c.cbk;                                         \
-  [[maybe_unused]] double *const gsc = sh->c.gsc;                                         \
   [[maybe_unused]] int64_t *const lf_lo = sh->c.lf_lo;                                    \
   [[maybe_unused]] int64_t *const lf_len = sh->c.lf_len;                                  \
   [[maybe_unused]] double *const lf_sum = sh->c.lf_sum;                                   \
@@ -242,7 +243,6 @@ struct Ctx {
   [[maybe_unused]] unsigned char *const scr = amvm_dyn_smem + sh->c.off_scr;               \
   [[maybe_unused]] Cand *const cbuf = sh->c.cbuf;                                         \
   [[maybe_unused]] Cand *const que = sh->c.que;                                           \
-  [[maybe_unused]] double *const rg = sh->c.rg;                                           \
   [[maybe_unused]] uint64_t *const hset = sh->c.hset;                                     \
   [[maybe_unused]] int32_t *const rem = sh->c.rem;                                        \
   [[maybe_unused]] int32_t *const sav = sh->c.sav;                                        \
@@ -416,7 +416,7 @@ struct Engine {
   // Screening rows for one_opt: each thread's largest |s|, then the kS largest
   // of those (a block bitonic sort of NT keys).  ANY row subset gives an exact
   // rejection test; large |s| rows reject almost every non-improving shift.
-  // Gathers gsc[j*kS + s] = A[srow[s], j].
+  // one_opt reads the screening rows straight from the row-major copy Ar.
   __device__ void select_screen() {
     AMVM_LOCALS
     uint64_t best = 0;
@@ -444,11 +444,6 @@ struct Engine {
     }
     if (tid < kS) sh->srow[tid] = sh->sidx[tid < m ? tid : 0];
     __syncthreads();
-    for (int64_t e = tid; e < n * kS; e += NT) {
-      const int64_t j = e / kS, q = e - j * kS;
-      gsc[e] = __ldg(At + j * m + sh->srow[q]);
-    }
-    __syncthreads();
   }
 
   // one_opt, localsearch.py:59-88, exact and in the reference's order, with a
@@ -469,6 +464,7 @@ struct Engine {
     __syncthreads();
     select_screen();
     const int srow_l = sh->srow[lane];
+    const double *arow = Ar + (int64_t)srow_l * n;  // this lane's screening row
     int wpar = 0, bpar = 0;
     for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
       bool changed = false;
@@ -482,7 +478,7 @@ struct Engine {
         const int kl = (lane < kCW && c0 + lane < wc) ? cidx[jb + lane] : 0;
         double a[kCW];
 #pragma unroll
-        for (int c = 0; c < kCW; ++c) a[c] = c0 + c < wc ? gsc[(jb + c) * kS + lane] : 0.0;
+        for (int c = 0; c < kCW; ++c) a[c] = c0 + c < wc ? __ldg(arow + jb + c) : 0.0;
         unsigned mine = 0u;  // bit c: column c0+c has a candidate no screening row rejects
 #pragma unroll
         for (int c = 0; c < kCW; ++c) {
@@ -506,38 +502,31 @@ struct Engine {
           sh->wsum[wpar][warp] = vsum;
         }
         __syncthreads();
-        unsigned fm[WS / 32];
+        // first-screen survivors as a 128-bit mask, popped in ascending order
+        static_assert(WS <= 128, "one_opt window mask is two 64-bit words");
+        uint64_t f0 = 0, f1 = 0;
 #pragma unroll
-        for (int q = 0; q < WS / 32; ++q) fm[q] = 0u;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) fm[(w * kCW) / 32] |= sh->sflag[wpar][w] << ((w * kCW) % 32);
-        // smallest flagged column >= c (WS if none); unrolled so fm stays in registers
-        auto next_flag = [&](int c) {
-          int r = WS;
-#pragma unroll
-          for (int w4 = WS / 32 - 1; w4 >= 0; --w4) {
-            unsigned word = fm[w4];
-            if (c >= w4 * 32 + 32) word = 0u;
-            else if (c > w4 * 32) word &= ~0u << (c - w4 * 32);
-            if (word) r = w4 * 32 + __ffs(word) - 1;
-          }
-          return r;
-        };
+        for (int w = 0; w < NW; ++w) {
+          const uint64_t bits = (uint64_t)sh->sflag[wpar][w] << ((w * kCW) % 64);
+          if ((w * kCW) / 64 == 0) f0 |= bits;
+          else f1 |= bits;
+        }
         int applied = -1;
-        int cnext = 0;
         const int rA = sh->sidx[tid];
         for (;;) {
           int cols[kB];
           int nb = 0;
 #pragma unroll
           for (int e = 0; e < kB; ++e) {
-            const int cf = next_flag(cnext);
-            cols[e] = cf < WS ? cf : 0;
-            if (cf < WS) {
+            cols[e] = 0;
+            if (f0) {
+              cols[e] = __ffsll((long long)f0) - 1;
+              f0 &= f0 - 1;
               nb = e + 1;
-              cnext = cf + 1;
-            } else {
-              cnext = WS;
+            } else if (f1) {
+              cols[e] = 64 + __ffsll((long long)f1) - 1;
+              f1 &= f1 - 1;
+              nb = e + 1;
             }
           }
           if (nb == 0) break;
@@ -788,34 +777,30 @@ struct Engine {
     AMVM_LOCALS
     for (int q = g; q < nr; ++q) {
       const int64_t rq = rows[q];
-      const double da = dsub(__ldg(At + (int64_t)j * m + rq), __ldg(At + i * m + rq));
+      const double da = dsub(__ldg(Ar + rq * n + j), __ldg(Ar + rq * n + i));
       const double bq = ddiv(reps[q], delta);
       if (!(rsgn[q] ? (da < bq) : (da > -bq))) return false;
     }
     return true;
   }
 
-  // Pairs alive after the staged rows (queued by every tile): the next
-  // kRowPasses rows of A are gathered once per call, each pass tests the
-  // whole queue against one row (independent loads) and compacts it (one
-  // atomic per warp) into the other half of the ping-pong queue; the rare
-  // survivors of all passes finish on A directly.
+  // Pairs alive after the staged rows (queued by every tile): each of the
+  // next kRowPasses rows tests the whole queue (independent loads from the
+  // contiguous row of Ar) and compacts it (one atomic per warp) into the
+  // other half of the ping-pong queue; the rare survivors of all passes
+  // finish row by row in fc_rest.
   __device__ void fc_drain(int nr, int g, bool counting) {
     AMVM_LOCALS
     const int qcap = (int)fc_qcap(cap);
     int qn = sh->qcount < qcap ? sh->qcount : qcap;
     const int np = nr - g < kRowPasses ? nr - g : kRowPasses;
-    for (int64_t e = tid; e < (int64_t)np * n; e += NT) {
-      const int64_t q = e / n, j = e - q * n;
-      rg[e] = __ldg(At + j * m + rows[g + q]);
-    }
     if (tid == 0) sh->qnext = 0;
     __syncthreads();
     Cand *src = que, *dst = que + qcap;
     int q = g;
     int base = 0;  // sh->qnext only grows: pass survivors land at [base, qnext)
     for (; q < g + np && qn > 0; ++q) {
-      const double *row = rg + (int64_t)(q - g) * n;
+      const double *row = Ar + (int64_t)rows[q] * n;
       const double eq = reps[q];
       const bool pos = rsgn[q] != 0;
       for (int e0 = warp * 32; e0 < qn; e0 += NT) {
@@ -824,7 +809,7 @@ struct Engine {
         bool alive = false;
         if (e < qn) {
           c = src[e];
-          const double da = dsub(row[c.j], row[c.i]);
+          const double da = dsub(__ldg(row + c.j), __ldg(row + c.i));
           const double bq = ddiv(eq, c.d);
           alive = pos ? (da < bq) : (da > -bq);
         }
@@ -1104,7 +1089,7 @@ struct Engine {
         for (int64_t e = tid; e < n2; e += NT) {
           if (e < n) {
             const int32_t j = perm[e];
-            const double a = __ldg(At + (int64_t)j * m + rows[0]);
+            const double a = __ldg(Ar + (int64_t)rows[0] * n + j);
             sk[e] = ((uint32_t)cidx[j] << 16) | (uint32_t)j;
             sb[e] = rsgn[0] ? a : -a;
           } else {
@@ -1138,7 +1123,7 @@ struct Engine {
         for (int64_t e = tid; e < n2; e += NT) {
           if (e < n) {
             const int32_t j = perm[e];
-            const double a = __ldg(At + (int64_t)j * m + rows[0]);
+            const double a = __ldg(Ar + (int64_t)rows[0] * n + j);
             sl[e] = cidx[j];
             sj[e] = j;
             sb[e] = rsgn[0] ? a : -a;
@@ -1172,7 +1157,7 @@ struct Engine {
     // staged rows in level-sorted order, sign folded: ag[q*n + pos]
     for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
       const int64_t q = e / n, ps = e - q * n;
-      const double a = __ldg(At + (int64_t)perm[ps] * m + rows[q]);
+      const double a = __ldg(Ar + (int64_t)rows[q] * n + perm[ps]);
       ag[e] = rsgn[q] ? a : -a;
     }
     const int ll = (int)(nlev * nlev);
@@ -1824,12 +1809,13 @@ struct Engine {
       c.n = a.n;
       c.nlev = a.nlev;
       c.At = a.At;
+      c.Ar = a.Ar;
       c.prm = a.prm;
       c.cap = a.cap;
       c.tab = a.tab;
       const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap);
       c.kk = L.kk;
-      unsigned char *base = a.ws + sizeof(WsHeader) + (size_t)slot * a.slot_bytes;
+      unsigned char *base = a.ws + sizeof(WsHeader) + ws_ar_bytes(a.m, a.n) + (size_t)slot * a.slot_bytes;
       c.status = (int32_t *)a.ws;
       c.ur = (double *)(base + L.ur);
       c.uidx = (int32_t *)(base + L.uidx);
@@ -1837,7 +1823,6 @@ struct Engine {
       c.dbuf = (double *)(base + L.dbuf);
       c.pbuf = (double *)(base + L.pbuf);
       c.cbk = (double *)(base + L.cbk);
-      c.gsc = (double *)(base + L.gsc);
       c.lf_lo = (int64_t *)(base + L.lf_lo);
       c.lf_len = (int64_t *)(base + L.lf_len);
       c.lf_sum = (double *)(base + L.lf_sum);
@@ -1847,7 +1832,6 @@ struct Engine {
       c.ag = (double *)(base + L.ag);
       c.cbuf = (Cand *)(base + L.cbuf);
       c.que = (Cand *)(base + L.que);
-      c.rg = (double *)(base + L.rg);
       c.hset = (uint64_t *)(base + L.hset);
       c.rem = (int32_t *)(base + L.rem);
       c.sav = (int32_t *)(base + L.sav);
