@@ -119,6 +119,18 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def ncu_traffic(rows: int, iters: int):
+    """DRAM bytes (read + write) of one k_solve launch of this workload, from
+    the committed `ncu --set full` capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "r01_ksolve_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    if d.get("rows") != rows or d.get("iters") != iters:
+        return None
+    return d["dram_bytes_per_launch"]
+
+
 def cpu_baseline(rows: int, iters: int, threads: int) -> dict:
     """The oracle (CPU restatement of the reference, bit-identical trajectories)
     on `rows` rows of the same layer, all host threads."""
@@ -233,7 +245,8 @@ def run_amvm(args, rank, world):
     pc = phase[:8]
     oo_frac = pc[4] / pc.sum() if pc.sum() else 0.0
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": pk["source"],
+            "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(hi - lo, args.iters),
+            "peak_source": pk["source"], "achieved_kind": "effective (algorithmic bytes, SURVEY.md 8d)",
             "kernel": "k_solve (fused ALNS iteration; all phases)",
             "bytes_per_move": bytes_per_move, "V_s": 2,
             "one_opt_phase_share": round(float(oo_frac), 4),
