@@ -41,8 +41,16 @@ constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differe
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
-constexpr int kIR = 8;         // impact stream (n >= NT): rows per slice
-constexpr int kIS = 3;         // impact stream: ring stages
+// impact stream shapes (columns per thread, rows per slice, ring stages):
+// wide instances 4 x 2 x 2 (four independent exp chains per thread),
+// n < 4*NT: 1 x 8 x 3.  Both rings fit the phase scratch.
+#ifndef AMVM_IMPACT_IC
+#define AMVM_IMPACT_IC 4
+#define AMVM_IMPACT_IR 2
+#define AMVM_IMPACT_IS 2
+#endif
+constexpr int kIC4 = AMVM_IMPACT_IC, kIR4 = AMVM_IMPACT_IR, kIS4 = AMVM_IMPACT_IS;
+constexpr int kIC1 = 1, kIR1 = 8, kIS1 = 3;
 
 // Phase-shared smem scratch: the impact tile or the find_candidates tiles.
 // find_candidates scratch: level-bucket bounds first (live across the bucket
@@ -53,7 +61,8 @@ __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
   size_t fc = fc_tb_off(nlev) + 8 * kG * kTJ + 4 * 2 * kTJ;
   if (tab) fc += 8 * kG * nlev * nlev;
   size_t imp = 8 * kTC * (kTK + 1) + 16 * kTK;
-  const size_t ring = 8 * (size_t)kIS * kTC * kIR;
+  const size_t r4 = 8 * (size_t)kIS4 * kIC4 * kTC * kIR4, r1 = 8 * (size_t)kIS1 * kIC1 * kTC * kIR1;
+  const size_t ring = r4 > r1 ? r4 : r1;
   if (ring > imp) imp = ring;
   return fc > imp ? fc : imp;
 }
@@ -1359,8 +1368,12 @@ struct Engine {
     const double t = cobj;
     const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
     const double na = -alpha;
+    if (n >= kIC4 * NT) {
+      impact_stream<kIC4, kIR4, kIS4>(na, t, tot);
+      return;
+    }
     if (n >= NT) {
-      impact_stream(na, t, tot);
+      impact_stream<kIC1, kIR1, kIS1>(na, t, tot);
       return;
     }
     double *tile = (double *)scr;                      // kTC x (kTK+1)
@@ -1407,38 +1420,51 @@ struct Engine {
     __syncthreads();
   }
 
-  // Wide instances (n >= NT): thread tid owns column cb + tid outright and
-  // adds its terms in row order straight from a kIS-stage cp.async ring of
-  // kIR-row slices of its own column (16-byte chunks XOR-swizzled by tid, so
-  // the ring is bank-conflict free).  Every thread only reads what it copied,
-  // so the stream needs no barrier: kIS - 1 slices are always in flight while
-  // one is scored.  Same operations in the same order as the tiled path.
+  // Wide instances (n >= NT): thread tid owns kIC columns (cb + u*NT + tid)
+  // outright and adds each column's terms in row order straight from a
+  // kIS-stage cp.async ring of kIR-row slices of its own columns (16-byte
+  // chunks XOR-swizzled by tid, so the ring is bank-conflict free).  Every
+  // thread only reads what it copied, so the stream needs no barrier: kIS - 1
+  // slices are in flight while one is scored, and the kIC columns are
+  // independent exp chains (ILP).  Same operations in the same order as the
+  // tiled path.
+  template <int kIC, int kIR, int kIS>
   __device__ void impact_stream(double na, double t, double tot) {
     AMVM_LOCALS
-    double *const ring = (double *)scr;  // kIS stages x NT threads x kIR doubles
+    // ring: kIS stages x kIC columns x NT threads x kIR doubles
+    double *const ring = (double *)scr;
     const bool vec = (m & 1) == 0 && (((uintptr_t)At) & 15) == 0;
     const int64_t ntile = (m + kIR - 1) / kIR;
-    const int sw = tid & 3;
-    double *const mine = ring + tid * kIR;
-    for (int64_t cb = 0; cb < n; cb += NT) {
-      const int64_t c = cb + tid;
-      const bool col_ok = c < n;
-      const double *colp = At + (col_ok ? c : 0) * m;
+    static_assert(kIR % 2 == 0 && ((kIR / 2) & (kIR / 2 - 1)) == 0 && kIR <= 8, "kIR/2 chunks, power of 2");
+    const int sw = tid & (kIR / 2 - 1);  // chunk swizzle within a thread's kIR/2 16-byte chunks
+    for (int64_t cb = 0; cb < n; cb += (int64_t)kIC * NT) {
+      const double *colp[kIC];
+      bool col_ok[kIC];
+#pragma unroll
+      for (int u = 0; u < kIC; ++u) {
+        const int64_t c = cb + u * NT + tid;
+        col_ok[u] = c < n;
+        colp[u] = At + (col_ok[u] ? c : 0) * m;
+      }
+      auto slot = [&](int64_t tix, int u) { return ring + (((tix % kIS) * kIC + u) * NT + tid) * kIR; };
       auto issue = [&](int64_t tix) {
         if (tix < ntile) {
-          double *dst = mine + (tix % kIS) * (NT * kIR);
           const int64_t kb = tix * kIR;
-          if (vec) {
 #pragma unroll
-            for (int p = 0; p < kIR / 2; ++p) {
-              const bool v = col_ok && kb + 2 * p < m;
-              cp_async16(dst + 2 * (p ^ sw), v ? colp + kb + 2 * p : At, v);
-            }
-          } else {
+          for (int u = 0; u < kIC; ++u) {
+            double *dst = slot(tix, u);
+            if (vec) {
 #pragma unroll
-            for (int k = 0; k < kIR; ++k) {
-              const bool v = col_ok && kb + k < m;
-              cp_async8(dst + 2 * ((k >> 1) ^ sw) + (k & 1), v ? colp + kb + k : At, v);
+              for (int p = 0; p < kIR / 2; ++p) {
+                const bool v = col_ok[u] && kb + 2 * p < m;
+                cp_async16(dst + 2 * (p ^ sw), v ? colp[u] + kb + 2 * p : At, v);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < kIR; ++k) {
+                const bool v = col_ok[u] && kb + k < m;
+                cp_async8(dst + 2 * ((k >> 1) ^ sw) + (k & 1), v ? colp[u] + kb + k : At, v);
+              }
             }
           }
         }
@@ -1446,35 +1472,38 @@ struct Engine {
       };
 #pragma unroll 1
       for (int s0 = 0; s0 < kIS; ++s0) issue(s0);
-      double acc = 0.0;
+      double acc[kIC];
+#pragma unroll
+      for (int u = 0; u < kIC; ++u) acc[u] = 0.0;
 #pragma unroll 1
       for (int64_t tix = 0; tix < ntile; ++tix) {
         cp_async_wait<kIS - 1>();  // slice tix has landed
-        const double *src = mine + (tix % kIS) * (NT * kIR);
         const int64_t kb = tix * kIR;
         const int rws = (int)(m - kb < kIR ? m - kb : kIR);
-        double av[kIR];
-#pragma unroll
-        for (int k = 0; k < kIR; ++k) av[k] = fabs(src[2 * ((k >> 1) ^ sw) + (k & 1)]);
 #pragma unroll
         for (int k = 0; k < kIR; ++k) {
           if (k < rws) {
             const double sv = fabs(cr[kb + k]);
             const double w = dmul(na, dsub(t, sv));
-            const double a = av[k];
-            const double as = a > 0.0 ? a : 1.0;
-            double y;
-            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
-            y = dfma(y, dfma(-as, y, 1.0), y);
-            y = dfma(y, dfma(-as, y, 1.0), y);
-            const double term = dmul(sv, exp_nonpos(dmul(w, y)));
-            acc = dadd(acc, a > 0.0 ? term : 0.0);
+#pragma unroll
+            for (int u = 0; u < kIC; ++u) {  // independent columns: ILP
+              const double a = fabs(slot(tix, u)[2 * ((k >> 1) ^ sw) + (k & 1)]);
+              const double as = a > 0.0 ? a : 1.0;
+              double y;
+              asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+              y = dfma(y, dfma(-as, y, 1.0), y);
+              y = dfma(y, dfma(-as, y, 1.0), y);
+              const double term = dmul(sv, exp_nonpos(dmul(w, y)));
+              acc[u] = dadd(acc[u], a > 0.0 ? term : 0.0);
+            }
           }
         }
         issue(tix + kIS);  // into the stage just consumed (its values are in registers)
       }
       cp_async_wait<0>();
-      if (col_ok) dbuf[c] = ddiv(acc, tot);
+#pragma unroll
+      for (int u = 0; u < kIC; ++u)
+        if (col_ok[u]) dbuf[cb + u * NT + tid] = ddiv(acc[u], tot);
     }
     __syncthreads();
   }
