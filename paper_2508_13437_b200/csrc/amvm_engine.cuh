@@ -35,7 +35,10 @@ constexpr int kS = 32;         // one_opt screening rows (exact rejection test),
 constexpr int kCW = 16;        // one_opt window: columns per warp (window = NW * kCW)
 constexpr int kB = 8;          // one_opt second screen: flagged columns per batch
 constexpr int kG = 8;          // filter rows staged in smem per find_candidates
-constexpr int kTJ = 2 * AMVM_NT;  // find_candidates j-tile (level-sorted positions)
+#ifndef AMVM_TJ
+#define AMVM_TJ (2 * AMVM_NT)
+#endif
+constexpr int kTJ = AMVM_TJ;  // find_candidates j-tile (level-sorted positions)
 constexpr int kRowPasses = 8;  // queue rows drained from an smem-gathered row
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
@@ -70,6 +73,14 @@ __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
 struct Cand {
   int32_t i, j;
   double d;
+};
+
+// find_candidates survivor-queue entry: the pair and its two level indices
+// (delta = lv[ki] - lv[kj] is recomputed bit-identically from smem).
+struct __align__(16) QEnt {
+  int32_t i, j;
+  uint16_t ki, kj;
+  uint32_t pad;
 };
 
 // The kernel's dynamic shared memory.  Engine pointers into it are derived
@@ -182,7 +193,7 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   L.rsgn = o; o = al256(o + 4 * L.kk);
   L.ag = o; o = al256(o + 8 * kG * n);
   L.cbuf = o; o = al256(o + sizeof(Cand) * cap);
-  L.que = o; o = al256(o + 2 * sizeof(Cand) * fc_qcap(cap));  // staged-row survivors, ping-pong
+  L.que = o; o = al256(o + 2 * sizeof(QEnt) * fc_qcap(cap));  // staged-row survivors, ping-pong
   L.hset = o; o = al256(o + 8 * L.hsz);
   L.rem = o; o = al256(o + 4 * rr);
   L.sav = o; o = al256(o + 4 * rr);
@@ -213,7 +224,8 @@ struct Ctx {
   int32_t *rows, *rsgn;
   double *reps, *ag;
   uint32_t off_lv, off_scr;
-  Cand *cbuf, *que;
+  Cand *cbuf;
+  QEnt *que;
   uint64_t *hset;
   int32_t *rem, *sav, *pick, *coin, *ibuf;
   unsigned char *srt;
@@ -251,7 +263,7 @@ struct Ctx {
   [[maybe_unused]] double *const ag = sh->c.ag;                                           \
   [[maybe_unused]] unsigned char *const scr = amvm_dyn_smem + sh->c.off_scr;               \
   [[maybe_unused]] Cand *const cbuf = sh->c.cbuf;                                         \
-  [[maybe_unused]] Cand *const que = sh->c.que;                                           \
+  [[maybe_unused]] QEnt *const que = sh->c.que;                                           \
   [[maybe_unused]] uint64_t *const hset = sh->c.hset;                                     \
   [[maybe_unused]] int32_t *const rem = sh->c.rem;                                        \
   [[maybe_unused]] int32_t *const sav = sh->c.sav;                                        \
@@ -800,48 +812,74 @@ struct Engine {
   // finish row by row in fc_rest.
   __device__ void fc_drain(int nr, int g, bool counting) {
     AMVM_LOCALS
+    constexpr int U = 4;  // queue entries per thread in flight
     const int qcap = (int)fc_qcap(cap);
     int qn = sh->qcount < qcap ? sh->qcount : qcap;
     const int np = nr - g < kRowPasses ? nr - g : kRowPasses;
+    // per-pass bound table eps_q / delta(ki, kj) in the (now idle) staged-tile
+    // scratch (bucket bounds and the staged-row table stay intact for any
+    // later pass of the overflow path)
+    const int ll = (int)(nlev * nlev);
+    const bool tab2 = ll <= kG * kTJ;
+    double *bt2 = (double *)(scr + fc_tb_off(nlev));
     if (tid == 0) sh->qnext = 0;
     __syncthreads();
-    Cand *src = que, *dst = que + qcap;
+    QEnt *src = que, *dst = que + qcap;
     int q = g;
     int base = 0;  // sh->qnext only grows: pass survivors land at [base, qnext)
     for (; q < g + np && qn > 0; ++q) {
       const double *row = Ar + (int64_t)rows[q] * n;
       const double eq = reps[q];
       const bool pos = rsgn[q] != 0;
-      for (int e0 = warp * 32; e0 < qn; e0 += NT) {
-        const int e = e0 + lane;
-        Cand c{0, 0, 1.0};
-        bool alive = false;
-        if (e < qn) {
-          c = src[e];
-          const double da = dsub(__ldg(row + c.j), __ldg(row + c.i));
-          const double bq = ddiv(eq, c.d);
-          alive = pos ? (da < bq) : (da > -bq);
+      if (tab2) {
+        for (int e = tid; e < ll; e += NT) {
+          const int ki = e / (int)nlev, kj = e - ki * (int)nlev;
+          bt2[e] = ki > kj ? ddiv(eq, dsub(lv[ki], lv[kj])) : 0.0;
         }
-        const unsigned bal = __ballot_sync(AMVM_FULL, alive);
-        if (!bal) continue;
-        int bse = 0;
-        if (lane == 0) bse = atomicAdd(&sh->qnext, __popc(bal));
-        bse = __shfl_sync(AMVM_FULL, bse, 0) - base;
-        if (alive) dst[bse + __popc(bal & ((1u << lane) - 1u))] = c;
+        __syncthreads();
+      }
+      for (int e0 = warp * 32; e0 < qn; e0 += NT * U) {
+        QEnt c[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * NT + lane;
+          ok[u] = e < qn;
+          c[u] = ok[u] ? src[e] : QEnt{0, 0, 1, 0, 0u};
+        }
+        double aj[U], ai[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          aj[u] = __ldg(row + c[u].j);
+          ai[u] = __ldg(row + c[u].i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double bq = tab2 ? bt2[c[u].ki * (int)nlev + c[u].kj] : ddiv(eq, dsub(lv[c[u].ki], lv[c[u].kj]));
+          const double da = dsub(aj[u], ai[u]);
+          const bool alive = ok[u] && (pos ? (da < bq) : (da > -bq));
+          const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+          if (!bal) continue;
+          int bse = 0;
+          if (lane == 0) bse = atomicAdd(&sh->qnext, __popc(bal));
+          bse = __shfl_sync(AMVM_FULL, bse, 0) - base;
+          if (alive) dst[bse + __popc(bal & ((1u << lane) - 1u))] = c[u];
+        }
       }
       __syncthreads();
       const int tot = sh->qnext;
-      __syncthreads();  // everyone has read it before the next pass adds to it
+      __syncthreads();  // everyone has read it (and the table) before the next pass
       qn = tot - base;
       base = tot;
-      Cand *t = src; src = dst; dst = t;
+      QEnt *t = src; src = dst; dst = t;
     }
 #ifdef AMVM_FC_STATS
     if (tid == 0) sh->c.pc[12] += qn;
 #endif
     for (int e = tid; e < qn; e += NT) {
-      const Cand c = src[e];
-      if (fc_rest(c.i, c.j, c.d, nr, q)) fc_append(c.i, c.j, c.d, counting);
+      const QEnt c = src[e];
+      const double delta = dsub(lv[c.ki], lv[c.kj]);
+      if (fc_rest(c.i, c.j, delta, nr, q)) fc_append(c.i, c.j, delta, counting);
     }
     __syncthreads();
     if (tid == 0) sh->qcount = 0;
@@ -963,7 +1001,7 @@ struct Engine {
               bse = __shfl_sync(AMVM_FULL, bse, 0);
               if (alive) {
                 const int qp = bse + __popc(bal & ((1u << lane) - 1u));
-                if (qp < qcap) que[qp] = Cand{i, tj[e], delta};
+                if (qp < qcap) que[qp] = QEnt{i, tj[e], (uint16_t)ki, (uint16_t)kj, 0u};
                 else if (fc_rest(i, tj[e], delta, nr, g)) fc_append(i, tj[e], delta, counting);
               }
             }
@@ -1031,7 +1069,7 @@ struct Engine {
                 if (nr <= g) {
                   if (pos < cap) cbuf[pos] = Cand{i, j, delta};
                 } else if (pos < qcap) {
-                  que[pos] = Cand{i, j, delta};
+                  que[pos] = QEnt{i, j, (uint16_t)ki, (uint16_t)kj, 0u};
                 } else if (fc_rest(i, j, delta, nr, g)) {
                   fc_append(i, j, delta, counting);
                 }
@@ -1860,7 +1898,7 @@ struct Engine {
       c.rsgn = (int32_t *)(base + L.rsgn);
       c.ag = (double *)(base + L.ag);
       c.cbuf = (Cand *)(base + L.cbuf);
-      c.que = (Cand *)(base + L.que);
+      c.que = (QEnt *)(base + L.que);
       c.hset = (uint64_t *)(base + L.hset);
       c.rem = (int32_t *)(base + L.rem);
       c.sav = (int32_t *)(base + L.sav);
