@@ -39,7 +39,10 @@ constexpr int kG = 8;          // filter rows staged in smem per find_candidates
 #define AMVM_TJ (2 * AMVM_NT)
 #endif
 constexpr int kTJ = AMVM_TJ;  // find_candidates j-tile (level-sorted positions)
-constexpr int kRowPasses = 8;  // queue rows drained from an smem-gathered row
+#ifndef AMVM_ROW_PASSES
+#define AMVM_ROW_PASSES 24
+#endif
+constexpr int kRowPasses = AMVM_ROW_PASSES;  // queue passes (one filter row each) before fc_rest
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
