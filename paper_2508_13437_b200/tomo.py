@@ -1,0 +1,114 @@
+"""Discrete-tomography front end (C3 family).
+
+Host-side instance construction for the tomography configs, restating the
+reference builder's arithmetic so the projection matrix is bit-identical to
+``dmmv.parallel_beam_matrix`` (builders.py:186-239) on the same numpy:
+
+* the image is the square [-side/2, side/2]^2 of unit pixels; ray k of angle
+  theta starts at offset o_k * (cos, sin) and runs along (-sin, cos);
+* a ray's pixel weights are the lengths between consecutive sorted, distinct
+  crossing parameters (the box entry/exit and every grid line strictly in
+  between), each attributed to the pixel containing its midpoint;
+* rows are ordered (angle, detector), columns row-major pixels.
+
+Everything here is numpy on the host: it builds A once per instance family
+(A is then shared by every slice of a batch).  The ALNS path itself runs on
+the GPU through ``solve`` / ``solve_from``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+_EPS = 1e-12  # builders.py:195 — degenerate-direction and zero-length cut-off
+
+
+def phantom(kind: str, side: int) -> np.ndarray:
+    """Integer label image (builders.py:158-183 semantics)."""
+    if side < 1:
+        raise ValueError("side must be at least 1")
+    if kind == "squares":
+        img = np.zeros((side, side), dtype=np.int64)
+        outer, inner = max(1, side // 8), max(2, (3 * side) // 8)
+        for margin, label in ((outer, 1), (inner, 2)):
+            if side > 2 * margin:
+                img[margin:side - margin, margin:side - margin] = label
+        return img
+    if kind == "disk":
+        c = (side - 1) / 2.0
+        r, q = np.mgrid[0:side, 0:side]
+        return ((r - c) ** 2 + (q - c) ** 2 <= (0.35 * side) ** 2).astype(np.int64)
+    if kind == "checker":
+        blk = max(1, side // 8)
+        r, q = np.mgrid[0:side, 0:side]
+        return ((r // blk + q // blk) % 2).astype(np.int64)
+    raise ValueError(f"unknown phantom kind {kind!r}; pick disk, squares, or checker")
+
+
+def _segments(side: int, origin, direction):
+    """(pixel indices, lengths) of the ray origin + tau * direction."""
+    half = side / 2.0
+    enter, leave = -np.inf, np.inf
+    steep = []  # axes the ray is not parallel to
+    for ax in (0, 1):
+        d, p = direction[ax], origin[ax]
+        if abs(d) > _EPS:
+            a, b = (-half - p) / d, (half - p) / d
+            enter, leave = max(enter, min(a, b)), min(leave, max(a, b))
+            steep.append(ax)
+        elif not -half <= p <= half:
+            return None
+    if leave <= enter:
+        return None
+    parts = [np.array([enter, leave])]
+    grid = -half + np.arange(side + 1)
+    for ax in steep:
+        cross = (grid - origin[ax]) / direction[ax]
+        parts.append(cross[(cross > enter) & (cross < leave)])
+    tau = np.unique(np.concatenate(parts))
+    seg = np.diff(tau)
+    mid = tau[:-1] + seg / 2
+    col = np.clip(np.floor(origin[0] + mid * direction[0] + half).astype(np.intp), 0, side - 1)
+    row = np.clip(np.floor(half - (origin[1] + mid * direction[1])).astype(np.intp), 0, side - 1)
+    use = seg > _EPS
+    return row[use] * side + col[use], seg[use]
+
+
+def projection_csr(side: int, n_angles: int):
+    """Parallel-beam projector as CSR (indptr, indices, values); rows =
+    (angle, detector), one detector per image column at unit spacing."""
+    thetas = np.arange(n_angles) * np.pi / n_angles
+    offs = np.arange(side) - (side - 1) / 2.0
+    indptr, idx, val = [0], [], []
+    for th in thetas:
+        c, s = np.cos(th), np.sin(th)
+        for o in offs:
+            hit = _segments(side, (o * c, o * s), (-s, c))
+            if hit is not None and hit[0].size:
+                # a convex cell is crossed once; keep builders.py's add.at
+                # semantics anyway (duplicates summed in order)
+                pix, w = hit
+                if np.unique(pix).size != pix.size:
+                    acc = {}
+                    for p_, w_ in zip(pix.tolist(), w.tolist()):
+                        acc[p_] = acc.get(p_, 0.0) + w_
+                    pix = np.array(sorted(acc), dtype=np.intp)
+                    w = np.array([acc[p_] for p_ in pix.tolist()])
+                order = np.argsort(pix, kind="stable")
+                idx.append(pix[order]); val.append(w[order])
+                indptr.append(indptr[-1] + pix.size)
+            else:
+                indptr.append(indptr[-1])
+    idx = np.concatenate(idx) if idx else np.zeros(0, np.intp)
+    val = np.concatenate(val) if val else np.zeros(0)
+    return np.asarray(indptr, dtype=np.int64), idx.astype(np.int64), val
+
+
+def projection_matrix(side: int, n_angles: int) -> np.ndarray:
+    """Dense projector (n_angles*side x side^2), bit-identical to the
+    reference's ``parallel_beam_matrix(side, arange(n)*pi/n)``."""
+    indptr, idx, val = projection_csr(side, n_angles)
+    A = np.zeros((n_angles * side, side * side))
+    for r in range(A.shape[0]):
+        A[r, idx[indptr[r]:indptr[r + 1]]] = val[indptr[r]:indptr[r + 1]]
+    return A

@@ -163,10 +163,29 @@ def c3_scaled() -> None:
     save("solve_c3s", [rec])
 
 
+def c3_medium() -> None:
+    """Tomography at 128^2 x 64 angles (8192 x 16384: 48 s per
+    reference iteration).  A is NOT stored: the package's own projector
+    (paper_2508_13437_b200.tomo) regenerates it bit-identically (sha checked)."""
+    side, n_angles = 128, 64
+    A = dmmv.parallel_beam_matrix(side, np.arange(n_angles) * np.pi / n_angles)
+    eta = 0.05 * float(A.sum(axis=1).max())
+    spec = dmmv.TomoSpec(side=side, gray_levels=(0.0, 1.0, 2.0), n_angles=n_angles, noise=eta,
+                         phantom="squares", sirt_iters=100, seed=0)
+    inst, _ = dmmv.build_tomo(spec)
+    rec = solve_record(inst, dmmv.SolverConfig(max_iters=3, seed=0), store_A=False)
+    rec.pop("continuous_init", None)
+    rec["A_recipe"] = np.array([side, n_angles])
+    save("solve_c3m", [rec])
+
+
 def main() -> None:
     assert os.environ.get("OPENBLAS_NUM_THREADS") == "1"
     if "--c3s" in sys.argv:
         c3_scaled()
+        return
+    if "--c3m" in sys.argv:
+        c3_medium()
         return
     save("components", component_cases())
     save("small_solves", small_solves())

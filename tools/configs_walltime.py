@@ -20,15 +20,19 @@ from tests.golden_io import cfg_kwargs, load, named_A, stored_A  # noqa: E402
 
 # reference CPU seconds per iteration, 1 core, dev container
 REF_S_PER_IT = {"c1": 16.79 / 1000, "c1x": 18.14 / 1000, "c2": 0.110, "c4row": 0.1855, "c5row": 4.12,
-                "c3s": 6.0}  # c3s: measured here, 4 it in ~24 s (make_golden --c3s)
+                "c3s": 6.0, "c3m": 48.1}  # c3s: measured here, 4 it in ~24 s (make_golden --c3s)
 
 
 def main():
     import torch
     out = []
-    for name in ["c1", "c1x", "c2", "c4row", "c5row", "c3s"]:
+    from paper_2508_13437_b200 import tomo
+    for name in ["c1", "c1x", "c2", "c4row", "c5row", "c3s", "c3m"]:
         rec = load(f"solve_{name}")[0]
-        A = stored_A(rec) if name == "c3s" else named_A(name, rec)
+        if name == "c3m":
+            A = tomo.projection_matrix(*(int(v) for v in rec["A_recipe"]))
+        else:
+            A = stored_A(rec) if name == "c3s" else named_A(name, rec)
         if A is None:
             out.append({"config": name, "skipped": "matrix not reproducible on this host"})
             continue
