@@ -84,6 +84,67 @@ __global__ void k_transpose(const double *__restrict__ At, double *__restrict__ 
   }
 }
 
+// CSC build: one warp per column.  count -> exclusive scan (one CTA) ->
+// fill in row order (ballot compaction keeps rows ascending).
+__global__ void k_csc_count(const double *__restrict__ At, int64_t m, int64_t n, int64_t *__restrict__ cnt) {
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const double *col = At + j * m;
+  int64_t c = 0;
+  for (int64_t i = lane; i < m; i += 32) c += col[i] != 0.0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(AMVM_FULL, c, o);
+  if (lane == 0) cnt[j + 1] = c;
+}
+
+__global__ void k_csc_scan(int64_t *ptr, int64_t n, int64_t cap, WsHeader *hdr) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  // each thread scans a contiguous chunk, then the chunk totals
+  const int64_t per = (n + 1023) / 1024, lo = 1 + t * per, hi = lo + per < n + 1 ? lo + per : n + 1;
+  int64_t s = 0;
+  for (int64_t k = lo; k < hi; ++k) s += ptr[k];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int k = 0; k < 1024; ++k) {
+      const int64_t v = part[k];
+      part[k] = acc;
+      acc += v;
+    }
+    ptr[0] = 0;
+    hdr->csc_ok = acc <= cap;
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int64_t k = lo; k < hi; ++k) {
+    acc += ptr[k];
+    ptr[k] = acc;
+  }
+}
+
+__global__ void k_csc_fill(const double *__restrict__ At, int64_t m, int64_t n, const int64_t *__restrict__ ptr,
+                           int32_t *__restrict__ row, double *__restrict__ val, const WsHeader *hdr) {
+  if (!hdr->csc_ok) return;
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const double *col = At + j * m;
+  int64_t pos = ptr[j];
+  for (int64_t i0 = 0; i0 < m; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const double v = i < m ? col[i] : 0.0;
+    const unsigned bal = __ballot_sync(AMVM_FULL, v != 0.0);
+    if (v != 0.0) {
+      const int64_t q = pos + __popc(bal & ((1u << lane) - 1u));
+      row[q] = (int32_t)i;
+      val[q] = v;
+    }
+    pos += __popc(bal);
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_op(KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -434,8 +495,8 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   // iterations so instances migrate between CTAs and the tail is one chunk
   P->chunk_iters = (!op && p->count > P->slots && prm->max_iters > kChunkIters) ? kChunkIters : 0;
   P->ist_bytes = P->chunk_iters ? inst_layout(p->m, p->n).total : 0;
-  P->ws_bytes = sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + (size_t)P->slots * P->slot_bytes +
-                (size_t)p->count * P->ist_bytes;
+  P->ws_bytes = sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
+                (size_t)P->slots * P->slot_bytes + (size_t)p->count * P->ist_bytes;
   return AMVM_OK;
 }
 
@@ -452,7 +513,15 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
   a.chunk_iters = P.chunk_iters;
   a.ist_bytes = P.ist_bytes;
   a.Ar = (const double *)(a.ws + sizeof(WsHeader));
-  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + (size_t)P.slots * P.slot_bytes
+  {
+    unsigned char *cb = a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n);
+    const CscLayout CL = csc_layout(p->m, p->n);
+    a.cptr = (const int64_t *)(cb + CL.ptr);
+    a.crow = (const int32_t *)(cb + CL.row);
+    a.cval = (const double *)(cb + CL.val);
+  }
+  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
+                            (size_t)P.slots * P.slot_bytes
                       : nullptr;
   a.cr_smem = P.cr_smem; a.tab = P.tab; a.cap = P.cap;
   a.time_budget_ns = prm->time_limit_s < 0 ? -1 : (int64_t)(prm->time_limit_s * 1e9);
@@ -472,6 +541,13 @@ int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
   {  // row-major copy of A for the row gathers (filter rows, screening rows)
     const dim3 tg((unsigned)((a.n + 31) / 32), (unsigned)((a.m + 31) / 32)), tb(32, 8);
     k_transpose<<<tg, tb, 0, st>>>(a.At, (double *)a.Ar, a.m, a.n);
+  }
+  {  // CSC copy for sparse A (sets the header's csc_ok when it fits)
+    int64_t *cptr = (int64_t *)a.cptr;
+    const unsigned cg = (unsigned)((a.n + 7) / 8);
+    k_csc_count<<<cg, 256, 0, st>>>(a.At, a.m, a.n, cptr);
+    k_csc_scan<<<1, 1024, 0, st>>>(cptr, a.n, csc_cap(a.m, a.n), (WsHeader *)a.ws);
+    k_csc_fill<<<cg, 256, 0, st>>>(a.At, a.m, a.n, cptr, (int32_t *)a.crow, (double *)a.cval, (WsHeader *)a.ws);
   }
   const dim3 grid((unsigned)P.slots), block((unsigned)P.nt);
   if (op) k_op<AMVM_NT><<<grid, block, P.smem, st>>>(a);

@@ -96,6 +96,9 @@ struct KArgs {
   int64_t m, n, nlev, count;
   const double *At, *B, *levels;
   const double *Ar;  // row-major copy of A (m x n), built in the workspace
+  const int64_t *cptr;  // CSC copy of A (valid when the header's csc_ok is set)
+  const int32_t *crow;
+  const double *cval;
   amvm_params prm;
   // start solution (solve) or in/out solution (component ops)
   int32_t *s_idx;
@@ -124,7 +127,8 @@ struct WsHeader {  // 256 bytes
   int32_t status;
   int32_t next;
   unsigned long long next_task;  // chunked solve: (chunk, instance) tasks handed out
-  int32_t pad[60];
+  int32_t csc_ok;                // the workspace CSC copy of A is complete (sparse A)
+  int32_t pad[59];
 };
 
 // A parked instance between chunks of a chunked solve (the persistent part
@@ -142,6 +146,22 @@ struct InstState {
 
 // Workspace: [WsHeader | Ar (row-major copy of A) | slots | parked instances]
 __host__ __device__ inline size_t ws_ar_bytes(int64_t m, int64_t n) { return ((size_t)8 * m * n + 255) & ~(size_t)255; }
+
+// CSC copy of A for sparse instances (tomography): built by every launch,
+// used when nnz <= csc_cap (density <= 1/8), else the dense paths run.
+__host__ __device__ inline int64_t csc_cap(int64_t m, int64_t n) { return (m * n) / 8; }
+struct CscLayout {
+  size_t ptr, row, val, total;
+};
+__host__ __device__ inline CscLayout csc_layout(int64_t m, int64_t n) {
+  CscLayout L;
+  const int64_t cap = csc_cap(m, n);
+  L.ptr = 0;
+  L.row = (((size_t)8 * (n + 1)) + 255) & ~(size_t)255;
+  L.val = L.row + ((((size_t)4 * cap) + 255) & ~(size_t)255);
+  L.total = L.val + ((((size_t)8 * cap) + 255) & ~(size_t)255);
+  return L;
+}
 
 struct InstLayout {
   size_t r, idx, total;
@@ -218,6 +238,10 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
 struct Ctx {
   int64_t m, n, nlev, kk, cap;
   const double *At, *Ar, *b;
+  const int64_t *cptr;
+  const int32_t *crow;
+  const double *cval;
+  int csc;
   double *cr, *ur;
   int32_t *cidx, *uidx;
   double *dbuf, *pbuf, *cbk;
@@ -1409,6 +1433,10 @@ struct Engine {
     const double t = cobj;
     const double tot = block_pairwise([&](int64_t k) { return fabs(cr[k]); }, m, lf_lo, lf_len, nleaf_m);
     const double na = -alpha;
+    if (sh->c.csc) {
+      impact_csc(na, t, tot);
+      return;
+    }
     if (n >= kIC4 * NT) {
       impact_stream<kIC4, kIR4, kIS4>(na, t, tot);
       return;
@@ -1457,6 +1485,34 @@ struct Engine {
       }
       if (tid < cols) dbuf[cb + tid] = ddiv(acc, tot);
       __syncthreads();
+    }
+    __syncthreads();
+  }
+
+  // Sparse A (CSC copy present): thread per column over its nonzeros in row
+  // order.  The dense sum adds an exact +0 for every zero entry (terms are
+  // >= +0, so the partial sum never is -0), hence skipping them is bitwise
+  // the same sum; per nonzero the operations are those of the dense paths.
+  __device__ void impact_csc(double na, double t, double tot) {
+    AMVM_LOCALS
+    const int64_t *cp = sh->c.cptr;
+    const int32_t *cr_ = sh->c.crow;
+    const double *cv = sh->c.cval;
+    for (int64_t j = tid; j < n; j += NT) {
+      double acc = 0.0;
+      const int64_t e1 = cp[j + 1];
+      for (int64_t e = cp[j]; e < e1; ++e) {
+        const int32_t k = __ldg(cr_ + e);
+        const double a = fabs(__ldg(cv + e));
+        const double sv = fabs(cr[k]);
+        const double w = dmul(na, dsub(t, sv));
+        double y;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+        y = dfma(y, dfma(-a, y, 1.0), y);
+        y = dfma(y, dfma(-a, y, 1.0), y);
+        acc = dadd(acc, dmul(sv, exp_nonpos(dmul(w, y))));
+      }
+      dbuf[j] = ddiv(acc, tot);
     }
     __syncthreads();
   }
@@ -1880,12 +1936,17 @@ struct Engine {
       c.nlev = a.nlev;
       c.At = a.At;
       c.Ar = a.Ar;
+      c.cptr = a.cptr;
+      c.crow = a.crow;
+      c.cval = a.cval;
+      c.csc = ((const WsHeader *)a.ws)->csc_ok;
       c.prm = a.prm;
       c.cap = a.cap;
       c.tab = a.tab;
       const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap);
       c.kk = L.kk;
-      unsigned char *base = a.ws + sizeof(WsHeader) + ws_ar_bytes(a.m, a.n) + (size_t)slot * a.slot_bytes;
+      unsigned char *base = a.ws + sizeof(WsHeader) + ws_ar_bytes(a.m, a.n) + csc_layout(a.m, a.n).total +
+                            (size_t)slot * a.slot_bytes;
       c.status = (int32_t *)a.ws;
       c.ur = (double *)(base + L.ur);
       c.uidx = (int32_t *)(base + L.uidx);
