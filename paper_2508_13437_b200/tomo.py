@@ -112,3 +112,57 @@ def projection_matrix(side: int, n_angles: int) -> np.ndarray:
     for r in range(A.shape[0]):
         A[r, idx[indptr[r]:indptr[r + 1]]] = val[indptr[r]:indptr[r + 1]]
     return A
+
+
+class SliceBatch:
+    """Several tomography slices sharing one projector A as ONE device batch
+    (slices shard like PTQ rows).  Slice k is the instance
+    (A, B[k], levels) started from idx0[k] with seed seeds[k]; each slice's
+    result equals ``solve_from`` on it alone (bitwise).
+
+    ``solve`` returns the same device-tensor dict as ``ptq.LayerBatch.solve``.
+    """
+
+    def __init__(self, A, B, levels, idx0, device=None):
+        from . import _native as N
+        from .ptq import LayerBatch
+
+        torch = N.torch_cuda()
+        dev_in = isinstance(A, torch.Tensor)  # a device A (m x n, float64) is used in place
+        if not dev_in:
+            A = np.ascontiguousarray(A, dtype=np.float64)
+        B = np.ascontiguousarray(np.atleast_2d(B), dtype=np.float64)
+        idx0 = np.ascontiguousarray(np.atleast_2d(idx0), dtype=np.int32)
+        levels = np.asarray(levels, dtype=np.float64)
+        m, n = (int(v) for v in A.shape)
+        if B.shape[1] != m or idx0.shape != (B.shape[0], n):
+            raise ValueError("B must be slices x m and idx0 slices x n")
+        if levels.ndim != 1 or np.any(np.diff(levels) <= 0) or not np.all(np.isfinite(levels)):
+            raise ValueError("levels must be strictly increasing and finite")
+        if idx0.min() < 0 or idx0.max() >= levels.size:
+            raise ValueError("idx0 outside the level set")
+        self._lb = lb = LayerBatch.__new__(LayerBatch)
+        lb.torch, lb.lib = torch, N.load_library()
+        lb.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        dev = lb.device
+        lb.m, lb.n, lb.count, lb.nlev = m, n, B.shape[0], levels.size
+        lb.rows = np.arange(lb.count)
+        lb.At = (A.to(dev, torch.float64) if dev_in else torch.from_numpy(A).to(dev)).t().contiguous()
+        lb.B = torch.from_numpy(B).to(dev)
+        lb.L = torch.from_numpy(np.tile(levels, (lb.count, 1))).to(dev)
+        lb.idx0 = torch.from_numpy(idx0).to(dev)
+        lb.r0 = torch.empty((lb.count, m), dtype=torch.float64, device=dev)
+        lb.obj0 = torch.empty(lb.count, dtype=torch.float64, device=dev)
+        lb.cnt0 = torch.empty(lb.count, dtype=torch.int32, device=dev)
+        prob = lb.problem()
+        sol = N.SolutionPtrs(lb.idx0.data_ptr(), lb.r0.data_ptr(), lb.obj0.data_ptr(), lb.cnt0.data_ptr())
+        # start residuals in numpy's BLAS order (core.py:183-197), on the device
+        N.check(lb.lib.amvm_compute_residual(N.C.byref(prob), N.C.byref(sol), N.stream_handle()),
+                "amvm_compute_residual")
+        lb.prepared = True
+
+    def solve(self, cfg=None, seeds=None, trace: bool = False) -> dict:
+        return self._lb.solve(cfg, seeds=seeds, trace=trace)
+
+    def check_status(self) -> None:
+        self._lb.check_status()
