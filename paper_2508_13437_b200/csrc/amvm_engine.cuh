@@ -323,6 +323,7 @@ struct Shared {
   uint64_t skey[NT];
   int sidx[NT];
   int64_t task_inst, task_chunk;  // k_solve: the task being run (kept out of registers)
+  int nfilter_rows, srt_rows_sorted;  // select_rows result (rows[] count, ordered by |s| desc)
   int task_live, task_skip;
   Pcg rng;
   Ctx c;
@@ -765,6 +766,10 @@ struct Engine {
       const double s = cr[rows[q]];
       reps[q] = dsub(cobj, fabs(s));
       rsgn[q] = s > 0.0;
+    }
+    if (tid == 0) {
+      sh->nfilter_rows = cnt;
+      sh->srt_rows_sorted = cnt <= 2048;
     }
     __syncthreads();
     return cnt;
@@ -1349,18 +1354,23 @@ struct Engine {
     double wt = 0.0, wd = 0.0;
     int wi = -1, wj = -1;
     const double t0 = cobj;
+    // sparse A: rows[] holds the filter rows by (|s| desc, index asc)
+    const int nrows = sh->c.csc && sh->srt_rows_sorted ? sh->nfilter_rows : 0;
     for (int c = warp; c < cnt; c += NW) {
       const Cand e = cbuf[c];
-      const double *ci = At + (int64_t)e.i * m;
-      const double *cj = At + (int64_t)e.j * m;
       double mx = 0.0;
-      int it = 0;
-      for (int64_t r = lane; r < m; r += 32) {
-        const double y = dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r))));
-        mx = fmax(mx, fabs(y));
-        if ((++it & 15) == 0 && __any_sync(AMVM_FULL, mx >= t0)) break;
+      if (!(nrows > 0 && swap_tprime_sparse(e.i, e.j, e.d, nrows, mx))) {
+        const double *ci = At + (int64_t)e.i * m;
+        const double *cj = At + (int64_t)e.j * m;
+        mx = 0.0;
+        int it = 0;
+        for (int64_t r = lane; r < m; r += 32) {
+          const double y = dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r))));
+          mx = fmax(mx, fabs(y));
+          if ((++it & 15) == 0 && __any_sync(AMVM_FULL, mx >= t0)) break;
+        }
+        mx = warp_max(mx);
       }
-      mx = warp_max(mx);
       if (mx < t0 && (wi < 0 || mx < wt || (mx == wt && (e.i < wi || (e.i == wi && e.j < wj))))) {
         wt = mx; wi = e.i; wj = e.j; wd = e.d;
       }
@@ -1386,6 +1396,42 @@ struct Engine {
     }
     __syncthreads();
     return found;
+  }
+
+  // t' = max_r |s_r + d (a_rj - a_ri)| for sparse A (warp-wide), exactly the
+  // dense evaluation's value: rows outside nz(i) U nz(j) contribute |s_r|
+  // (s + d*0 = s), so t' = max(touched rows, the largest-|s| untouched row).
+  // The latter is the first row of rows[] (|s| descending) touched by
+  // neither column; if every filter row is touched, returns false (the caller
+  // scans densely).
+  __device__ bool swap_tprime_sparse(int i, int j, double d, int nrows, double &out) {
+    AMVM_LOCALS
+    const int64_t *cp = sh->c.cptr;
+    const int32_t *crw = sh->c.crow;
+    const double *cv = sh->c.cval;
+    int u = -1;
+    for (int b0 = 0; b0 < nrows && u < 0; b0 += 32) {
+      const int q = b0 + lane;
+      bool free_row = false;
+      if (q < nrows) {
+        const int64_t r = rows[q];
+        free_row = __ldg(Ar + r * n + i) == 0.0 && __ldg(Ar + r * n + j) == 0.0;
+      }
+      const unsigned bal = __ballot_sync(AMVM_FULL, free_row);
+      if (bal) u = b0 + __ffs(bal) - 1;
+    }
+    if (u < 0) return false;
+    double mx = fabs(cr[rows[u]]);
+    for (int64_t e = cp[i] + lane; e < cp[i + 1]; e += 32) {  // rows touched by column i
+      const int64_t r = __ldg(crw + e);
+      mx = fmax(mx, fabs(dadd(cr[r], dmul(d, dsub(__ldg(Ar + r * n + j), __ldg(cv + e))))));
+    }
+    for (int64_t e = cp[j] + lane; e < cp[j + 1]; e += 32) {  // rows only column j touches
+      const int64_t r = __ldg(crw + e);
+      if (__ldg(Ar + r * n + i) == 0.0) mx = fmax(mx, fabs(dadd(cr[r], dmul(d, dsub(__ldg(cv + e), 0.0)))));
+    }
+    out = warp_max(mx);
+    return true;
   }
 
   // apply_swap, core.py:228-245, with the objective predicted by best_swap.
