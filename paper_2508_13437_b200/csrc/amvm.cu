@@ -455,7 +455,10 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   if (nt != AMVM_NT) return AMVM_ERR_UNSUPPORTED;  // this build instantiates one CTA size
   P->nt = nt;
   P->tab = p->nlev <= kTabMaxLev;
-  P->cr_smem = p->m * 8 <= 96 * 1024;
+#ifndef AMVM_CR_SMEM_MAX
+#define AMVM_CR_SMEM_MAX (96 * 1024)
+#endif
+  P->cr_smem = p->m * 8 <= AMVM_CR_SMEM_MAX;
   const int64_t n = p->n;
   const int64_t maxc = prm->max_candidates;
   // swap-candidate survivor buffer: batches get room for 2x max_candidates

@@ -306,6 +306,7 @@ struct Shared {
   static constexpr int NW = NT / 32;
   double red[NW][4];  // best_swap per-warp winners
   double red2[2][NW];
+  int red2i[2][NW];
   double redS[NW];
   double bc_d[8];
   int bc_i[16];
@@ -437,28 +438,44 @@ struct Engine {
 
   // ------------------------------------------------------------- one_opt
   // Exact max_i |cr_i + d*col_i| for both candidates of one column (CTA-wide).
-  __device__ void exact_pair_max(const double *col, double dm, double dp, double &tm, double &tp) {
+  // Also returns a row attaining each maximum (the new objective's row if
+  // that shift is applied: it becomes a screening row, see one_opt).
+  __device__ void exact_pair_max(const double *col, double dm, double dp, double &tm, double &tp, int &im,
+                                 int &ip) {
     AMVM_LOCALS
     double mm = 0.0, mp = 0.0;
+    int jm = -1, jp = -1;
     for (int64_t i = tid; i < m; i += NT) {
       const double r = cr[i], a = __ldg(col + i);
-      mm = fmax(mm, fabs(dadd(r, dmul(dm, a))));
-      mp = fmax(mp, fabs(dadd(r, dmul(dp, a))));
+      const double ym = fabs(dadd(r, dmul(dm, a))), yp = fabs(dadd(r, dmul(dp, a)));
+      if (ym > mm || jm < 0) { mm = ym; jm = (int)i; }
+      if (yp > mp || jp < 0) { mp = yp; jp = (int)i; }
     }
-    mm = warp_max(mm);
-    mp = warp_max(mp);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double om = __shfl_xor_sync(AMVM_FULL, mm, o), op = __shfl_xor_sync(AMVM_FULL, mp, o);
+      const int oim = __shfl_xor_sync(AMVM_FULL, jm, o), oip = __shfl_xor_sync(AMVM_FULL, jp, o);
+      if (om > mm || (om == mm && (unsigned)oim < (unsigned)jm)) { mm = om; jm = oim; }
+      if (op > mp || (op == mp && (unsigned)oip < (unsigned)jp)) { mp = op; jp = oip; }
+    }
     if (lane == 0) {
       sh->red2[0][warp] = mm;
       sh->red2[1][warp] = mp;
+      sh->red2i[0][warp] = jm;
+      sh->red2i[1][warp] = jp;
     }
     __syncthreads();
-    tm = 0.0;
-    tp = 0.0;
+    tm = -1.0;
+    tp = -1.0;
+    im = ip = 0;
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
-      tm = fmax(tm, sh->red2[0][k]);
-      tp = fmax(tp, sh->red2[1][k]);
+      const int km = sh->red2i[0][k], kp = sh->red2i[1][k];
+      if (km >= 0 && sh->red2[0][k] > tm) { tm = sh->red2[0][k]; im = km; }
+      if (kp >= 0 && sh->red2[1][k] > tp) { tp = sh->red2[1][k]; ip = kp; }
     }
+    if (tm < 0.0) tm = 0.0;
+    if (tp < 0.0) tp = 0.0;
     __syncthreads();
   }
 
@@ -512,15 +529,15 @@ struct Engine {
     constexpr int WS = NW * kCW;
     __syncthreads();
     select_screen();
-    const int srow_l = sh->srow[lane];
-    const double *arow = Ar + (int64_t)srow_l * n;  // this lane's screening row
     int wpar = 0, bpar = 0;
     for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
       bool changed = false;
       int64_t p = 0;
       while (p < n) {
         const int wc = (int)(n - p < WS ? n - p : WS);
-        const double rs = cr[srow_l];  // current residual of this lane's screening row
+        const int srow_l = sh->srow[lane];  // this lane's screening row (row 0 follows the objective)
+        const double *arow = Ar + (int64_t)srow_l * n;
+        const double rs = cr[srow_l];
         const double t = cobj;
         const int c0 = warp * kCW;
         const int64_t jb = p + c0;
@@ -624,7 +641,8 @@ struct Engine {
 #ifndef AMVM_FC_STATS
             if (tid == 0) sh->c.pc[11] += 1;
 #endif
-            exact_pair_max(At + j * m, dm, dp, tm, tpv);
+            int rm, rp;
+            exact_pair_max(At + j * m, dm, dp, tm, tpv, rm, rp);
             int lvl = -1;
             double bt = cobj;
             if (k > 0 && tm < bt) { bt = tm; lvl = k - 1; }
@@ -638,7 +656,15 @@ struct Engine {
               const double *col = At + j * m;
               for (int64_t i = tid; i < m; i += NT) cr[i] = dadd(cr[i], dmul(d, __ldg(col + i)));
               __syncthreads();  // all reads of cidx[j] done; residual published
-              if (tid == 0) cidx[j] = lvl;
+              if (tid == 0) {
+                cidx[j] = lvl;
+                // the row attaining the new objective leads both screens from
+                // now on (any row set is an exact screen; the current maximum
+                // row is the one that rejects most)
+                const int top = lvl == k - 1 ? rm : rp;
+                sh->srow[0] = top;
+                sh->sidx[0] = top;
+              }
               bump_known(bt);
               __syncthreads();
               break;

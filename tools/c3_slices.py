@@ -67,4 +67,7 @@ print(json.dumps({
     "moves_scored_per_s": mv / (ms / 1e3),
     "initial_obj_mean": float(o["initial_objective"].mean()), "best_obj_mean": float(o["best_objective"].mean()),
     "phase_share": {k: round(float(v / pc[:8].sum()), 3) for k, v in zip(names, pc[:8])},
+    "events_per_slice": {k: round(float(v / S), 1) for k, v in zip(
+        ["fc_calls", "fc_survivors", "swaps", "oo_exact_scans", "oo_moves", "oo_windows", "impact_calls",
+         "refreshes"], pc[8:16])},
     "front_end_s": {"projector_csr": round(t1 - t0, 2), "device_build_sirt": round(t2 - t1, 2)}}))
