@@ -42,6 +42,7 @@ constexpr int kTJ = AMVM_TJ;  // find_candidates j-tile (level-sorted positions)
 #ifndef AMVM_ROW_PASSES
 #define AMVM_ROW_PASSES 24
 #endif
+constexpr int kDrainLong = 1024;  // queue length that keeps the batched passes going
 constexpr int kRowPasses = AMVM_ROW_PASSES;  // queue passes (one filter row each) before fc_rest
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
@@ -885,7 +886,9 @@ struct Engine {
     QEnt *src = que, *dst = que + qcap;
     int q = g;
     int base = 0;  // sh->qnext only grows: pass survivors land at [base, qnext)
-    for (; q < g + np && qn > 0; ++q) {
+    // kRowPasses passes, and more while the queue stays long (sparse rows
+    // keep most pairs alive; batched passes beat per-pair fc_rest there)
+    for (; q < nr && qn > 0 && (q < g + np || qn > kDrainLong); ++q) {
       const double *row = Ar + (int64_t)rows[q] * n;
       const double eq = reps[q];
       const bool pos = rsgn[q] != 0;
