@@ -190,6 +190,22 @@ AMVM_API int amvm_ptq_prepare(int64_t m, int64_t n, int64_t count, int64_t nlev,
                               const double *At, const double *W, double *B,
                               double *levels, int32_t *idx, void *stream);
 
+/* ---- exact oracle: replaces dmmv.oracle.brute_force (oracle.py:38-111) --
+ * Exhaustive enumeration of all nlev^n assignments of ONE instance
+ * (count == 1, n <= 64).  Result: the lexicographically smallest level-index
+ * vector attaining the minimum max|A x - b| (the reference's first-strict-
+ * improvement order), its objective, and its code (sum_j idx_j nlev^(n-1-j)).
+ * order 0 evaluates t as `assignments @ A.T - b` (oracle.py:62-64: numpy's
+ * dgemm, a sequential FMA chain over j), order 1 as the pruned DFS does
+ * (oracle.py:95-111: -b + levels[d_0]*A[:,0] + ..., unfused).  The budget
+ * check (BudgetExceededError) stays on the host.  best_idx (int32[n]),
+ * best_t (double[1]), best_code (int64[1], may be NULL) are device pointers;
+ * ws holds amvm_brute_force_workspace_bytes(prob) bytes.                  */
+AMVM_API size_t amvm_brute_force_workspace_bytes(const amvm_problem *prob);
+AMVM_API int amvm_brute_force(const amvm_problem *prob, int order, int32_t *best_idx,
+                              double *best_t, int64_t *best_code, void *ws,
+                              size_t ws_bytes, void *stream);
+
 /* HOST helper: numpy default_rng(seed).bit_generator.state for each seed
  * (SeedSequence -> PCG64), so per-instance seeds need no Python loop.      */
 AMVM_API int amvm_seed_pcg64(const uint64_t *seeds_host, int64_t count,

@@ -256,3 +256,36 @@ def pairwise_sum(a) -> float:
 def norm(x) -> float:
     x = np.ascontiguousarray(x, dtype=np.float64)
     return float(lib().orc_norm(_p(x), x.size))
+
+
+def brute_force(A, b, levels, prune: bool = False, chunk: int = 1 << 15):
+    """Exhaustive enumeration (dmmv.oracle.brute_force, oracle.py:38-111),
+    numpy restatement: codes in lexicographic order (oracle.py:58-60), the
+    first code attaining the minimum wins.  prune=False evaluates t as the
+    reference's `assignments @ A.T - b` (oracle.py:62-64); prune=True in the
+    pruned DFS's order, s = -b + levels[d_0] A[:,0] + ... unfused
+    (oracle.py:95-111) — without pruning, which does not change the optimum.
+    Returns (best_idx, best_t, enumerated = |V|^n)."""
+    A = np.asarray(A, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    levels = np.asarray(levels, dtype=np.float64)
+    m, n = A.shape
+    nlev = levels.size
+    total = nlev ** n
+    place = nlev ** np.arange(n - 1, -1, -1, dtype=np.int64)
+    best_t, best_idx = np.inf, None
+    for lo in range(0, total, chunk):
+        codes = np.arange(lo, min(lo + chunk, total), dtype=np.int64)
+        digits = (codes[:, None] // place) % nlev
+        X = levels[digits]
+        if not prune:
+            S = X @ A.T - b
+        else:
+            S = np.broadcast_to(-b, (codes.size, m)).copy()
+            for j in range(n):
+                S = S + X[:, j:j + 1] * A[:, j]
+        t_all = np.max(np.abs(S), axis=1)
+        k = int(np.argmin(t_all))
+        if t_all[k] < best_t:
+            best_t, best_idx = float(t_all[k]), digits[k].astype(np.intp)
+    return best_idx, best_t, total

@@ -36,6 +36,7 @@ from .controller import (  # noqa: F401
     solve,
     worst_remove_destroy,
 )
+from .exact import DEFAULT_BUDGET, BudgetExceededError, OracleResult, brute_force  # noqa: F401
 from .core import (  # noqa: F401
     REFRESH_PERIOD,
     Instance,
@@ -54,4 +55,5 @@ __all__ = [
     "SwapCandidate", "SolveReport", "SolverConfig", "TraceEntry", "best_swap", "find_candidates",
     "greedy_repair", "impact_scores", "initial_solution", "local_search", "one_opt",
     "random_destroy", "random_repair", "removal_count", "solve", "worst_remove_destroy",
+    "DEFAULT_BUDGET", "BudgetExceededError", "OracleResult", "brute_force",
 ]

@@ -22,7 +22,7 @@ EXPORTS = (
     "amvm_workspace_bytes", "amvm_solve", "amvm_one_opt", "amvm_local_search",
     "amvm_find_candidates", "amvm_best_swap", "amvm_impact_scores", "amvm_destroy",
     "amvm_repair", "amvm_compute_residual", "amvm_ptq_prepare", "amvm_seed_pcg64", "amvm_status",
-    "amvm_strerror", "amvm_abi_version",
+    "amvm_strerror", "amvm_abi_version", "amvm_brute_force_workspace_bytes", "amvm_brute_force",
 )
 
 
@@ -92,6 +92,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_ptq_prepare.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]
     lib.amvm_seed_pcg64.argtypes = [vp, i64, vp]
     lib.amvm_status.argtypes = [vp, vp]
+    lib.amvm_brute_force_workspace_bytes.restype = sz
+    lib.amvm_brute_force_workspace_bytes.argtypes = [vp]
+    lib.amvm_brute_force.argtypes = [vp, C.c_int, vp, vp, vp, vp, sz, vp]
     lib.amvm_strerror.restype = C.c_char_p
     lib.amvm_strerror.argtypes = [C.c_int]
     for name in EXPORTS:

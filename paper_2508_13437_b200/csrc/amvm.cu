@@ -10,6 +10,7 @@
 #include <cstring>
 
 #include "amvm_engine.cuh"
+#include "amvm_exact.cuh"
 
 using namespace amvm;
 
@@ -745,6 +746,67 @@ int amvm_seed_pcg64(const uint64_t *seeds_host, int64_t count, amvm_pcg64 *out_h
   if (!seeds_host || !out_host || count < 0) return AMVM_ERR_INVALID;
   for (int64_t k = 0; k < count; ++k) seed_pcg64(seeds_host[k], &out_host[k]);
   return AMVM_OK;
+}
+
+// ---- exact oracle: brute_force (oracle.py:38-111), see amvm_exact.cuh ----
+static int bf_shape(const amvm_problem *prob, long long *total, int *blocks) {
+  if (!prob || !prob->At || !prob->B || !prob->levels) return AMVM_ERR_INVALID;
+  if (prob->m < 1 || prob->n < 1 || prob->nlev < 1 || prob->count != 1) return AMVM_ERR_INVALID;
+  if (prob->n > kBFMaxN) return AMVM_ERR_UNSUPPORTED;
+  long long t = 1;
+  for (int64_t j = 0; j < prob->n; ++j) {
+    if (t > (long long)(0x3fffffffffffffffLL / prob->nlev)) return AMVM_ERR_UNSUPPORTED;
+    t *= prob->nlev;
+  }
+  *total = t;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long per = 256;
+  long long want = (t + per - 1) / per;
+  const long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM
+  *blocks = (int)std::max(1LL, std::min(want, cap));
+  return AMVM_OK;
+}
+
+size_t amvm_brute_force_workspace_bytes(const amvm_problem *prob) {
+  long long total;
+  int blocks;
+  if (bf_shape(prob, &total, &blocks)) return 0;
+  return 64 + (size_t)blocks * 16;
+}
+
+int amvm_brute_force(const amvm_problem *prob, int order, int32_t *best_idx, double *best_t, int64_t *best_code,
+                     void *ws, size_t ws_bytes, void *stream) {
+  if (!best_idx || !best_t || (order != 0 && order != 1)) return AMVM_ERR_INVALID;
+  long long total;
+  int blocks;
+  int rc = bf_shape(prob, &total, &blocks);
+  if (rc) return rc;
+  if (!ws || ws_bytes < 64 + (size_t)blocks * 16) return AMVM_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  char *w = (char *)ws;
+  unsigned long long *gbest = (unsigned long long *)w;
+  double *blk_t = (double *)(w + 64);
+  long long *blk_c = (long long *)(w + 64 + (size_t)blocks * 8);
+  const unsigned long long inf_bits = 0x7ff0000000000000ULL;
+  cudaError_t e = cudaMemcpyAsync(gbest, &inf_bits, sizeof(inf_bits), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  const int64_t m = prob->m, n = prob->n, nlev = prob->nlev;
+  size_t smem = sizeof(double) * (size_t)(nlev + m);
+  const size_t full = smem + sizeof(double) * (size_t)(m * n);
+  const size_t limit = 200 * 1024;
+  int staged = full <= limit;
+  if (staged) smem = full;
+  if (smem > limit) return AMVM_ERR_UNSUPPORTED;  // b + levels alone exceed shared memory
+  e = cudaFuncSetAttribute(k_brute_force<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  k_brute_force<256><<<blocks, 256, smem, st>>>(m, (int)n, (int)nlev, total, order, staged, prob->At, prob->B,
+                                                prob->levels, gbest, blk_t, blk_c);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  k_brute_force_final<256><<<1, 256, 0, st>>>(blocks, (int)n, (int)nlev, blk_t, blk_c, best_idx, best_t,
+                                               best_code);
+  return cuda_rc(cudaGetLastError());
 }
 
 }  // extern "C"
