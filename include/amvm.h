@@ -206,6 +206,34 @@ AMVM_API int amvm_brute_force(const amvm_problem *prob, int order, int32_t *best
                               double *best_t, int64_t *best_code, void *ws,
                               size_t ws_bytes, void *stream);
 
+/* ---- device warm start: initial_solution without continuous_init --------
+ * (controller.py:134-165): (A^T A + 1e-8 I) x = A^T b by Cholesky on the
+ * device, idx[j] = nearest level of x_j (ties to the lower level), x = 0 if
+ * the factorisation fails or x is not finite.  Agrees with the reference's
+ * LAPACK solve to rounding (not bitwise; the host path stays the default).
+ * count == 1.  idx (int32[n]), target (double[n], may be NULL) and flag
+ * (int32[1]: 0 ok, 1 factorisation failed, 2 not finite; both fall back to
+ * zeros as the reference does, with a warning on the host) are device
+ * pointers; ws holds amvm_ls_start_workspace_bytes(m, n) bytes.           */
+AMVM_API size_t amvm_ls_start_workspace_bytes(int64_t m, int64_t n);
+AMVM_API int amvm_ls_start(const amvm_problem *prob, int32_t *idx, double *target,
+                           int32_t *flag, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- tomography front end: replaces parallel_beam_matrix / _ray_weights --
+ * (builders.py:186-239) as a device CSR build, bit-identical to the
+ * reference's dense matrix restricted to its nonzeros (rows = (angle,
+ * detector), columns = pixels ascending).  dirs (device double[4*n_angles])
+ * = (cos, sin, -sin, cos) of each angle, computed by the host exactly as the
+ * reference does (np.cos / np.sin).  amvm_projector_indptr writes
+ * indptr[0..side*n_angles] (int64; workspace amvm_projector_workspace_bytes);
+ * the caller allocates indptr[rows] entries and calls amvm_projector_fill. */
+AMVM_API size_t amvm_projector_workspace_bytes(int64_t side, int64_t n_angles);
+AMVM_API int amvm_projector_indptr(int64_t side, int64_t n_angles, const double *dirs,
+                                   int64_t *indptr, void *ws, size_t ws_bytes, void *stream);
+AMVM_API int amvm_projector_fill(int64_t side, int64_t n_angles, const double *dirs,
+                                 const int64_t *indptr, int64_t *indices, double *values,
+                                 void *stream);
+
 /* HOST helper: numpy default_rng(seed).bit_generator.state for each seed
  * (SeedSequence -> PCG64), so per-instance seeds need no Python loop.      */
 AMVM_API int amvm_seed_pcg64(const uint64_t *seeds_host, int64_t count,

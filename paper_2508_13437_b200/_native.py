@@ -23,6 +23,8 @@ EXPORTS = (
     "amvm_find_candidates", "amvm_best_swap", "amvm_impact_scores", "amvm_destroy",
     "amvm_repair", "amvm_compute_residual", "amvm_ptq_prepare", "amvm_seed_pcg64", "amvm_status",
     "amvm_strerror", "amvm_abi_version", "amvm_brute_force_workspace_bytes", "amvm_brute_force",
+    "amvm_ls_start_workspace_bytes", "amvm_ls_start",
+    "amvm_projector_workspace_bytes", "amvm_projector_indptr", "amvm_projector_fill",
 )
 
 
@@ -95,6 +97,13 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_brute_force_workspace_bytes.restype = sz
     lib.amvm_brute_force_workspace_bytes.argtypes = [vp]
     lib.amvm_brute_force.argtypes = [vp, C.c_int, vp, vp, vp, vp, sz, vp]
+    lib.amvm_ls_start_workspace_bytes.restype = sz
+    lib.amvm_ls_start_workspace_bytes.argtypes = [i64, i64]
+    lib.amvm_ls_start.argtypes = [vp, vp, vp, vp, vp, sz, vp]
+    lib.amvm_projector_workspace_bytes.restype = sz
+    lib.amvm_projector_workspace_bytes.argtypes = [i64, i64]
+    lib.amvm_projector_indptr.argtypes = [i64, i64, vp, vp, vp, sz, vp]
+    lib.amvm_projector_fill.argtypes = [i64, i64, vp, vp, vp, vp, vp]
     lib.amvm_strerror.restype = C.c_char_p
     lib.amvm_strerror.argtypes = [C.c_int]
     for name in EXPORTS:

@@ -135,11 +135,17 @@ def _nearest_level_indices(levels: np.ndarray, vec: np.ndarray) -> np.ndarray:
     return np.argmin(dist, axis=1).astype(np.intp)
 
 
-def initial_solution(inst: Instance) -> Solution:
+def initial_solution(inst: Instance, *, device: bool = False) -> Solution:
     """Rounded warm start or regularized least squares (controller.py:134-165).
 
-    Host numpy on purpose: the starting residual is the one numpy's BLAS
-    produces, bit for bit."""
+    Host numpy by default: the starting residual is the one numpy's BLAS
+    produces, bit for bit.  ``device=True`` solves the
+    least-squares system on the GPU (``amvm_ls_start``: Gram matrix,
+    Cholesky, substitution and rounding in CUDA); its target agrees with
+    LAPACK's to rounding, so the rounded start matches unless a component
+    sits within rounding of a midpoint between two levels."""
+    if device and inst.continuous_init is None:
+        return _initial_solution_device(inst)
     if inst.continuous_init is not None:
         target = inst.continuous_init
     else:
@@ -154,6 +160,29 @@ def initial_solution(inst: Instance) -> Solution:
             target = np.zeros(inst.n)
     idx = _nearest_level_indices(inst.values.levels, target)
     return Solution.from_indices(inst, idx)
+
+
+def _initial_solution_device(inst: Instance, return_target: bool = False):
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    At, b, lv = inst.device_arrays(dev)
+    prob = N.Problem(inst.m, inst.n, len(inst.values), 1, At.data_ptr(), b.data_ptr(), lv.data_ptr())
+    nbytes = lib.amvm_ls_start_workspace_bytes(inst.m, inst.n)
+    ws = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+    idx = torch.empty(inst.n, dtype=torch.int32, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    tgt = torch.empty(inst.n, dtype=torch.float64, device=dev) if return_target else None
+    N.check(lib.amvm_ls_start(N.C.byref(prob), N.ptr(idx), N.ptr(tgt) if return_target else None, N.ptr(flag),
+                              N.ptr(ws),
+                              N.C.c_size_t(ws.numel()), N.stream_handle()), "amvm_ls_start")
+    f = int(flag.item())
+    if f == 1:
+        warnings.warn("least-squares start failed; starting from zeros", stacklevel=3)
+    elif f == 2:
+        warnings.warn("least-squares start not finite; starting from zeros", stacklevel=3)
+    sol = Solution.from_indices(inst, idx.cpu().numpy().astype(np.intp))
+    return (sol, tgt.cpu().numpy(), f) if return_target else sol
 
 
 # ----------------------------------------------------------------- plumbing
@@ -224,15 +253,17 @@ def _rng_sync_back(rng: np.random.Generator, dev_buf) -> None:
 
 
 # --------------------------------------------------------------------- solve
-def solve(inst: Instance, cfg: SolverConfig | None = None) -> SolveReport:
+def solve(inst: Instance, cfg: SolverConfig | None = None, *, device_warm_start: bool = False) -> SolveReport:
     """Run the adaptive destroy/repair/local-search loop on the GPU.
 
     Same semantics as dmmv.solve (controller.py:211-286): deterministic for a
-    fixed seed, stops at ``max_iters``, ``time_limit`` or a zero objective."""
+    fixed seed, stops at ``max_iters``, ``time_limit`` or a zero objective.
+    ``device_warm_start`` computes the least-squares start on the GPU
+    (``initial_solution(device=True)``)."""
     cfg = cfg or SolverConfig()
     started = time.perf_counter()
     rng = np.random.default_rng(cfg.seed)
-    current = initial_solution(inst)
+    current = initial_solution(inst, device=device_warm_start)
     initial_objective = current.objective
     max_iters = cfg.max_iters
     budget = None

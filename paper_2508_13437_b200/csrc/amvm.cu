@@ -11,6 +11,8 @@
 
 #include "amvm_engine.cuh"
 #include "amvm_exact.cuh"
+#include "amvm_lsq.cuh"
+#include "amvm_tomo.cuh"
 
 using namespace amvm;
 
@@ -806,6 +808,65 @@ int amvm_brute_force(const amvm_problem *prob, int order, int32_t *best_idx, dou
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
   k_brute_force_final<256><<<1, 256, 0, st>>>(blocks, (int)n, (int)nlev, blk_t, blk_c, best_idx, best_t,
                                                best_code);
+  return cuda_rc(cudaGetLastError());
+}
+
+// ---- device warm start: initial_solution's least-squares start (amvm_lsq.cuh) ----
+size_t amvm_ls_start_workspace_bytes(int64_t m, int64_t n) {
+  if (m < 1 || n < 1) return 0;
+  return 256 + (size_t)n * (size_t)n * sizeof(double) + (size_t)n * sizeof(double);
+}
+
+int amvm_ls_start(const amvm_problem *prob, int32_t *idx, double *target, int32_t *flag, void *ws,
+                  size_t ws_bytes, void *stream) {
+  if (!prob || !prob->At || !prob->B || !prob->levels || !idx || !flag) return AMVM_ERR_INVALID;
+  if (prob->m < 1 || prob->n < 1 || prob->nlev < 1 || prob->count != 1) return AMVM_ERR_INVALID;
+  const int64_t m = prob->m, n = prob->n;
+  if (!ws || ws_bytes < amvm_ls_start_workspace_bytes(m, n)) return AMVM_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  double *G = (double *)((char *)ws + 256);
+  double *y = G + n * n;
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  const int64_t tiles = (n + kLsT - 1) / kLsT;
+  k_gram<<<dim3((unsigned)tiles, (unsigned)tiles), 256, 0, st>>>(m, n, prob->At, G);
+  k_atb<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(m, n, prob->At, prob->B, y);
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    const unsigned g = (unsigned)((n - k - 1 + 15) / 16);
+    k_chol_step<<<dim3(g, g), 256, 0, st>>>(n, k, G, flag);
+  }
+  // the last pivot is only checked (no trailing matrix)
+  k_chol_step<<<dim3(1, 1), 256, 0, st>>>(n, n - 1, G, flag);
+  k_chol_solve<1024><<<1, 1024, 0, st>>>(n, prob->nlev, G, y, prob->levels, target, idx, flag);
+  return cuda_rc(cudaGetLastError());
+}
+
+// ---- tomography front end: parallel-beam projector as CSR (amvm_tomo.cuh) ----
+size_t amvm_projector_workspace_bytes(int64_t side, int64_t n_angles) {
+  if (side < 1 || n_angles < 1) return 0;
+  return (size_t)(side * n_angles) * sizeof(int64_t);
+}
+
+int amvm_projector_indptr(int64_t side, int64_t n_angles, const double *dirs, int64_t *indptr, void *ws,
+                          size_t ws_bytes, void *stream) {
+  if (side < 1 || n_angles < 1 || !dirs || !indptr) return AMVM_ERR_INVALID;
+  if (side > (1LL << 20)) return AMVM_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < amvm_projector_workspace_bytes(side, n_angles)) return AMVM_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = side * n_angles;
+  k_proj_count<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(side, n_angles, dirs, (int64_t *)ws);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  k_proj_scan<1024><<<1, 1024, 0, st>>>(rows, (const int64_t *)ws, indptr);
+  return cuda_rc(cudaGetLastError());
+}
+
+int amvm_projector_fill(int64_t side, int64_t n_angles, const double *dirs, const int64_t *indptr,
+                        int64_t *indices, double *values, void *stream) {
+  if (side < 1 || n_angles < 1 || !dirs || !indptr || !indices || !values) return AMVM_ERR_INVALID;
+  const int64_t rows = side * n_angles;
+  k_proj_fill<<<(unsigned)((rows + 127) / 128), 128, 0, (cudaStream_t)stream>>>(side, n_angles, dirs, indptr,
+                                                                                indices, values);
   return cuda_rc(cudaGetLastError());
 }
 

@@ -166,3 +166,32 @@ class SliceBatch:
 
     def check_status(self) -> None:
         self._lb.check_status()
+
+
+def projection_csr_device(side: int, n_angles: int, device=None):
+    """The projector built on the GPU (``amvm_projector_indptr`` /
+    ``amvm_projector_fill``, csrc/amvm_tomo.cuh) as device CSR tensors
+    (indptr, indices int64, values f64), bit-identical to
+    :func:`projection_csr` and to the reference's ``parallel_beam_matrix``
+    (builders.py:186-239).  The angle cosines/sines come from numpy, as in
+    the reference (builders.py:234-235)."""
+    from . import _native as N
+
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    th = np.arange(n_angles) * np.pi / n_angles
+    c, s = np.cos(th), np.sin(th)
+    dirs = torch.from_numpy(np.ascontiguousarray(np.stack([c, s, -s, c], axis=1))).to(dev)
+    rows = side * n_angles
+    ws = torch.empty(int(lib.amvm_projector_workspace_bytes(side, n_angles)), dtype=torch.uint8, device=dev)
+    indptr = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    st = N.stream_handle()
+    N.check(lib.amvm_projector_indptr(side, n_angles, N.ptr(dirs), N.ptr(indptr), N.ptr(ws),
+                                      N.C.c_size_t(ws.numel()), st), "amvm_projector_indptr")
+    nnz = int(indptr[-1].item())
+    indices = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+    values = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    N.check(lib.amvm_projector_fill(side, n_angles, N.ptr(dirs), N.ptr(indptr), N.ptr(indices), N.ptr(values),
+                                    st), "amvm_projector_fill")
+    return indptr, indices[:nnz], values[:nnz]
