@@ -234,6 +234,26 @@ AMVM_API int amvm_projector_fill(int64_t side, int64_t n_angles, const double *d
                                  const int64_t *indptr, int64_t *indices, double *values,
                                  void *stream);
 
+/* out (S x m) = A @ X[:, s] (+ noise, S x m, may be NULL) for the CSR A
+ * (m x n, columns ascending per row) and X (n x S): builders.py:322's
+ * projections `A @ truth + noise`, in numpy's dense dgemv_t order (zeros
+ * skipped exactly), bit-identical to the reference.                       */
+AMVM_API int amvm_csr_gemv(int64_t m, int64_t n, int64_t S, const int64_t *indptr,
+                           const int64_t *cols, const double *vals, const double *X,
+                           const double *noise, double *out, void *stream);
+
+/* SIRT warm start (builders.py:242-274) for S right-hand sides B (S x m)
+ * sharing the CSR A: X (n x S) from 0, `iters` updates
+ * x <- clip(x + C A^T R (b - A x), lo, hi) (clamp != 0).  Sums run in CSR /
+ * CSC storage order (not numpy's dense BLAS order): agrees with the
+ * reference to rounding.  Validation (A >= 0, a live row and column) is the
+ * caller's; ws holds amvm_sirt_workspace_bytes(m, n, nnz, S) bytes.       */
+AMVM_API size_t amvm_sirt_workspace_bytes(int64_t m, int64_t n, int64_t nnz, int64_t S);
+AMVM_API int amvm_sirt(int64_t m, int64_t n, int64_t nnz, int64_t S, const int64_t *indptr,
+                       const int64_t *cols, const double *vals, const double *B, int32_t iters,
+                       double lo, double hi, int clamp, double *X, void *ws, size_t ws_bytes,
+                       void *stream);
+
 /* HOST helper: numpy default_rng(seed).bit_generator.state for each seed
  * (SeedSequence -> PCG64), so per-instance seeds need no Python loop.      */
 AMVM_API int amvm_seed_pcg64(const uint64_t *seeds_host, int64_t count,

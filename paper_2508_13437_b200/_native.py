@@ -25,6 +25,7 @@ EXPORTS = (
     "amvm_strerror", "amvm_abi_version", "amvm_brute_force_workspace_bytes", "amvm_brute_force",
     "amvm_ls_start_workspace_bytes", "amvm_ls_start",
     "amvm_projector_workspace_bytes", "amvm_projector_indptr", "amvm_projector_fill",
+    "amvm_csr_gemv", "amvm_sirt_workspace_bytes", "amvm_sirt",
 )
 
 
@@ -104,6 +105,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_projector_workspace_bytes.argtypes = [i64, i64]
     lib.amvm_projector_indptr.argtypes = [i64, i64, vp, vp, vp, sz, vp]
     lib.amvm_projector_fill.argtypes = [i64, i64, vp, vp, vp, vp, vp]
+    lib.amvm_csr_gemv.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
+    lib.amvm_sirt_workspace_bytes.restype = sz
+    lib.amvm_sirt_workspace_bytes.argtypes = [i64, i64, i64, i64]
+    lib.amvm_sirt.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, i32, C.c_double, C.c_double, C.c_int, vp, vp,
+                              sz, vp]
     lib.amvm_strerror.restype = C.c_char_p
     lib.amvm_strerror.argtypes = [C.c_int]
     for name in EXPORTS:

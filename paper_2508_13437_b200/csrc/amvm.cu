@@ -870,4 +870,65 @@ int amvm_projector_fill(int64_t side, int64_t n_angles, const double *dirs, cons
   return cuda_rc(cudaGetLastError());
 }
 
+// ---- tomography front end: projections and SIRT (amvm_tomo.cuh) ----
+int amvm_csr_gemv(int64_t m, int64_t n, int64_t S, const int64_t *indptr, const int64_t *cols, const double *vals,
+                  const double *X, const double *noise, double *out, void *stream) {
+  if (m < 1 || n < 1 || S < 1 || !indptr || !cols || !vals || !X || !out) return AMVM_ERR_INVALID;
+  const int64_t t = m * S;
+  k_csr_gemv_t<<<(unsigned)((t + 255) / 256), 256, 0, (cudaStream_t)stream>>>(m, n, S, indptr, cols, vals, X,
+                                                                              noise, out);
+  return cuda_rc(cudaGetLastError());
+}
+
+static size_t sirt_layout(int64_t m, int64_t n, int64_t nnz, int64_t S, size_t off[8]) {
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~(size_t)255; return r; };
+  off[0] = take(sizeof(int64_t) * (size_t)n);        // column counts
+  off[1] = take(sizeof(int64_t) * (size_t)(n + 1));  // cptr
+  off[2] = take(sizeof(int64_t) * (size_t)n);        // fill positions
+  off[3] = take(sizeof(int64_t) * (size_t)nnz);      // CSC rows
+  off[4] = take(sizeof(double) * (size_t)nnz);       // CSC values
+  off[5] = take(sizeof(double) * (size_t)m);         // R
+  off[6] = take(sizeof(double) * (size_t)n);         // C
+  off[7] = take(sizeof(double) * (size_t)(m * S));   // R (b - A x)
+  return o;
+}
+
+size_t amvm_sirt_workspace_bytes(int64_t m, int64_t n, int64_t nnz, int64_t S) {
+  if (m < 1 || n < 1 || nnz < 0 || S < 1) return 0;
+  size_t off[8];
+  return sirt_layout(m, n, nnz, S, off);
+}
+
+int amvm_sirt(int64_t m, int64_t n, int64_t nnz, int64_t S, const int64_t *indptr, const int64_t *cols,
+              const double *vals, const double *B, int32_t iters, double lo, double hi, int clamp, double *X,
+              void *ws, size_t ws_bytes, void *stream) {
+  if (m < 1 || n < 1 || nnz < 0 || S < 1 || iters < 0 || !indptr || !cols || !vals || !B || !X)
+    return AMVM_ERR_INVALID;
+  size_t off[8];
+  const size_t need = sirt_layout(m, n, nnz, S, off);
+  if (!ws || ws_bytes < need) return AMVM_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  char *w = (char *)ws;
+  int64_t *ccnt = (int64_t *)(w + off[0]), *cptr = (int64_t *)(w + off[1]), *fpos = (int64_t *)(w + off[2]);
+  int64_t *crow = (int64_t *)(w + off[3]);
+  double *cval = (double *)(w + off[4]), *R = (double *)(w + off[5]), *Cw = (double *)(w + off[6]);
+  double *Rres = (double *)(w + off[7]);
+  cudaError_t e = cudaMemsetAsync(ccnt, 0, sizeof(int64_t) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(fpos, 0, sizeof(int64_t) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(X, 0, sizeof(double) * n * S, st);  // x = 0
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  if (nnz > 0) k_csr_colcount<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, cols, ccnt);
+  k_proj_scan<1024><<<1, 1024, 0, st>>>(n, ccnt, cptr);
+  k_csr_to_csc<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, indptr, cols, vals, cptr, fpos, crow, cval);
+  k_csc_sort<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, cptr, crow, cval);
+  const int64_t mx = m > n ? m : n;
+  k_sirt_weights<<<(unsigned)((mx + 255) / 256), 256, 0, st>>>(m, n, indptr, vals, cptr, cval, R, Cw);
+  for (int32_t it = 0; it < iters; ++it) {
+    k_sirt_rows<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(m, S, indptr, cols, vals, R, B, X, Rres);
+    k_sirt_cols<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, S, cptr, crow, cval, Cw, Rres, lo, hi, clamp, X);
+  }
+  return cuda_rc(cudaGetLastError());
+}
+
 }  // extern "C"

@@ -205,3 +205,164 @@ __global__ void __launch_bounds__(128) k_proj_fill(int64_t side, int64_t n_angle
 }
 
 }  // namespace amvm
+
+// ===================================================== projections and SIRT
+// b = A @ truth (builders.py:322) in numpy's dense dgemv_t order, from the
+// CSR rows: the dense kernel sums K & -4 columns in blocks of 2048 with the
+// output row's kernel (kind 4: four FMA lanes by column mod 4, folded
+// (l0+l2)+(l1+l3); kind 2: two mul+add lanes; kind 1: two mul+add pairs),
+// each block added to y, then the K & 3 leftover.  Zero entries add exact
+// zeros, so visiting only the nonzeros, in column order, reproduces the
+// dense result bit for bit.  Thread per (row, slice); X is n x S.
+namespace amvm {
+__device__ double csr_gemv_t_row(const int64_t *__restrict__ cols, const double *__restrict__ vals, int64_t lo,
+                                 int64_t hi, const double *__restrict__ X, int64_t S, int64_t s, int64_t K,
+                                 int kind) {
+  const int64_t m1 = K & -4;
+  double y = 0.0, l[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t blk = 0;
+  auto fold = [&]() {
+    double t;
+    if (kind == 4) t = __dadd_rn(__dadd_rn(l[0], l[2]), __dadd_rn(l[1], l[3]));
+    else if (kind == 2) t = __dadd_rn(l[0], l[1]);
+    else t = __dadd_rn(__dadd_rn(l[0], l[2]), __dadd_rn(l[1], l[3]));  // (u0+v0)+(u1+v1)
+    y = __dadd_rn(y, t);
+    l[0] = l[1] = l[2] = l[3] = 0.0;
+  };
+  int64_t e = lo;
+  for (; e < hi && cols[e] < m1; ++e) {
+    const int64_t j = cols[e];
+    const int64_t b = j >> 11;  // 2048-column block
+    while (blk < b) { fold(); ++blk; }
+    const double p = X[j * S + s];
+    if (kind == 4) l[j & 3] = __fma_rn(vals[e], p, l[j & 3]);
+    else if (kind == 2) l[j & 1] = __dadd_rn(l[j & 1], __dmul_rn(vals[e], p));
+    else l[j & 3] = __dadd_rn(l[j & 3], __dmul_rn(vals[e], p));  // u0,u1,v0,v1 = lanes 0,1,2,3
+  }
+  if (m1 > 0) {
+    const int64_t nb = (m1 + 2047) >> 11;
+    while (blk < nb) { fold(); ++blk; }
+  }
+  // K & 3 leftover (scalar, compiler-contracted in OpenBLAS)
+  double a[3] = {0.0, 0.0, 0.0};
+  for (; e < hi; ++e) a[cols[e] - m1] = vals[e];
+  double x3[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < (int)(K & 3); ++q) x3[q] = X[(m1 + q) * S + s];
+  switch (K & 3) {
+    case 1: y = __fma_rn(a[0], x3[0], y); break;
+    case 2: y = __dadd_rn(y, __fma_rn(a[0], x3[0], __dmul_rn(a[1], x3[1]))); break;
+    case 3: y = __dadd_rn(y, __fma_rn(a[2], x3[2], __fma_rn(a[0], x3[0], __dmul_rn(a[1], x3[1])))); break;
+    default: break;
+  }
+  return y;
+}
+
+// out[i*S + s] = (A @ X[:, s])_i (+ noise[s*m + i] when noise != NULL,
+// builders.py:322: `A @ truth + rng.uniform(...)`)
+__global__ void __launch_bounds__(256) k_csr_gemv_t(int64_t m, int64_t n, int64_t S, const int64_t *__restrict__ indptr,
+                                                    const int64_t *__restrict__ cols, const double *__restrict__ vals,
+                                                    const double *__restrict__ X, const double *__restrict__ noise,
+                                                    double *__restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (t >= m * S) return;
+  const int64_t i = t / S, s = t - i * S;
+  const int kind = gemv_kind(i, m);
+  double y = csr_gemv_t_row(cols, vals, indptr[i], indptr[i + 1], X, S, s, n, kind);
+  if (noise) y = __dadd_rn(y, noise[s * m + i]);
+  out[s * m + i] = y;
+}
+
+// ---- CSC copy of the CSR matrix (columns in ascending row order) ----------
+__global__ void k_csr_colcount(int64_t nnz, const int64_t *__restrict__ cols, int64_t *__restrict__ cnt) {
+  const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (e < nnz) atomicAdd((unsigned long long *)&cnt[cols[e]], 1ull);
+}
+
+__global__ void k_csr_to_csc(int64_t m, const int64_t *__restrict__ indptr, const int64_t *__restrict__ cols,
+                             const double *__restrict__ vals, const int64_t *__restrict__ cptr,
+                             int64_t *__restrict__ fillpos, int64_t *__restrict__ rows, double *__restrict__ cvals) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= m) return;
+  for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+    const int64_t j = cols[e];
+    const int64_t p = cptr[j] + (int64_t)atomicAdd((unsigned long long *)&fillpos[j], 1ull);
+    rows[p] = i;
+    cvals[p] = vals[e];
+  }
+}
+
+// insertion sort of each column by row (atomics placed them in any order)
+__global__ void k_csc_sort(int64_t n, const int64_t *__restrict__ cptr, int64_t *__restrict__ rows,
+                           double *__restrict__ cvals) {
+  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (j >= n) return;
+  const int64_t lo = cptr[j], hi = cptr[j + 1];
+  for (int64_t a = lo + 1; a < hi; ++a) {
+    const int64_t r = rows[a];
+    const double v = cvals[a];
+    int64_t b = a - 1;
+    while (b >= lo && rows[b] > r) {
+      rows[b + 1] = rows[b];
+      cvals[b + 1] = cvals[b];
+      --b;
+    }
+    rows[b + 1] = r;
+    cvals[b + 1] = v;
+  }
+}
+
+// ---- SIRT (builders.py:242-274), S right-hand sides: B is S x m, X n x S --
+// rowsum / colsum in storage order; R = 1/rowsum (live rows), C = 1/colsum
+// (0 for empty columns).
+__global__ void k_sirt_weights(int64_t m, int64_t n, const int64_t *__restrict__ indptr,
+                               const double *__restrict__ vals, const int64_t *__restrict__ cptr,
+                               const double *__restrict__ cvals, double *__restrict__ R, double *__restrict__ Cw) {
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (t < m) {
+    double s = 0.0;
+    for (int64_t e = indptr[t]; e < indptr[t + 1]; ++e) s = __dadd_rn(s, vals[e]);
+    R[t] = s > 0.0 ? __ddiv_rn(1.0, s) : 0.0;
+  }
+  if (t < n) {
+    double s = 0.0;
+    for (int64_t e = cptr[t]; e < cptr[t + 1]; ++e) s = __dadd_rn(s, cvals[e]);
+    Cw[t] = s > 0.0 ? __ddiv_rn(1.0, s) : 0.0;
+  }
+}
+
+// Rres[i][s] = R_i (b_is - (A x_s)_i), warp per row, lanes over slices.
+__global__ void __launch_bounds__(256) k_sirt_rows(int64_t m, int64_t S, const int64_t *__restrict__ indptr,
+                                                   const int64_t *__restrict__ cols, const double *__restrict__ vals,
+                                                   const double *__restrict__ R, const double *__restrict__ B,
+                                                   const double *__restrict__ X, double *__restrict__ Rres) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= m) return;
+  const int64_t lo = indptr[i], hi = indptr[i + 1];
+  const double ri = R[i];
+  for (int64_t s = lane; s < S; s += 32) {
+    double ax = 0.0;
+    for (int64_t e = lo; e < hi; ++e) ax = __fma_rn(vals[e], X[cols[e] * S + s], ax);
+    Rres[i * S + s] = ri > 0.0 ? __dmul_rn(ri, __dsub_rn(B[s * m + i], ax)) : 0.0;
+  }
+}
+
+// x_js = clip(x_js + C_j (A^T r_s)_j, lo, hi), warp per column.
+__global__ void __launch_bounds__(256) k_sirt_cols(int64_t n, int64_t S, const int64_t *__restrict__ cptr,
+                                                   const int64_t *__restrict__ rows, const double *__restrict__ cvals,
+                                                   const double *__restrict__ Cw, const double *__restrict__ Rres,
+                                                   double lo, double hi, int clamp, double *__restrict__ X) {
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const int64_t a = cptr[j], b = cptr[j + 1];
+  const double cj = Cw[j];
+  for (int64_t s = lane; s < S; s += 32) {
+    double g = 0.0;
+    for (int64_t e = a; e < b; ++e) g = __fma_rn(cvals[e], Rres[rows[e] * S + s], g);
+    double x = __dadd_rn(X[j * S + s], __dmul_rn(cj, g));
+    if (clamp) x = fmin(fmax(x, lo), hi);
+    X[j * S + s] = x;
+  }
+}
+}  // namespace amvm

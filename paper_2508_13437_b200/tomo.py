@@ -195,3 +195,83 @@ def projection_csr_device(side: int, n_angles: int, device=None):
     N.check(lib.amvm_projector_fill(side, n_angles, N.ptr(dirs), N.ptr(indptr), N.ptr(indices), N.ptr(values),
                                     st), "amvm_projector_fill")
     return indptr, indices[:nnz], values[:nnz]
+
+
+def projections_device(csr, m: int, n: int, X, noise=None):
+    """``A @ X[:, s] (+ noise[s])`` for each column s of X (n x S, device),
+    in numpy's dense dgemv order (``amvm_csr_gemv``): bitwise the
+    reference's ``A @ truth.ravel() + noise`` (builders.py:322).  Returns
+    S x m."""
+    from . import _native as N
+
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    indptr, indices, values = csr
+    X = X.contiguous()
+    S = X.shape[1]
+    out = torch.empty((S, m), dtype=torch.float64, device=X.device)
+    nz = noise.contiguous() if noise is not None else None
+    N.check(lib.amvm_csr_gemv(m, n, S, N.ptr(indptr), N.ptr(indices), N.ptr(values), N.ptr(X),
+                              N.ptr(nz) if nz is not None else None, N.ptr(out), N.stream_handle()),
+            "amvm_csr_gemv")
+    return out
+
+
+def sirt_device(csr, m: int, n: int, B, iters: int, lo=None, hi=None):
+    """Clamped SIRT (builders.py:242-274) for the S right-hand sides B (S x m,
+    device) sharing the CSR A, on the GPU (``amvm_sirt``); returns X (n x S).
+    Same validation as the reference; the sums run in sparse storage order,
+    so X agrees with the reference to rounding."""
+    from . import _native as N
+
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    indptr, indices, values = csr
+    if iters < 0:
+        raise ValueError("iters must be non-negative")
+    if bool((values < 0).any()):
+        raise ValueError("the projection matrix must be non-negative")
+    if int(indptr[-1]) == 0:
+        raise ValueError("every row of A is zero")
+    B = B.contiguous()
+    S = B.shape[0]
+    nnz = int(values.numel())
+    X = torch.empty((n, S), dtype=torch.float64, device=B.device)
+    ws = torch.empty(int(lib.amvm_sirt_workspace_bytes(m, n, nnz, S)), dtype=torch.uint8, device=B.device)
+    clamp = lo is not None or hi is not None
+    lo_v = float(lo) if lo is not None else -np.inf
+    hi_v = float(hi) if hi is not None else np.inf
+    N.check(lib.amvm_sirt(m, n, nnz, S, N.ptr(indptr), N.ptr(indices), N.ptr(values), N.ptr(B), int(iters),
+                          lo_v, hi_v, int(clamp), N.ptr(X), N.ptr(ws), N.C.c_size_t(ws.numel()),
+                          N.stream_handle()), "amvm_sirt")
+    return X
+
+
+def build_tomo_device(side: int, gray_levels, n_angles: int, noise: float, seeds=(0,), phantom_kinds=("disk",),
+                      sirt_iters: int = 500, device=None) -> dict:
+    """The reference's ``build_tomo`` (builders.py:306-327) for several slices
+    at once, front end on the GPU: projector (bitwise), noisy projections
+    (bitwise; the uniform noise is drawn by numpy from each slice's seed, as
+    the reference does), clamped SIRT warm start (to rounding) and its
+    nearest-level start.  Slice k uses seeds[k] and phantom_kinds[k % len].
+    Returns device tensors: csr, B (S x m), warm (S x n), idx0 (S x n int32),
+    truth (S x n) and the host levels."""
+    from . import _native as N
+
+    torch = N.torch_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    lv = np.asarray(gray_levels, dtype=np.float64)
+    m, n = n_angles * side, side * side
+    csr = projection_csr_device(side, n_angles, dev)
+    truths, noises = [], []
+    for k, seed in enumerate(seeds):
+        labels = phantom(phantom_kinds[k % len(phantom_kinds)], side)
+        truths.append(lv[np.minimum(labels, lv.size - 1)].ravel())
+        noises.append(np.random.default_rng(seed).uniform(-noise, noise, m))
+    truth = torch.from_numpy(np.stack(truths)).to(dev)
+    B = projections_device(csr, m, n, truth.t().contiguous(), torch.from_numpy(np.stack(noises)).to(dev))
+    X = sirt_device(csr, m, n, B, sirt_iters, lo=float(lv[0]), hi=float(lv[-1]))
+    warm = X.t().contiguous()
+    lvd = torch.from_numpy(lv).to(dev)
+    idx0 = torch.argmin(torch.abs(warm[:, :, None] - lvd[None, None, :]), dim=2).to(torch.int32)
+    return {"csr": csr, "B": B, "warm": warm, "idx0": idx0, "truth": truth, "levels": lv, "m": m, "n": n}

@@ -44,3 +44,38 @@ def test_device_projector_matches_reference_matrices(tomo):
     dp, dx, dv = tomo.projection_csr_device(side, n_angles)
     A = torch.sparse_csr_tensor(dp, dx, dv, size=(side * n_angles, side * side)).to_dense().cpu().numpy()
     assert sha(A) == str(rec["A_sha"])
+
+
+@pytest.mark.parametrize("name", ["c3s", "c3m"])
+def test_device_front_end_matches_reference_build_tomo(tomo, name):
+    """build_tomo on the GPU vs the reference's own instances
+    (make_golden.py: TomoSpec squares, levels 0/1/2, eta = 5% of the max row
+    sum, sirt_iters 100, seed 0): projections b bit for bit, the SIRT warm
+    start within SIRT_ATOL (sparse vs dense BLAS summation order), and its
+    rounded start equal to the reference's initial solution."""
+    SIRT_ATOL = 1e-9
+    rec = load(f"solve_{name}")[0]
+    if name == "c3s":
+        side, n_angles = 64, 45
+        A = stored_A(rec)
+    else:
+        side, n_angles = (int(v) for v in rec["A_recipe"])
+        A = tomo.projection_matrix(side, n_angles)
+    eta = 0.05 * float(A.sum(axis=1).max())
+    del A
+    out = tomo.build_tomo_device(side, (0.0, 1.0, 2.0), n_angles, eta, seeds=(0,), phantom_kinds=("squares",),
+                                 sirt_iters=100)
+    b = out["B"][0].cpu().numpy()
+    assert np.array_equal(b.view(np.uint64), rec["b"].view(np.uint64))
+    if "continuous_init" in rec:
+        np.testing.assert_allclose(out["warm"][0].cpu().numpy(), rec["continuous_init"], rtol=0, atol=SIRT_ATOL)
+    np.testing.assert_array_equal(out["idx0"][0].cpu().numpy(), rec["idx0"])
+
+
+def test_sirt_validation(tomo):
+    import torch
+
+    csr = (torch.tensor([0, 1], device="cuda"), torch.tensor([0], device="cuda"),
+           torch.tensor([-1.0], device="cuda", dtype=torch.float64))
+    with pytest.raises(ValueError, match="non-negative"):
+        tomo.sirt_device(csr, 1, 1, torch.ones((1, 1), device="cuda", dtype=torch.float64), 3)

@@ -1,7 +1,7 @@
 """C3 family throughput: S tomography slices sharing one projector, one
-device batch (tomo.SliceBatch).  Front end on the device with torch
-(projector CSR -> dense A, noisy projections, clamped SIRT warm start);
-the ALNS path is libamvm.  Prints one JSON line.
+device batch (tomo.SliceBatch).  Front end on the device through libamvm
+(tomo.build_tomo_device: projector CSR, noisy projections, clamped SIRT warm
+start); the ALNS path is libamvm.  Prints one JSON line.
 
 usage: python tools/c3_slices.py SIDE N_ANGLES SLICES ITERS [SIRT_ITERS]
 """
@@ -21,32 +21,28 @@ side, n_ang, S, iters = (int(v) for v in sys.argv[1:5])
 sirt_iters = int(sys.argv[5]) if len(sys.argv) > 5 else 100
 dev = torch.device("cuda")
 t0 = time.perf_counter()
-indptr, idx, val = tomo.projection_csr(side, n_ang)
 m, n = n_ang * side, side * side
-t1 = time.perf_counter()
-import warnings  # noqa: E402
-warnings.filterwarnings("ignore", message="Sparse CSR tensor support is in beta")
-A = torch.sparse_csr_tensor(torch.from_numpy(indptr), torch.from_numpy(idx), torch.from_numpy(val),
-                            size=(m, n), dtype=torch.float64).to(dev).to_dense()
 lv = np.array([0.0, 1.0, 2.0])
 kinds = ("squares", "disk", "checker")
-truth = torch.stack([torch.from_numpy(lv[np.minimum(tomo.phantom(kinds[k % 3], side), 2)].ravel())
-                     for k in range(S)]).to(dev).t()  # n x S
-eta = 0.05 * float(A.sum(dim=1).max())
-g = torch.Generator(device=dev).manual_seed(0)
-Bm = A @ truth + (torch.rand((m, S), generator=g, device=dev, dtype=torch.float64) * 2 - 1) * eta
-# SIRT (builders.py:242-274 semantics), batched over slices, clamped
-rs, cs = A.sum(dim=1), A.sum(dim=0)
-R = torch.where(rs > 0, 1.0 / rs, torch.zeros_like(rs))[:, None]
-C = torch.where(cs > 0, 1.0 / cs, torch.zeros_like(cs))[:, None]
-X = torch.zeros((n, S), dtype=torch.float64, device=dev)
-for _ in range(sirt_iters):
-    X = (X + C * (A.t() @ (R * (Bm - A @ X)))).clamp(lv[0], lv[-1])
-idx0 = torch.argmin((X[:, :, None] - torch.from_numpy(lv).to(dev)).abs(), dim=2).t().to(torch.int32)
+# eta = 5% of the max row sum (make_golden.py), from the device projector
+csr = tomo.projection_csr_device(side, n_ang, dev)
+rows = torch.repeat_interleave(torch.arange(m, device=dev), csr[0][1:] - csr[0][:-1])
+eta = 0.05 * float(torch.zeros(m, dtype=torch.float64, device=dev).index_add_(0, rows, csr[2]).max())
+torch.cuda.synchronize()
+t1 = time.perf_counter()
+# build_tomo (builders.py:306-327) for S slices on the device: projector,
+# noisy projections (bitwise), clamped SIRT, rounded start
+fe = tomo.build_tomo_device(side, lv, n_ang, eta, seeds=tuple(range(S)), phantom_kinds=kinds,
+                            sirt_iters=sirt_iters, device=dev)
 torch.cuda.synchronize()
 t2 = time.perf_counter()
-sb = tomo.SliceBatch(A, Bm.t().contiguous().cpu().numpy(), lv, idx0.cpu().numpy())
-del A, truth, X
+indptr = fe["csr"][0].cpu().numpy()
+import warnings  # noqa: E402
+warnings.filterwarnings("ignore", message="Sparse CSR tensor support is in beta")
+A = torch.sparse_csr_tensor(*fe["csr"], size=(m, n), dtype=torch.float64).to_dense()
+Bm, idx0 = fe["B"], fe["idx0"]
+sb = tomo.SliceBatch(A, Bm.cpu().numpy(), lv, idx0.cpu().numpy())
+del A, fe
 torch.cuda.synchronize()
 cfg = SolverConfig(max_iters=iters)
 o = sb.solve(cfg)  # warm-up
@@ -70,4 +66,5 @@ print(json.dumps({
     "events_per_slice": {k: round(float(v / S), 1) for k, v in zip(
         ["fc_calls", "fc_survivors", "swaps", "oo_exact_scans", "oo_moves", "oo_windows", "impact_calls",
          "refreshes"], pc[8:16])},
-    "front_end_s": {"projector_csr": round(t1 - t0, 2), "device_build_sirt": round(t2 - t1, 2)}}))
+    "front_end_s": {"projector_csr_eta": round(t1 - t0, 2),
+                    f"build_tomo_device (projector, projections, {sirt_iters} SIRT iterations)": round(t2 - t1, 2)}}))
