@@ -206,6 +206,23 @@ AMVM_API int amvm_brute_force(const amvm_problem *prob, int order, int32_t *best
                               double *best_t, int64_t *best_code, void *ws,
                               size_t ws_bytes, void *stream);
 
+/* is_improving (localsearch.py:91-125) for nc swap candidates (i, j,
+ * delta = x_i - x_j > 0) against the solution (residual, objective):
+ * verdict[c] = 1 iff every row keeps (-t-s)/delta < a_j - a_i < (t-s)/delta.
+ * The reference's row screen only skips rows that pass, so this is its
+ * verdict with or without the screen.  Device pointers; count == 1.       */
+AMVM_API int amvm_is_improving(const amvm_problem *prob, const double *residual, double objective,
+                               int64_t nc, const int32_t *ci, const int32_t *cj,
+                               const double *cd, int32_t *verdict, void *stream);
+
+/* exhaustive_swap_check (oracle.py:135-161): for every ordered pair with
+ * x_i > x_j, out_t[i*n+j] = objective of the swapped assignment recomputed
+ * from scratch in numpy's order (compute_residual, core.py:183-197) and
+ * out_v[i*n+j] = the swap test's verdict; other entries are not written.
+ * count == 1, n <= 4096 (the reference allows n <= 64).                    */
+AMVM_API int amvm_swap_check(const amvm_problem *prob, const int32_t *idx, const double *residual,
+                             double objective, double *out_t, int32_t *out_v, void *stream);
+
 /* ---- device warm start: initial_solution without continuous_init --------
  * (controller.py:134-165): (A^T A + 1e-8 I) x = A^T b by Cholesky on the
  * device, idx[j] = nearest level of x_j (ties to the lower level), x = 0 if

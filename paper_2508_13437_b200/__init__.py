@@ -36,7 +36,16 @@ from .controller import (  # noqa: F401
     solve,
     worst_remove_destroy,
 )
-from .exact import DEFAULT_BUDGET, BudgetExceededError, OracleResult, brute_force  # noqa: F401
+from .exact import (  # noqa: F401
+    DEFAULT_BUDGET,
+    MAX_SWAP_CHECK_N,
+    BudgetExceededError,
+    OracleResult,
+    SwapCheckReport,
+    brute_force,
+    exhaustive_swap_check,
+    is_improving,
+)
 from .core import (  # noqa: F401
     REFRESH_PERIOD,
     Instance,
@@ -55,5 +64,6 @@ __all__ = [
     "SwapCandidate", "SolveReport", "SolverConfig", "TraceEntry", "best_swap", "find_candidates",
     "greedy_repair", "impact_scores", "initial_solution", "local_search", "one_opt",
     "random_destroy", "random_repair", "removal_count", "solve", "worst_remove_destroy",
-    "DEFAULT_BUDGET", "BudgetExceededError", "OracleResult", "brute_force",
+    "DEFAULT_BUDGET", "BudgetExceededError", "OracleResult", "brute_force", "MAX_SWAP_CHECK_N",
+    "SwapCheckReport", "exhaustive_swap_check", "is_improving",
 ]

@@ -931,4 +931,27 @@ int amvm_sirt(int64_t m, int64_t n, int64_t nnz, int64_t S, const int64_t *indpt
   return cuda_rc(cudaGetLastError());
 }
 
+// ---- verification kernels: is_improving, exhaustive_swap_check (amvm_exact.cuh) ----
+int amvm_is_improving(const amvm_problem *prob, const double *residual, double objective, int64_t nc,
+                      const int32_t *ci, const int32_t *cj, const double *cd, int32_t *verdict, void *stream) {
+  if (!prob || !prob->At || !residual || nc < 0 || (nc > 0 && (!ci || !cj || !cd || !verdict)))
+    return AMVM_ERR_INVALID;
+  if (prob->m < 1 || prob->n < 1) return AMVM_ERR_INVALID;
+  if (nc == 0) return AMVM_OK;
+  k_is_improving<<<(unsigned)((nc + 7) / 8), 256, 0, (cudaStream_t)stream>>>(prob->m, prob->At, residual, objective,
+                                                                             nc, ci, cj, cd, verdict);
+  return cuda_rc(cudaGetLastError());
+}
+
+int amvm_swap_check(const amvm_problem *prob, const int32_t *idx, const double *residual, double objective,
+                    double *out_t, int32_t *out_v, void *stream) {
+  if (!prob || !prob->At || !prob->B || !prob->levels || !idx || !residual || !out_t || !out_v)
+    return AMVM_ERR_INVALID;
+  if (prob->m < 1 || prob->n < 1 || prob->count != 1) return AMVM_ERR_INVALID;
+  if (prob->n > 4096) return AMVM_ERR_UNSUPPORTED;
+  k_swap_check<<<(unsigned)(prob->n * prob->n), 256, 0, (cudaStream_t)stream>>>(
+      prob->m, prob->n, prob->At, prob->B, prob->levels, idx, residual, objective, out_t, out_v);
+  return cuda_rc(cudaGetLastError());
+}
+
 }  // extern "C"

@@ -189,3 +189,79 @@ __global__ void __launch_bounds__(NTB) k_brute_force_final(int nblk, int n, int 
 }
 
 }  // namespace amvm
+
+// ---- is_improving (localsearch.py:91-125) and exhaustive_swap_check
+// (oracle.py:135-161), verification kernels off the solve path.
+namespace amvm {
+// Swap test of candidate c: every row keeps lo < a_j - a_i < hi with
+// lo = (-t - s)/delta, hi = (t - s)/delta (the row screen only skips rows
+// that provably pass, so the verdict is the unscreened one).  Warp per
+// candidate.
+__global__ void __launch_bounds__(256) k_is_improving(int64_t m, const double *__restrict__ At,
+                                                      const double *__restrict__ s, double t, int64_t nc,
+                                                      const int32_t *__restrict__ ci, const int32_t *__restrict__ cj,
+                                                      const double *__restrict__ cd, int32_t *__restrict__ verdict) {
+  const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= nc) return;
+  const double d = cd[c];
+  const double *ai = At + (int64_t)ci[c] * m, *aj = At + (int64_t)cj[c] * m;
+  bool ok = true;
+  for (int64_t r = lane; r < m && ok; r += 32) {
+    const double lo = __ddiv_rn(__dsub_rn(-t, s[r]), d), hi = __ddiv_rn(__dsub_rn(t, s[r]), d);
+    const double diff = __dsub_rn(aj[r], ai[r]);
+    ok = lo < diff && diff < hi;
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (lane == 0) verdict[c] = ok;
+}
+
+// For every ordered pair (i, j) with x_i > x_j: the post-swap objective
+// recomputed from scratch (compute_residual, core.py:183-197: numpy's
+// dgemv_t order per row, ddot when m == 1) and the swap test's verdict.
+// CTA per pair; out_t / out_v are n x n (untouched where x_i <= x_j).
+__global__ void __launch_bounds__(256) k_swap_check(int64_t m, int64_t n, const double *__restrict__ At,
+                                                    const double *__restrict__ b, const double *__restrict__ lv,
+                                                    const int32_t *__restrict__ idx, const double *__restrict__ s,
+                                                    double t, double *__restrict__ out_t,
+                                                    int32_t *__restrict__ out_v) {
+  const int64_t i = blockIdx.x / n, j = blockIdx.x - i * n;
+  const double xi = lv[idx[i]], xj = lv[idx[j]];
+  if (i == j || !(xi > xj)) return;
+  const double d = __dsub_rn(xi, xj);
+  auto x = [&](int64_t q) { return q == i ? xj : (q == j ? xi : lv[idx[q]]); };
+  double tm = 0.0;
+  bool ok = true;
+  if (m == 1) {
+    if (threadIdx.x < 32) {
+      const double v = warp_ddot_skx([&](int64_t q) { return At[q]; }, [&](int64_t q) { return x(q); }, n,
+                                     (int)threadIdx.x);
+      tm = fabs(__dsub_rn(v, b[0]));
+    }
+  } else {
+    for (int64_t r = threadIdx.x; r < m; r += 256) {
+      const double v = gemv_row([&](int64_t q) { return At[q * m + r]; }, [&](int64_t q) { return x(q); }, n,
+                                gemv_kind(r, m));
+      tm = fmax(tm, fabs(__dsub_rn(v, b[r])));
+    }
+  }
+  for (int64_t r = threadIdx.x; r < m; r += 256) {
+    const double lo = __ddiv_rn(__dsub_rn(-t, s[r]), d), hi = __ddiv_rn(__dsub_rn(t, s[r]), d);
+    const double diff = __dsub_rn(At[j * m + r], At[i * m + r]);
+    ok = ok && lo < diff && diff < hi;
+  }
+  tm = warp_max(tm);
+  ok = __all_sync(0xffffffffu, ok);
+  __shared__ double wt[8];
+  __shared__ int wv[8];
+  if ((threadIdx.x & 31) == 0) { wt[threadIdx.x >> 5] = tm; wv[threadIdx.x >> 5] = ok; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double T = 0.0;
+    int V = 1;
+    for (int w = 0; w < 8; ++w) { T = fmax(T, wt[w]); V &= wv[w]; }
+    out_t[blockIdx.x] = T;
+    out_v[blockIdx.x] = V;
+  }
+}
+}  // namespace amvm

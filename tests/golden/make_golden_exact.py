@@ -53,6 +53,61 @@ def cases():
     return out
 
 
+def swap_cases():
+    """(A, b, levels, idx) for exhaustive_swap_check: random starts, a start
+    after the reference's own local search (few improving pairs, boundary
+    ties), integer data (exact ties) and m = 1 (numpy's ddot path)."""
+    from dmmv import localsearch as ls
+
+    rng = np.random.default_rng(137)
+    out = []
+    for m, n, nlev in [(30, 12, 5), (64, 20, 8), (9, 16, 4), (1, 10, 6), (120, 7, 16)]:
+        A = rng.uniform(-1, 1, (m, n))
+        lv = np.linspace(-2, 2, nlev)
+        b = A @ rng.uniform(-2, 2, n)
+        out.append((A, b, lv, rng.integers(0, nlev, n)))
+    A = rng.uniform(-1, 1, (40, 24))
+    lv = np.linspace(-3, 3, 7)
+    b = A @ rng.uniform(-3, 3, 24)
+    inst = dmmv.Instance(A, b, dmmv.ValueSet(lv))
+    sol = dmmv.Solution.from_indices(inst, rng.integers(0, 7, 24))
+    ls.local_search(inst, sol, dmmv.FilterConfig())
+    out.append((A, b, lv, sol.idx.copy()))
+    A = rng.integers(-2, 3, (10, 9)).astype(float)
+    lv = np.arange(5, dtype=float) - 2
+    out.append((A, rng.integers(-3, 4, 10).astype(float), lv, rng.integers(0, 5, 9)))
+    return out
+
+
+def swap_main() -> None:
+    from dmmv import localsearch as ls
+
+    rec = {}
+    cs = swap_cases()
+    for k, (A, b, lv, idx) in enumerate(cs):
+        inst = dmmv.Instance(A, b, dmmv.ValueSet(lv))
+        sol = dmmv.Solution.from_indices(inst, idx)
+        n = inst.n
+        T = np.full((n, n), np.nan)
+        V = np.zeros((n, n), np.int32)
+        x = sol.values(inst)
+        for i in range(n):
+            for j in range(n):
+                if i == j or x[i] <= x[j]:
+                    continue
+                sw = sol.idx.copy()
+                sw[i], sw[j] = sw[j], sw[i]
+                T[i, j] = dmmv.compute_residual(inst, sw)[1]
+                V[i, j] = ls.is_improving(inst, sol, ls.SwapCandidate(i, j, float(x[i] - x[j])))
+        rep = ref_oracle.exhaustive_swap_check(inst, sol)
+        rec.update({f"{k}/A": A, f"{k}/b": b, f"{k}/levels": lv, f"{k}/idx": sol.idx.astype(np.int32),
+                    f"{k}/residual": sol.residual, f"{k}/objective": sol.objective, f"{k}/T": T, f"{k}/V": V,
+                    f"{k}/pairs_checked": rep.pairs_checked, f"{k}/n_discrepancies": len(rep.discrepancies),
+                    f"{k}/n_boundary": len(rep.boundary)})
+    np.savez_compressed(os.path.join(HERE, "swap_check.npz"), count=len(cs), **rec)
+    print(f"{len(cs)} swap_check records")
+
+
 def main() -> None:
     rec = {}
     cs = cases()
@@ -71,3 +126,4 @@ def main() -> None:
 
 if __name__ == "__main__":
     main()
+    swap_main()

@@ -92,3 +92,58 @@ def test_gpu_brute_force_matches_oracle_large(amvm, m, n, nlev, kind):
         np.testing.assert_array_equal(res.best_idx, idx)
         assert res.best_t == t
         assert res.enumerated == enum
+
+
+def test_swap_check_host_validation(monkeypatch):
+    """n > 64 and delta <= 0 are rejected before any device work, with the
+    reference's messages (oracle.py:142-143, localsearch.py:110-111)."""
+    import torch
+
+    import paper_2508_13437_b200 as P
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    inst = P.Instance(np.ones((2, 65)), np.ones(2), P.ValueSet([0.0, 1.0]))
+    sol = P.Solution.from_indices(inst, np.zeros(65, dtype=np.intp))
+    with pytest.raises(ValueError, match="restricted to n <= 64"):
+        P.exhaustive_swap_check(inst, sol)
+    with pytest.raises(ValueError, match="delta = x_i - x_j > 0"):
+        P.is_improving(inst, sol, P.SwapCandidate(0, 1, 0.0))
+
+
+@pytest.mark.gpu
+def test_gpu_swap_check_matches_reference(amvm):
+    """Every pair's recomputed objective bitwise (numpy's compute_residual
+    order, incl. the m = 1 ddot path), every verdict, and the report."""
+    from paper_2508_13437_b200.exact import is_improving_batch
+
+    P = amvm
+    recs = load("swap_check")
+    assert len(recs) >= 7
+    for r in recs:
+        inst = P.Instance(r["A"], r["b"], P.ValueSet(r["levels"]))
+        sol = P.Solution.from_indices(inst, r["idx"].astype(np.intp))
+        assert sol.objective == r["objective"]
+        rep = P.exhaustive_swap_check(inst, sol)
+        assert rep.pairs_checked == r["pairs_checked"]
+        assert len(rep.discrepancies) == r["n_discrepancies"] and len(rep.boundary) == r["n_boundary"]
+        x = sol.values(inst)
+        pairs = [(i, j) for i in range(inst.n) for j in range(inst.n) if i != j and x[i] > x[j]]
+        cands = [P.SwapCandidate(i, j, float(x[i] - x[j])) for i, j in pairs]
+        v = is_improving_batch(inst, sol, cands)
+        np.testing.assert_array_equal(v, [bool(r["V"][i, j]) for i, j in pairs])
+        assert P.is_improving(inst, sol, cands[0]) == bool(r["V"][pairs[0]])
+        # the per-pair objectives behind the report, bit for bit
+        from paper_2508_13437_b200 import _native as N
+        import torch
+        dev = torch.device("cuda")
+        At, b, lv = inst.device_arrays(dev)
+        prob = N.Problem(inst.m, inst.n, len(inst.values), 1, At.data_ptr(), b.data_ptr(), lv.data_ptr())
+        idx = torch.from_numpy(r["idx"]).to(dev)
+        s = torch.from_numpy(sol.residual).to(dev)
+        T = torch.zeros(inst.n * inst.n, dtype=torch.float64, device=dev)
+        V = torch.zeros(inst.n * inst.n, dtype=torch.int32, device=dev)
+        N.check(N.load_library().amvm_swap_check(N.C.byref(prob), N.ptr(idx), N.ptr(s), float(sol.objective),
+                                                 N.ptr(T), N.ptr(V), N.stream_handle()), "amvm_swap_check")
+        T = T.cpu().numpy().reshape(inst.n, inst.n)
+        for i, j in pairs:
+            assert T[i, j] == r["T"][i, j], (i, j, T[i, j], r["T"][i, j])
