@@ -158,10 +158,14 @@ __global__ void __launch_bounds__(NT) k_op(KArgs a) {
 
 // compute_residual (core.py:183-197) for a batch sharing A: residual[k] =
 // A @ levels_k[idx_k] - B[k] in numpy's OpenBLAS dgemv order, objective[k] =
-// max |residual[k]|.  CTA = kRI instances x all rows; thread = rows; each A
-// element loaded once feeds kRI instances (FP64 FMA, 4 lane-accumulators per
-// output exactly as the dgemv_t 4x4 kernel).  Rows outside the 4x4 groups
-// (m % 4 != 0) and m == 1 take the scalar emulation.
+// max |residual[k]|.  CTA = kRI instances x NT rows (grid: instance groups x
+// row chunks, so a C5 shard is ~1800 CTAs and every SM stays busy); thread =
+// one row; each A element loaded once feeds kRI instances (FP64 FMA, 4
+// lane-accumulators per output exactly as the dgemv_t 4x4 kernel; the x
+// values come from shared memory as 16-byte broadcasts).  Rows outside the
+// 4x4 groups (m % 4 != 0) and m == 1 take the scalar emulation in the first
+// row chunk.  The objective is an atomicMax over the chunks on the bit
+// pattern of |v| >= 0 (obj zeroed by the caller).
 constexpr int kRI = 8;
 constexpr int kRJ = 256;
 
@@ -173,18 +177,19 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
                                                  const double *__restrict__ levels, const int32_t *__restrict__ idx,
                                                  const double *__restrict__ Xd,
                                                  double *__restrict__ res, double *__restrict__ obj) {
-  __shared__ double xs[kRI][kRJ];
+  __shared__ __align__(16) double xs[kRI][kRJ];
   __shared__ double red[kRI][NT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t k0 = (int64_t)blockIdx.x * kRI;
+  const int64_t chunk = blockIdx.y;
   const int ni = (int)(count - k0 < kRI ? count - k0 : kRI);
   const int64_t g4 = m & ~(int64_t)3, m1 = n & -4;
   double mx[kRI];
 #pragma unroll
   for (int q = 0; q < kRI; ++q) mx[q] = 0.0;
   if (m > 1) {
-    for (int64_t i0 = 0; i0 < g4; i0 += NT) {
-      const int64_t i = i0 + tid;
+    {
+      const int64_t i = chunk * NT + tid;
       double y[kRI], l[kRI][4];
 #pragma unroll
       for (int q = 0; q < kRI; ++q) {
@@ -209,10 +214,12 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
             const double a2 = __ldg(At + (j + 2) * m + i), a3 = __ldg(At + (j + 3) * m + i);
 #pragma unroll
             for (int q = 0; q < kRI; ++q) {
-              l[q][0] = amvm::dfma(a0, xs[q][jj], l[q][0]);
-              l[q][1] = amvm::dfma(a1, xs[q][jj + 1], l[q][1]);
-              l[q][2] = amvm::dfma(a2, xs[q][jj + 2], l[q][2]);
-              l[q][3] = amvm::dfma(a3, xs[q][jj + 3], l[q][3]);
+              const double2 x01 = *reinterpret_cast<const double2 *>(&xs[q][jj]);
+              const double2 x23 = *reinterpret_cast<const double2 *>(&xs[q][jj + 2]);
+              l[q][0] = amvm::dfma(a0, x01.x, l[q][0]);
+              l[q][1] = amvm::dfma(a1, x01.y, l[q][1]);
+              l[q][2] = amvm::dfma(a2, x23.x, l[q][2]);
+              l[q][3] = amvm::dfma(a3, x23.y, l[q][3]);
             }
             if (((j + 4) % 2048) == 0 || j + 4 == m1) {  // end of a dgemv_t block
 #pragma unroll
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
       }
     }
     // leftover rows (4x2 / 4x1 kernels)
-    for (int64_t i = g4 + tid; i < m; i += NT) {
+    for (int64_t i = g4 + tid; chunk == 0 && i < m; i += NT) {
       for (int q = 0; q < ni; ++q) {
         const double *lvq = levels + (k0 + q) * nlev;
         const int32_t *ix = idx + (k0 + q) * n;
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
         mx[q] = fmax(mx[q], fabs(v));
       }
     }
-  } else if (warp < ni) {  // m == 1: numpy uses ddot
+  } else if (chunk == 0 && warp < ni) {  // m == 1: numpy uses ddot
     const int q = warp;
     const double *lvq = levels + (k0 + q) * nlev;
     const int32_t *ix = idx + (k0 + q) * n;
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(NT) k_residual(int64_t m, int64_t n, int64_t n
   if (obj && tid < ni) {
     double v = 0.0;
     for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[tid][w]);
-    obj[k0 + tid] = v;
+    atomicMax(reinterpret_cast<unsigned long long *>(obj + k0 + tid), (unsigned long long)__double_as_longlong(v));
   }
 }
 
@@ -722,10 +729,13 @@ int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol, void *st
   if (!prob || !sol_ok(sol) || !prob->At || !prob->B || !prob->levels) return AMVM_ERR_INVALID;
   if (prob->m < 1 || prob->n < 1 || prob->count < 1) return AMVM_ERR_INVALID;
   const int64_t blocks = (prob->count + kRI - 1) / kRI;
-  k_residual<256><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+  const int64_t chunks = std::max<int64_t>(1, ((prob->m & ~(int64_t)3) + 255) / 256);
+  cudaError_t e = cudaMemsetAsync(sol->objective, 0, sizeof(double) * prob->count, (cudaStream_t)stream);
+  if (e != cudaSuccess) return AMVM_ERR_CUDA;
+  k_residual<256><<<dim3((unsigned)blocks, (unsigned)chunks), 256, 0, (cudaStream_t)stream>>>(
       prob->m, prob->n, prob->nlev, prob->count, prob->At, prob->B, prob->levels, sol->idx, nullptr,
       sol->residual, sol->objective);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
   e = cudaMemsetAsync(sol->updates, 0, sizeof(int32_t) * prob->count, (cudaStream_t)stream);
   return cuda_rc(e);
@@ -740,7 +750,9 @@ int amvm_ptq_prepare(int64_t m, int64_t n, int64_t count, int64_t nlev, const do
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
   const int64_t blocks = (count + kRI - 1) / kRI;
-  k_residual<256><<<(unsigned)blocks, 256, 0, st>>>(m, n, nlev, count, At, nullptr, levels, idx, W, B, nullptr);
+  const int64_t chunks = std::max<int64_t>(1, ((m & ~(int64_t)3) + 255) / 256);
+  k_residual<256><<<dim3((unsigned)blocks, (unsigned)chunks), 256, 0, st>>>(m, n, nlev, count, At, nullptr, levels,
+                                                                            idx, W, B, nullptr);
   return cuda_rc(cudaGetLastError());
 }
 

@@ -159,9 +159,15 @@ def solve_layer(X, W, bits: int = 4, cfg: SolverConfig | None = None, rows=None,
     o = lb.solve(cfg, seeds=seeds, trace=trace)
     lb.check_status()
     t1 = time.perf_counter()
-    host = {k: v.cpu().numpy() for k, v in o.items()}
+    # only what the report carries crosses PCIe; codes narrowed on the device
+    keep = ("best_objective", "initial_objective", "iterations", "moves_scored")
+    if trace:
+        keep += ("trace_current_t", "trace_best_t", "trace_pair", "trace_accepted")
+    host = {k: o[k].cpu().numpy() for k in keep}
+    code_t = torch.int8 if lb.nlev <= 128 else torch.int16
+    host["best_idx"] = o["best_idx"].to(code_t).cpu().numpy()
     rep = LayerReport(
-        rows=lb.rows, codes=host["best_idx"].astype(np.int8 if lb.nlev <= 128 else np.int16),
+        rows=lb.rows, codes=host["best_idx"],
         levels=lb.L.cpu().numpy(), objective=host["best_objective"],
         initial_objective=host["initial_objective"], iterations=host["iterations"],
         moves_scored=host["moves_scored"], seconds={"device_pipeline": t1 - t0},
