@@ -330,7 +330,9 @@ def run_amvm(args, rank, world):
                    "rows_per_gpu": hi - lo, "iters_per_row": args.iters, "m": M_CALIB, "n": D_IN,
                    "levels": 16, "parallelism": f"rows sharded over {world} GPU(s)",
                    "l2": "flushed (256 MB write) before every timed step"},
-        "gpu_launches": 2 * args.steps,  # per step: k_transpose (row-major A) + k_solve
+        # per step (ncu launch list, profiles/r01_launches.csv): k_transpose (row-major A),
+        # k_csc_count + k_csc_scan + k_csc_fill (sparse copy of A; dense X: counted, not filled), k_solve
+        "gpu_launches": 5 * args.steps,
         "roofline": roof,
         "phase_share": {nm: round(float(v / pc.sum()), 4) for nm, v in zip(names, pc)} if pc.sum() else {},
         "busy_gcycles_per_step": round(float(pc.sum()) / 1e9 / args.steps, 3),
