@@ -46,6 +46,17 @@ from .exact import (  # noqa: F401
     exhaustive_swap_check,
     is_improving,
 )
+from .formats import (  # noqa: F401
+    InstanceParseError,
+    RunArtifacts,
+    export_lp,
+    format_values,
+    instance_to_text,
+    read_instance,
+    write_instance,
+    write_run_artifacts,
+    write_solution,
+)
 from .core import (  # noqa: F401
     REFRESH_PERIOD,
     Instance,
@@ -66,4 +77,6 @@ __all__ = [
     "random_destroy", "random_repair", "removal_count", "solve", "worst_remove_destroy",
     "DEFAULT_BUDGET", "BudgetExceededError", "OracleResult", "brute_force", "MAX_SWAP_CHECK_N",
     "SwapCheckReport", "exhaustive_swap_check", "is_improving",
+    "InstanceParseError", "RunArtifacts", "export_lp", "format_values", "instance_to_text",
+    "read_instance", "write_instance", "write_run_artifacts", "write_solution",
 ]
