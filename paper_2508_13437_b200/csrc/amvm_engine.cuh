@@ -34,7 +34,10 @@ namespace amvm {
 constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
 constexpr int kCW = 16;        // one_opt window: columns per warp (window = NW * kCW)
 constexpr int kB = 8;          // one_opt second screen: flagged columns per batch
-constexpr int kG = 8;          // filter rows staged in smem per find_candidates
+#ifndef AMVM_KG
+#define AMVM_KG 8
+#endif
+constexpr int kG = AMVM_KG;    // filter rows staged in smem per find_candidates
 #ifndef AMVM_TJ
 #define AMVM_TJ (2 * AMVM_NT)
 #endif
