@@ -244,6 +244,64 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def scorer_roofline(X, dev, flush, reps: int = 10, batch: int = 512) -> dict:
+    """The standalone candidate-move scorer (amvm_score_moves, north star (c))
+    on the C5 shapes: A = X (m=2048 x n=4096), 16 levels.
+      * adjacent mode (the reference's one_opt set, |V_s| = 2), one instance,
+        L2 flushed before every launch: HBM roofline of one column stream;
+        algorithmic bytes = 8mn (A) + 8m (s) + 4n (idx) + 16n (scores).
+      * all-levels mode over a batch of rows sharing A (|V| = 16): candidate
+        moves scored per second; A is L2-resident across the batch, so this
+        leg is FP64-pipe bound (2 flops = DMUL + DADD per candidate element).
+    Times are CUDA events on the launching stream around the scorer's two
+    kernels (k_score_moves + k_score_best)."""
+    import torch
+
+    from paper_2508_13437_b200 import _native as N
+    from paper_2508_13437_b200.scoring import score_moves_device
+
+    m, n = X.shape
+    nlev = 16
+    g = torch.Generator(device="cpu").manual_seed(11)
+    At = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)
+    st = torch.cuda.current_stream()
+
+    def leg(count, mode, flush_each):
+        lv = torch.linspace(-1, 1, nlev, dtype=torch.float64).repeat(count, 1).to(dev)
+        idx = torch.randint(0, nlev, (count, n), generator=g, dtype=torch.int32).to(dev)
+        s = (torch.randn((count, m), generator=g, dtype=torch.float64) * 0.1).to(dev)
+        B = torch.zeros((count, m), dtype=torch.float64, device=dev)
+        prob = N.Problem(m, n, nlev, count, At.data_ptr(), B.data_ptr(), lv.data_ptr())
+        for _ in range(3):
+            score_moves_device(prob, idx, s, mode)
+        ms = []
+        for _ in range(reps):
+            if flush_each:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            score_moves_device(prob, idx, s, mode)
+            b.record(st)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return float(np.median(ms))
+
+    pk = peaks()
+    ms1 = leg(1, "adjacent", True)
+    alg = 8 * m * n + 8 * m + 4 * n + 16 * n
+    gbs = alg / (ms1 / 1e3) / 1e9
+    msb = leg(batch, "all", False)
+    moves = batch * n * (nlev - 1)
+    return {
+        "adjacent_single": {"ms": round(ms1, 4), "bytes": alg, "achieved_GBps": round(gbs, 1),
+                            "peak_GBps": pk["hbm_gbs"], "frac": round(gbs / pk["hbm_gbs"], 4),
+                            "moves_per_s": 2 * n / (ms1 / 1e3), "l2": "flushed before every launch"},
+        "all_levels_batch": {"rows": batch, "ms": round(msb, 3), "moves_per_s": moves / (msb / 1e3),
+                             "fp64_tflops": round(2 * batch * m * n * nlev / (msb / 1e3) / 1e12, 2)},
+        "kernel": "k_score_moves (+ k_score_best)",
+    }
+
+
 def run_amvm(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -347,6 +405,7 @@ def run_amvm(args, rank, world):
         line["cpu_baseline"].pop("moves", None)
         if not args.no_ttr:
             line["time_to_reference_linf"] = time_to_reference()
+        line["scorer"] = scorer_roofline(X, dev, flush)
     print(json.dumps(line), flush=True)
 
 

@@ -215,6 +215,21 @@ AMVM_API int amvm_is_improving(const amvm_problem *prob, const double *residual,
                                int64_t nc, const int32_t *ci, const int32_t *cj,
                                const double *cd, int32_t *verdict, void *stream);
 
+/* Batched candidate-move scoring: the one_opt candidate objective
+ * (localsearch.py:76-78) for every column and candidate level at once,
+ * for all `count` instances sharing A:
+ *   out_t[(c*n + j)*nv + v] = max_k |s_ck + (lv_c[l] - lv_c[idx_cj]) * A[k,j]|
+ * (level difference, then unfused DMUL and DADD; bitwise numpy's value).
+ * mode 0: all levels, nv = nlev, l = v (l == idx gives the objective).
+ * mode 1: adjacent levels (the reference's one_opt set), nv = 2,
+ *         l = idx-1, idx+1; +inf where that level does not exist.
+ * best[c] = flat index j*nv + v of the smallest (t, j, l) over candidates
+ * that change the level (-1 if none), best_t[c] its t.  `idx` is count x n,
+ * `residual` count x m; device pointers; replaces the Python loop of
+ * localsearch.py:70-80 for scoring (no move is applied).                   */
+AMVM_API int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual,
+                              int mode, double *out_t, int64_t *best, double *best_t, void *stream);
+
 /* exhaustive_swap_check (oracle.py:135-161): for every ordered pair with
  * x_i > x_j, out_t[i*n+j] = objective of the swapped assignment recomputed
  * from scratch in numpy's order (compute_residual, core.py:183-197) and

@@ -289,3 +289,29 @@ def brute_force(A, b, levels, prune: bool = False, chunk: int = 1 << 15):
         if t_all[k] < best_t:
             best_t, best_idx = float(t_all[k]), digits[k].astype(np.intp)
     return best_idx, best_t, total
+
+
+def score_moves(A, s, levels, idx, mode: str = "adjacent"):
+    """numpy restatement of the one_opt candidate objective
+    (/root/reference/pkg/src/dmmv/localsearch.py:76-78) for every column and
+    candidate level: t[j, v] = max|s + (lv[l] - lv[idx_j]) * A[:, j]|, the
+    same numpy expression per candidate.  Returns (t, best (j, level) | None,
+    best_t) with best = the smallest (t, j, level) over level-changing moves."""
+    A = np.asarray(A, dtype=np.float64)
+    lv = np.asarray(levels, dtype=np.float64)
+    m, n = A.shape
+    nlev = lv.size
+    nv = 2 if mode == "adjacent" else nlev
+    t = np.full((n, nv), np.inf)
+    best, best_t = None, np.inf
+    for j in range(n):
+        k = int(idx[j])
+        col = A[:, j]
+        cands = (k - 1, k + 1) if mode == "adjacent" else range(nlev)
+        for v, c in enumerate(cands):
+            if not 0 <= c < nlev:
+                continue
+            t[j, v] = float(np.max(np.abs(s + (lv[c] - lv[k]) * col)))
+            if c != k and (best is None or t[j, v] < best_t):
+                best, best_t = (j, c), t[j, v]
+    return t, best, best_t

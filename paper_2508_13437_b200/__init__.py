@@ -46,6 +46,7 @@ from .exact import (  # noqa: F401
     exhaustive_swap_check,
     is_improving,
 )
+from .scoring import MoveScores, score_moves  # noqa: F401
 from .formats import (  # noqa: F401
     InstanceParseError,
     RunArtifacts,
@@ -79,4 +80,5 @@ __all__ = [
     "SwapCheckReport", "exhaustive_swap_check", "is_improving",
     "InstanceParseError", "RunArtifacts", "export_lp", "format_values", "instance_to_text",
     "read_instance", "write_instance", "write_run_artifacts", "write_solution",
+    "MoveScores", "score_moves",
 ]

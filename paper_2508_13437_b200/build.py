@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libamvm.so")
-SOURCES = ["amvm.cu", "amvm_engine.cuh", "amvm_device.cuh", "amvm_exact.cuh", "amvm_lsq.cuh", "amvm_tomo.cuh"]
+SOURCES = ["amvm.cu", "amvm_engine.cuh", "amvm_device.cuh", "amvm_exact.cuh", "amvm_lsq.cuh", "amvm_tomo.cuh", "amvm_score.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

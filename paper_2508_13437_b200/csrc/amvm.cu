@@ -12,6 +12,7 @@
 #include "amvm_engine.cuh"
 #include "amvm_exact.cuh"
 #include "amvm_lsq.cuh"
+#include "amvm_score.cuh"
 #include "amvm_tomo.cuh"
 
 using namespace amvm;
@@ -963,6 +964,24 @@ int amvm_swap_check(const amvm_problem *prob, const int32_t *idx, const double *
   if (prob->n > 4096) return AMVM_ERR_UNSUPPORTED;
   k_swap_check<<<(unsigned)(prob->n * prob->n), 256, 0, (cudaStream_t)stream>>>(
       prob->m, prob->n, prob->At, prob->B, prob->levels, idx, residual, objective, out_t, out_v);
+  return cuda_rc(cudaGetLastError());
+}
+
+int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual, int mode,
+                     double *out_t, int64_t *best, double *best_t, void *stream) {
+  if (!prob || !prob->At || !prob->levels || !idx || !residual || !out_t || !best || !best_t) return AMVM_ERR_INVALID;
+  if (prob->m < 1 || prob->n < 1 || prob->nlev < 1 || prob->count < 1 || (mode != 0 && mode != 1))
+    return AMVM_ERR_INVALID;
+  if (prob->count > 65535) return AMVM_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)((prob->n + kScoreWarps - 1) / kScoreWarps), (unsigned)prob->count);
+  if (mode == 1)
+    k_score_moves<1><<<grid, 32 * kScoreWarps, 0, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At,
+                                                        prob->levels, idx, residual, out_t);
+  else
+    k_score_moves<0><<<grid, 32 * kScoreWarps, 0, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At,
+                                                        prob->levels, idx, residual, out_t);
+  k_score_best<<<(unsigned)prob->count, 256, 0, st>>>(prob->n, prob->nlev, prob->count, idx, mode, out_t, best, best_t);
   return cuda_rc(cudaGetLastError());
 }
 

@@ -1,0 +1,10 @@
+"""Launch the candidate-move scorer once per mode on the C5 shapes (for ncu)."""
+import numpy as np
+import torch
+
+import bench
+
+X, _ = bench.layer_rows(0, 1)
+dev = torch.device("cuda", 0)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+print(bench.scorer_roofline(X, dev, flush, reps=1, batch=64))
