@@ -272,15 +272,17 @@ def scorer_roofline(X, dev, flush, reps: int = 10, batch: int = 512) -> dict:
         s = (torch.randn((count, m), generator=g, dtype=torch.float64) * 0.1).to(dev)
         B = torch.zeros((count, m), dtype=torch.float64, device=dev)
         prob = N.Problem(m, n, nlev, count, At.data_ptr(), B.data_ptr(), lv.data_ptr())
+        ws = torch.empty(int(N.load_library().amvm_score_workspace_bytes(N.C.byref(prob))), dtype=torch.uint8,
+                         device=dev)
         for _ in range(3):
-            score_moves_device(prob, idx, s, mode)
+            score_moves_device(prob, idx, s, mode, ws)
         ms = []
         for _ in range(reps):
             if flush_each:
                 flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            score_moves_device(prob, idx, s, mode)
+            score_moves_device(prob, idx, s, mode, ws)
             b.record(st)
             torch.cuda.synchronize()
             ms.append(a.elapsed_time(b))

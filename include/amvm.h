@@ -226,9 +226,12 @@ AMVM_API int amvm_is_improving(const amvm_problem *prob, const double *residual,
  * best[c] = flat index j*nv + v of the smallest (t, j, l) over candidates
  * that change the level (-1 if none), best_t[c] its t.  `idx` is count x n,
  * `residual` count x m; device pointers; replaces the Python loop of
- * localsearch.py:70-80 for scoring (no move is applied).                   */
+ * localsearch.py:70-80 for scoring (no move is applied).  Workspace (8-byte
+ * aligned) of amvm_score_workspace_bytes(prob): per-column bests.          */
+AMVM_API size_t amvm_score_workspace_bytes(const amvm_problem *prob);
 AMVM_API int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual,
-                              int mode, double *out_t, int64_t *best, double *best_t, void *stream);
+                              int mode, double *out_t, int64_t *best, double *best_t,
+                              void *ws, size_t ws_bytes, void *stream);
 
 /* exhaustive_swap_check (oracle.py:135-161): for every ordered pair with
  * x_i > x_j, out_t[i*n+j] = objective of the swapped assignment recomputed

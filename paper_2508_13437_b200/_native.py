@@ -26,7 +26,7 @@ EXPORTS = (
     "amvm_ls_start_workspace_bytes", "amvm_ls_start",
     "amvm_projector_workspace_bytes", "amvm_projector_indptr", "amvm_projector_fill",
     "amvm_csr_gemv", "amvm_sirt_workspace_bytes", "amvm_sirt", "amvm_is_improving", "amvm_swap_check",
-    "amvm_score_moves",
+    "amvm_score_moves", "amvm_score_workspace_bytes",
 )
 
 
@@ -108,7 +108,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_projector_fill.argtypes = [i64, i64, vp, vp, vp, vp, vp]
     lib.amvm_is_improving.argtypes = [vp, vp, C.c_double, i64, vp, vp, vp, vp, vp]
     lib.amvm_swap_check.argtypes = [vp, vp, vp, C.c_double, vp, vp, vp]
-    lib.amvm_score_moves.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, vp]
+    lib.amvm_score_moves.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, vp, sz, vp]
+    lib.amvm_score_workspace_bytes.argtypes = [vp]
+    lib.amvm_score_workspace_bytes.restype = sz
     lib.amvm_csr_gemv.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
     lib.amvm_sirt_workspace_bytes.restype = sz
     lib.amvm_sirt_workspace_bytes.argtypes = [i64, i64, i64, i64]

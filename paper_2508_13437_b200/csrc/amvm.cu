@@ -967,21 +967,35 @@ int amvm_swap_check(const amvm_problem *prob, const int32_t *idx, const double *
   return cuda_rc(cudaGetLastError());
 }
 
+size_t amvm_score_workspace_bytes(const amvm_problem *prob) {
+  if (!prob || prob->n < 1 || prob->count < 1) return 0;
+  const size_t nblk = (size_t)((prob->n + kScoreWarps - 1) / kScoreWarps);
+  return (size_t)prob->count * (nblk * 16 + 4) + 16;
+}
+
 int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual, int mode,
-                     double *out_t, int64_t *best, double *best_t, void *stream) {
+                     double *out_t, int64_t *best, double *best_t, void *ws, size_t ws_bytes, void *stream) {
   if (!prob || !prob->At || !prob->levels || !idx || !residual || !out_t || !best || !best_t) return AMVM_ERR_INVALID;
   if (prob->m < 1 || prob->n < 1 || prob->nlev < 1 || prob->count < 1 || (mode != 0 && mode != 1))
     return AMVM_ERR_INVALID;
-  if (prob->count > 65535) return AMVM_ERR_UNSUPPORTED;
+  if (prob->count > 65535 || (prob->n + kScoreWarps - 1) / kScoreWarps > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < amvm_score_workspace_bytes(prob) || ((uintptr_t)ws & 7)) return AMVM_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  const dim3 grid((unsigned)((prob->n + kScoreWarps - 1) / kScoreWarps), (unsigned)prob->count);
+  // workspace: per-CTA bests (t, flat) and one ticket counter per instance
+  const int64_t nblk = (prob->n + kScoreWarps - 1) / kScoreWarps;
+  double *blk_t = (double *)ws;
+  int64_t *blk_i = (int64_t *)(blk_t + prob->count * nblk);
+  unsigned *done = (unsigned *)(blk_i + prob->count * nblk);
+  if (cudaMemsetAsync(done, 0, (size_t)prob->count * 4, st) != cudaSuccess) return AMVM_ERR_CUDA;
+  const dim3 grid((unsigned)nblk, (unsigned)prob->count);
   if (mode == 1)
     k_score_moves<1><<<grid, 32 * kScoreWarps, 0, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At,
-                                                        prob->levels, idx, residual, out_t);
+                                                        prob->levels, idx, residual, out_t, blk_t, blk_i, done,
+                                                        best, best_t);
   else
     k_score_moves<0><<<grid, 32 * kScoreWarps, 0, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At,
-                                                        prob->levels, idx, residual, out_t);
-  k_score_best<<<(unsigned)prob->count, 256, 0, st>>>(prob->n, prob->nlev, prob->count, idx, mode, out_t, best, best_t);
+                                                        prob->levels, idx, residual, out_t, blk_t, blk_i, done,
+                                                        best, best_t);
   return cuda_rc(cudaGetLastError());
 }
 

@@ -24,111 +24,139 @@ namespace amvm {
 constexpr int kScoreVC = 16;      // candidates per pass over a column
 constexpr int kScoreWarps = 8;    // columns per CTA
 
-// mode 0: all levels (nv = nlev, candidate v = level v; v == idx gives the
-// current objective).  mode 1: adjacent levels (nv = 2: idx - 1, idx + 1;
-// +inf where the level does not exist).
-template <int MODE>
-__global__ void __launch_bounds__(256) k_score_moves(int64_t m, int64_t n, int64_t nlev, int64_t count,
-                                                     const double *__restrict__ At, const double *__restrict__ lvs,
-                                                     const int32_t *__restrict__ idxs, const double *__restrict__ S,
-                                                     double *__restrict__ out_t) {
-  constexpr int mode = MODE;
-  constexpr int VC = MODE == 1 ? 2 : kScoreVC;
-  constexpr int kScoreUnroll = MODE == 1 ? 8 : 2;  // rows in flight per lane
-  const int lane = threadIdx.x & 31;
-  const int64_t col = (int64_t)blockIdx.x * kScoreWarps + (threadIdx.x >> 5);
-  const int64_t c = blockIdx.y;
-  if (col >= n || c >= count) return;
-  const double *lv = lvs + c * nlev;
-  const double *s = S + c * m;
-  const double *a = At + col * m;
-  const int k = idxs[c * n + col];
-  const int64_t nv = mode == 1 ? 2 : nlev;
-  double *out = out_t + (c * n + col) * nv;
-  for (int64_t v0 = 0; v0 < nv; v0 += VC) {
-    double d[VC], mx[VC];
-    bool live[VC];
-#pragma unroll
-    for (int u = 0; u < VC; ++u) {
-      const int64_t lvl = mode == 1 ? (int64_t)k + (u == 0 ? -1 : 1) : v0 + u;
-      live[u] = (mode == 1 ? u < 2 : v0 + u < nv) && lvl >= 0 && lvl < nlev;
-      d[u] = live[u] ? __dsub_rn(lv[lvl], lv[k]) : 0.0;
-      mx[u] = 0.0;
-    }
-    int64_t r = lane;
-    for (; r + 32 * (kScoreUnroll - 1) < m; r += 32 * kScoreUnroll) {
-      double av[kScoreUnroll], sv[kScoreUnroll];
-#pragma unroll
-      for (int q = 0; q < kScoreUnroll; ++q) {
-        av[q] = __ldg(a + r + 32 * q);
-        sv[q] = __ldg(s + r + 32 * q);
-      }
-#pragma unroll
-      for (int q = 0; q < kScoreUnroll; ++q)
-#pragma unroll
-        for (int u = 0; u < VC; ++u)
-          if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv[q], __dmul_rn(d[u], av[q]))));
-    }
-    for (; r < m; r += 32) {
-      const double av = __ldg(a + r), sv = __ldg(s + r);
-#pragma unroll
-      for (int u = 0; u < VC; ++u)
-        if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv, __dmul_rn(d[u], av))));
-    }
-#pragma unroll
-    for (int u = 0; u < VC; ++u) {
-      if (mode == 1 && u >= 2) break;
-      double x = mx[u];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
-      if (lane == u && (mode == 1 || v0 + u < nv)) out[v0 + u] = live[u] ? x : __longlong_as_double(0x7ff0000000000000LL);
-    }
-    if (mode == 1) break;
-  }
+// lexicographic (t, flat) order with -1 = no candidate (worst)
+__device__ __forceinline__ bool score_better(double xa, int64_t ia, double xb, int64_t ib) {
+  if (ib < 0) return true;
+  if (ia < 0) return false;
+  return xa < xb || (xa == xb && ia < ib);
 }
 
-// Best move per instance: the lexicographically smallest (t, j, level) over
-// candidates that change the level (level != idx_j, level exists), as one
-// CTA per instance.  best[c] = j * nv + v (flat index into out_t), -1 if the
-// instance has no candidate; best_t[c] = its objective.
-__global__ void __launch_bounds__(256) k_score_best(int64_t n, int64_t nlev, int64_t count,
-                                                    const int32_t *__restrict__ idxs, int mode,
-                                                    const double *__restrict__ out_t, int64_t *__restrict__ best,
-                                                    double *__restrict__ best_t) {
-  __shared__ double st[8];
-  __shared__ int64_t si[8];
-  const int64_t c = blockIdx.x;
-  if (c >= count) return;
-  const int64_t nv = mode == 1 ? 2 : nlev;
-  const double *t = out_t + c * n * nv;
-  const int32_t *idx = idxs + c * n;
-  double bt = __longlong_as_double(0x7ff0000000000000LL);
-  int64_t bi = -1;
-  for (int64_t e = threadIdx.x; e < n * nv; e += blockDim.x) {
-    const int64_t j = e / nv, v = e - j * nv;
-    const int64_t lvl = mode == 1 ? (int64_t)idx[j] + (v == 0 ? -1 : 1) : v;
-    if (lvl < 0 || lvl >= nlev || lvl == idx[j]) continue;
-    const double x = t[e];
-    if (bi < 0 || x < bt) { bt = x; bi = e; }  // e ascends per thread: first wins ties
-  }
-  auto better = [](double xa, int64_t ia, double xb, int64_t ib) {
-    if (ib < 0) return true;
-    if (ia < 0) return false;
-    return xa < xb || (xa == xb && ia < ib);
-  };
+__device__ __forceinline__ void score_warp_best(double &bt, int64_t &bi) {
+#pragma unroll
   for (int o = 16; o; o >>= 1) {
     const double ox = __shfl_xor_sync(0xffffffffu, bt, o);
     const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (!better(bt, bi, ox, oi)) { bt = ox; bi = oi; }
+    if (!score_better(bt, bi, ox, oi)) { bt = ox; bi = oi; }
   }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) { st[w] = bt; si[w] = bi; }
+}
+
+// MODE 0: all levels (nv = nlev, candidate v = level v; v == idx gives the
+// current objective).  MODE 1: adjacent levels (nv = 2: idx - 1, idx + 1;
+// +inf where the level does not exist).  Grid (n / kScoreWarps, count).
+// Best move per instance, fused: the lexicographically smallest (t, j, level)
+// over candidates that change the level, per warp, per CTA (slot in the
+// workspace), then by the instance's last CTA to finish (ticket counter,
+// reset for the next call).  best[c] = j * nv + v (flat index into out_t),
+// -1 if the instance has no candidate; best_t[c] = its objective.
+template <int MODE>
+__global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t m, int64_t n, int64_t nlev, int64_t count,
+                                                     const double *__restrict__ At, const double *__restrict__ lvs,
+                                                     const int32_t *__restrict__ idxs, const double *__restrict__ S,
+                                                     double *__restrict__ out_t, double *__restrict__ blk_t,
+                                                     int64_t *__restrict__ blk_i, unsigned *__restrict__ done,
+                                                     int64_t *__restrict__ best, double *__restrict__ best_t) {
+  constexpr int mode = MODE;
+  constexpr int VC = MODE == 1 ? 2 : kScoreVC;
+  constexpr int kScoreUnroll = MODE == 1 ? 8 : 2;  // rows in flight per lane
+  __shared__ double sbt[kScoreWarps];
+  __shared__ int64_t sbi[kScoreWarps];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t col = (int64_t)blockIdx.x * kScoreWarps + w;
+  const int64_t c = blockIdx.y;
+  const int64_t nv = mode == 1 ? 2 : nlev;
+  // this column's smallest (t, level) over level-changing candidates (every
+  // lane holds every reduced max, so every lane tracks it redundantly)
+  double cbt = 0.0;
+  int32_t cbv = -1;
+  if (col < n) {
+    const double *lv = lvs + c * nlev;
+    const double *s = S + c * m;
+    const double *a = At + col * m;
+    const int k = idxs[c * n + col];
+    double *out = out_t + (c * n + col) * nv;
+    for (int64_t v0 = 0; v0 < nv; v0 += VC) {
+      double d[VC], mx[VC];
+      // candidate u of this pass: its level, and whether that level exists
+      auto cand = [&](int u, int64_t &lvl) {
+        lvl = mode == 1 ? (int64_t)k + (u == 0 ? -1 : 1) : v0 + u;
+        return (mode == 1 ? u < 2 : v0 + u < nv) && lvl >= 0 && lvl < nlev;
+      };
+#pragma unroll
+      for (int u = 0; u < VC; ++u) {
+        int64_t lvl;
+        d[u] = cand(u, lvl) ? __dsub_rn(lv[lvl], lv[k]) : 0.0;
+        mx[u] = 0.0;
+      }
+      int64_t r = lane;
+      for (; r + 32 * (kScoreUnroll - 1) < m; r += 32 * kScoreUnroll) {
+        double av[kScoreUnroll], sv[kScoreUnroll];
+#pragma unroll
+        for (int q = 0; q < kScoreUnroll; ++q) {
+          av[q] = __ldg(a + r + 32 * q);
+          sv[q] = __ldg(s + r + 32 * q);
+        }
+#pragma unroll
+        for (int q = 0; q < kScoreUnroll; ++q)
+#pragma unroll
+          for (int u = 0; u < VC; ++u)
+            if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv[q], __dmul_rn(d[u], av[q]))));
+      }
+      for (; r < m; r += 32) {
+        const double av = __ldg(a + r), sv = __ldg(s + r);
+#pragma unroll
+        for (int u = 0; u < VC; ++u)
+          if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv, __dmul_rn(d[u], av))));
+      }
+#pragma unroll
+      for (int u = 0; u < VC; ++u) {
+        if (mode == 1 && u >= 2) break;
+        double x = mx[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+        int64_t lvl;
+        const bool live = cand(u, lvl);
+        if (lane == u && (mode == 1 || v0 + u < nv)) out[v0 + u] = live ? x : __longlong_as_double(0x7ff0000000000000LL);
+        const bool moves = live && lvl != k;
+        if (moves && (cbv < 0 || x < cbt)) { cbt = x; cbv = (int32_t)(v0 + u); }
+      }
+      if (mode == 1) break;
+    }
+  }
+  // CTA best -> per-CTA slot; the last CTA of the instance reduces the slots
+  double bt = cbt;
+  int64_t bi = cbv < 0 ? -1 : col * nv + cbv;
+  if (lane == 0) { sbt[w] = bt; sbi[w] = bi; }
+  __syncthreads();
+  const int64_t nblk = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < kScoreWarps; ++q)
+      if (!score_better(bt, bi, sbt[q], sbi[q])) { bt = sbt[q]; bi = sbi[q]; }
+    blk_t[c * nblk + blockIdx.x] = bt;
+    blk_i[c * nblk + blockIdx.x] = bi;
+    __threadfence();
+    last = atomicAdd(&done[c], 1u) == (unsigned)(nblk - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  bt = 0.0;
+  bi = -1;
+  for (int64_t e = threadIdx.x; e < nblk; e += blockDim.x) {
+    const double x = __ldcg(blk_t + c * nblk + e);
+    const int64_t i = __ldcg(blk_i + c * nblk + e);
+    if (score_better(x, i, bt, bi)) { bt = x; bi = i; }
+  }
+  score_warp_best(bt, bi);
+  __syncthreads();
+  if (lane == 0) { sbt[w] = bt; sbi[w] = bi; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
-      if (!better(bt, bi, st[q], si[q])) { bt = st[q]; bi = si[q]; }
+    for (int q = 1; q < kScoreWarps; ++q)
+      if (!score_better(bt, bi, sbt[q], sbi[q])) { bt = sbt[q]; bi = sbi[q]; }
     best[c] = bi;
-    best_t[c] = bt;
+    best_t[c] = bi < 0 ? __longlong_as_double(0x7ff0000000000000LL) : bt;
+    done[c] = 0u;  // ready for the next call on this workspace
   }
 }
 

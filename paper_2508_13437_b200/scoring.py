@@ -43,11 +43,13 @@ class MoveScores:
     improving: bool
 
 
-def score_moves_device(prob: "N.Problem", idx, residual, mode: str = "adjacent"):
+def score_moves_device(prob: "N.Problem", idx, residual, mode: str = "adjacent", ws=None):
     """Device-tensor form for batches sharing A (``prob.count`` instances):
     idx int32 [count, n], residual float64 [count, m] -> (t [count, n, nv],
     best flat index int64 [count], best_t float64 [count]), all on device,
-    asynchronous on the current stream."""
+    asynchronous on the current stream.  ``ws``: optional uint8 device
+    workspace of at least ``amvm_score_workspace_bytes`` (allocated if
+    absent or short)."""
     torch = N.torch_cuda()
     lib = N.load_library()
     if mode not in MODES:
@@ -57,8 +59,12 @@ def score_moves_device(prob: "N.Problem", idx, residual, mode: str = "adjacent")
     t = torch.empty((int(prob.count), int(prob.n), nv), dtype=torch.float64, device=dev)
     best = torch.empty(int(prob.count), dtype=torch.int64, device=dev)
     best_t = torch.empty(int(prob.count), dtype=torch.float64, device=dev)
+    wsb = int(lib.amvm_score_workspace_bytes(N.C.byref(prob)))
+    if ws is None or ws.numel() < wsb:
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     N.check(lib.amvm_score_moves(N.C.byref(prob), N.ptr(idx), N.ptr(residual), MODES[mode], N.ptr(t),
-                                 N.ptr(best), N.ptr(best_t), N.stream_handle()), "amvm_score_moves")
+                                 N.ptr(best), N.ptr(best_t), N.ptr(ws), ws.numel(), N.stream_handle()),
+            "amvm_score_moves")
     return t, best, best_t
 
 

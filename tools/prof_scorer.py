@@ -1,8 +1,12 @@
 """Launch the candidate-move scorer once per mode on the C5 shapes (for ncu)."""
-import numpy as np
+import os
+import sys
+
 import torch
 
-import bench
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import bench  # noqa: E402
 
 X, _ = bench.layer_rows(0, 1)
 dev = torch.device("cuda", 0)
