@@ -969,7 +969,8 @@ int amvm_swap_check(const amvm_problem *prob, const int32_t *idx, const double *
 
 size_t amvm_score_workspace_bytes(const amvm_problem *prob) {
   if (!prob || prob->n < 1 || prob->count < 1) return 0;
-  const size_t nblk = (size_t)((prob->n + kScoreWarps - 1) / kScoreWarps);
+  const int cpb = score_cols_per_cta(1) < score_cols_per_cta(0) ? score_cols_per_cta(1) : score_cols_per_cta(0);
+  const size_t nblk = (size_t)((prob->n + cpb - 1) / cpb);  // the larger grid of the two modes
   return (size_t)prob->count * (nblk * 16 + 4) + 16;
 }
 
@@ -978,11 +979,12 @@ int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double 
   if (!prob || !prob->At || !prob->levels || !idx || !residual || !out_t || !best || !best_t) return AMVM_ERR_INVALID;
   if (prob->m < 1 || prob->n < 1 || prob->nlev < 1 || prob->count < 1 || (mode != 0 && mode != 1))
     return AMVM_ERR_INVALID;
-  if (prob->count > 65535 || (prob->n + kScoreWarps - 1) / kScoreWarps > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
+  const int cpb = score_cols_per_cta(mode);
+  if (prob->count > 65535 || (prob->n + cpb - 1) / cpb > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
   if (!ws || ws_bytes < amvm_score_workspace_bytes(prob) || ((uintptr_t)ws & 7)) return AMVM_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   // workspace: per-CTA bests (t, flat) and one ticket counter per instance
-  const int64_t nblk = (prob->n + kScoreWarps - 1) / kScoreWarps;
+  const int64_t nblk = (prob->n + cpb - 1) / cpb;
   double *blk_t = (double *)ws;
   int64_t *blk_i = (int64_t *)(blk_t + prob->count * nblk);
   unsigned *done = (unsigned *)(blk_i + prob->count * nblk);

@@ -22,7 +22,12 @@
 namespace amvm {
 
 constexpr int kScoreVC = 16;      // candidates per pass over a column
-constexpr int kScoreWarps = 8;    // columns per CTA
+constexpr int kScoreWarps = 8;    // warps per CTA
+// warps per column: the adjacent set streams each column with 4 warps (one
+// instance has too few columns to fill 148 SMs with a warp per column); all
+// levels keep one warp per column (FP64-bound, batches fill the GPU)
+__host__ __device__ constexpr int score_row_split(int mode) { return mode == 1 ? 4 : 1; }
+__host__ __device__ constexpr int score_cols_per_cta(int mode) { return kScoreWarps / score_row_split(mode); }
 
 // lexicographic (t, flat) order with -1 = no candidate (worst)
 __device__ __forceinline__ bool score_better(double xa, int64_t ia, double xb, int64_t ib) {
@@ -58,11 +63,14 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
   constexpr int mode = MODE;
   constexpr int VC = MODE == 1 ? 2 : kScoreVC;
   constexpr int kScoreUnroll = MODE == 1 ? 8 : 2;  // rows in flight per lane
+  constexpr int RS = score_row_split(MODE), CPB = score_cols_per_cta(MODE);
   __shared__ double sbt[kScoreWarps];
   __shared__ int64_t sbi[kScoreWarps];
+  __shared__ double smx[kScoreWarps][2];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t col = (int64_t)blockIdx.x * kScoreWarps + w;
+  const int part = w % RS;  // this warp's share of the column's rows
+  const int64_t col = (int64_t)blockIdx.x * CPB + w / RS;
   const int64_t c = blockIdx.y;
   const int64_t nv = mode == 1 ? 2 : nlev;
   // this column's smallest (t, level) over level-changing candidates (every
@@ -88,13 +96,13 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
         d[u] = cand(u, lvl) ? __dsub_rn(lv[lvl], lv[k]) : 0.0;
         mx[u] = 0.0;
       }
-      int64_t r = lane;
-      for (; r + 32 * (kScoreUnroll - 1) < m; r += 32 * kScoreUnroll) {
+      int64_t r = 32 * part + lane;
+      for (; r + 32 * RS * (kScoreUnroll - 1) < m; r += 32 * RS * kScoreUnroll) {
         double av[kScoreUnroll], sv[kScoreUnroll];
 #pragma unroll
         for (int q = 0; q < kScoreUnroll; ++q) {
-          av[q] = __ldg(a + r + 32 * q);
-          sv[q] = __ldg(s + r + 32 * q);
+          av[q] = __ldg(a + r + 32 * RS * q);
+          sv[q] = __ldg(s + r + 32 * RS * q);
         }
 #pragma unroll
         for (int q = 0; q < kScoreUnroll; ++q)
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
           for (int u = 0; u < VC; ++u)
             if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv[q], __dmul_rn(d[u], av[q]))));
       }
-      for (; r < m; r += 32) {
+      for (; r < m; r += 32 * RS) {
         const double av = __ldg(a + r), sv = __ldg(s + r);
 #pragma unroll
         for (int u = 0; u < VC; ++u)
@@ -114,6 +122,10 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
         double x = mx[u];
 #pragma unroll
         for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+        if (RS > 1) {  // combined across the column's warps below
+          if (lane == 0) smx[w][u] = x;
+          continue;
+        }
         int64_t lvl;
         const bool live = cand(u, lvl);
         if (lane == u && (mode == 1 || v0 + u < nv)) out[v0 + u] = live ? x : __longlong_as_double(0x7ff0000000000000LL);
@@ -121,6 +133,22 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
         if (moves && (cbv < 0 || x < cbt)) { cbt = x; cbv = (int32_t)(v0 + u); }
       }
       if (mode == 1) break;
+    }
+  }
+  if (RS > 1) {
+    __syncthreads();
+    if (col < n && part == 0) {
+      const int k = idxs[c * n + col];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double x = smx[w][u];
+#pragma unroll
+        for (int p = 1; p < RS; ++p) x = fmax(x, smx[w + p][u]);
+        const int64_t lvl = (int64_t)k + (u == 0 ? -1 : 1);
+        const bool live = lvl >= 0 && lvl < nlev;
+        if (lane == u) out_t[(c * n + col) * 2 + u] = live ? x : __longlong_as_double(0x7ff0000000000000LL);
+        if (live && (cbv < 0 || x < cbt)) { cbt = x; cbv = u; }
+      }
     }
   }
   // CTA best -> per-CTA slot; the last CTA of the instance reduces the slots
