@@ -253,8 +253,8 @@ def scorer_roofline(X, dev, flush, reps: int = 10, batch: int = 512) -> dict:
       * all-levels mode over a batch of rows sharing A (|V| = 16): candidate
         moves scored per second; A is L2-resident across the batch, so this
         leg is FP64-pipe bound (2 flops = DMUL + DADD per candidate element).
-    Times are CUDA events on the launching stream around the scorer's two
-    kernels (k_score_moves + k_score_best)."""
+    Times are CUDA events on the launching stream around the scorer call
+    (ticket-counter memset + k_score_moves with the fused best-move reduction)."""
     import torch
 
     from paper_2508_13437_b200 import _native as N
@@ -300,7 +300,7 @@ def scorer_roofline(X, dev, flush, reps: int = 10, batch: int = 512) -> dict:
                             "moves_per_s": 2 * n / (ms1 / 1e3), "l2": "flushed before every launch"},
         "all_levels_batch": {"rows": batch, "ms": round(msb, 3), "moves_per_s": moves / (msb / 1e3),
                              "fp64_tflops": round(2 * batch * m * n * nlev / (msb / 1e3) / 1e12, 2)},
-        "kernel": "k_score_moves (+ k_score_best)",
+        "kernel": "k_score_moves (best move fused; + a 4-byte-per-instance memset)",
     }
 
 

@@ -23,10 +23,13 @@ namespace amvm {
 
 constexpr int kScoreVC = 16;      // candidates per pass over a column
 constexpr int kScoreWarps = 8;    // warps per CTA
-// warps per column: the adjacent set streams each column with 4 warps (one
-// instance has too few columns to fill 148 SMs with a warp per column); all
-// levels keep one warp per column (FP64-bound, batches fill the GPU)
-__host__ __device__ constexpr int score_row_split(int mode) { return mode == 1 ? 4 : 1; }
+// warps per column (rows split across them, maxima combined in smem).  ncu on
+// one C5 instance (adjacent set): 1 warp/column 26 us, 4 warps/column 30 us
+// (shorter-lived CTAs, register-limited occupancy), so 1 ships; kept as a knob
+#ifndef AMVM_SCORE_ROW_SPLIT
+#define AMVM_SCORE_ROW_SPLIT 1
+#endif
+__host__ __device__ constexpr int score_row_split(int mode) { return mode == 1 ? AMVM_SCORE_ROW_SPLIT : 1; }
 __host__ __device__ constexpr int score_cols_per_cta(int mode) { return kScoreWarps / score_row_split(mode); }
 
 // lexicographic (t, flat) order with -1 = no candidate (worst)
