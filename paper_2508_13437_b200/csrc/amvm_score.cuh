@@ -32,6 +32,14 @@ constexpr int kScoreWarps = 8;    // warps per CTA
 __host__ __device__ constexpr int score_row_split(int mode) { return mode == 1 ? AMVM_SCORE_ROW_SPLIT : 1; }
 __host__ __device__ constexpr int score_cols_per_cta(int mode) { return kScoreWarps / score_row_split(mode); }
 
+// running max of |y| as compare + select: DSETP + DADD(|y|) + 2 FSEL, where
+// fmax lowers to DSETP.MAX + SEL + FSEL + register moves; same value (no NaN
+// reaches the scorer: Instance validates finiteness)
+__device__ __forceinline__ double score_amax(double m, double y) {
+  const double ay = fabs(y);
+  return ay > m ? ay : m;
+}
+
 // lexicographic (t, flat) order with -1 = no candidate (worst)
 __device__ __forceinline__ bool score_better(double xa, int64_t ia, double xb, int64_t ib) {
   if (ib < 0) return true;
@@ -111,13 +119,13 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
         for (int q = 0; q < kScoreUnroll; ++q)
 #pragma unroll
           for (int u = 0; u < VC; ++u)
-            if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv[q], __dmul_rn(d[u], av[q]))));
+            if (mode != 1 || u < 2) mx[u] = score_amax(mx[u], __dadd_rn(sv[q], __dmul_rn(d[u], av[q])));
       }
       for (; r < m; r += 32 * RS) {
         const double av = __ldg(a + r), sv = __ldg(s + r);
 #pragma unroll
         for (int u = 0; u < VC; ++u)
-          if (mode != 1 || u < 2) mx[u] = fmax(mx[u], fabs(__dadd_rn(sv, __dmul_rn(d[u], av))));
+          if (mode != 1 || u < 2) mx[u] = score_amax(mx[u], __dadd_rn(sv, __dmul_rn(d[u], av)));
       }
 #pragma unroll
       for (int u = 0; u < VC; ++u) {
