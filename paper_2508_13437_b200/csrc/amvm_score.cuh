@@ -26,6 +26,9 @@ constexpr int kScoreWarps = 8;    // warps per CTA
 // warps per column (rows split across them, maxima combined in smem).  ncu on
 // one C5 instance (adjacent set): 1 warp/column 26 us, 4 warps/column 30 us
 // (shorter-lived CTAs, register-limited occupancy), so 1 ships; kept as a knob
+#ifndef AMVM_SCORE_UNROLL
+#define AMVM_SCORE_UNROLL 16  // adjacent set: rows in flight per lane (A/B: 16 beats 8 by ~5 %)
+#endif
 #ifndef AMVM_SCORE_ROW_SPLIT
 #define AMVM_SCORE_ROW_SPLIT 1
 #endif
@@ -65,7 +68,7 @@ __device__ __forceinline__ void score_warp_best(double &bt, int64_t &bi) {
 // reset for the next call).  best[c] = j * nv + v (flat index into out_t),
 // -1 if the instance has no candidate; best_t[c] = its objective.
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t m, int64_t n, int64_t nlev, int64_t count,
+__global__ void __launch_bounds__(256, MODE == 1 ? (AMVM_SCORE_UNROLL > 8 ? 2 : 3) : 2) k_score_moves(int64_t m, int64_t n, int64_t nlev, int64_t count,
                                                      const double *__restrict__ At, const double *__restrict__ lvs,
                                                      const int32_t *__restrict__ idxs, const double *__restrict__ S,
                                                      double *__restrict__ out_t, double *__restrict__ blk_t,
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_score_moves(int64_t 
                                                      int64_t *__restrict__ best, double *__restrict__ best_t) {
   constexpr int mode = MODE;
   constexpr int VC = MODE == 1 ? 2 : kScoreVC;
-  constexpr int kScoreUnroll = MODE == 1 ? 8 : 2;  // rows in flight per lane
+  constexpr int kScoreUnroll = MODE == 1 ? AMVM_SCORE_UNROLL : 2;  // rows in flight per lane
   constexpr int RS = score_row_split(MODE), CPB = score_cols_per_cta(MODE);
   __shared__ double sbt[kScoreWarps];
   __shared__ int64_t sbi[kScoreWarps];
