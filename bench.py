@@ -48,8 +48,12 @@ def parse():
     ap.add_argument("--impl", default="amvm", choices=["amvm", "reference"])
     ap.add_argument("--rows", type=int, default=D_OUT // 8,
                     help="rows of the layer per GPU per step (default 1792: the whole layer at 8 GPUs)")
-    ap.add_argument("--iters", type=int, default=2, help="ALNS iterations per row per step")
+    ap.add_argument("--iters", type=int, default=100,
+                    help="ALNS iterations per row per step (SURVEY.md §8d: 100 per row)")
     ap.add_argument("--cpu-rows", type=int, default=16, help="rows in the CPU baseline sample")
+    ap.add_argument("--cpu-iters", type=int, default=2,
+                    help="ALNS iterations per row in the CPU sample (a bounded sample: the port runs "
+                         "~5 s per C5 row-iteration per core)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttr", action="store_true", help="skip the wall-time-to-reference-l_inf leg")
     return ap.parse_args()
@@ -105,6 +109,9 @@ class Clocks:
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "amvm":
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))  # before NCCL init
     if world > 1:
         import torch.distributed as dist
         backend = "nccl" if args.impl == "amvm" else "gloo"
@@ -120,21 +127,35 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic(rows: int, iters: int):
-    """DRAM bytes (read + write) of one k_solve launch of this workload, from
-    the committed `ncu --set full` capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ksolve_traffic.json")
+def ncu_traffic():
+    """DRAM bytes (read + write) per row-iteration of k_solve on this workload,
+    from the committed ncu capture (profiles/r02_ksolve_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r02_ksolve_traffic.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p))
-    if d.get("rows") != rows or d.get("iters") != iters:
-        return None
-    return d["dram_bytes_per_launch"]
+    return json.load(open(p))
 
 
-def cpu_baseline(rows: int, iters: int, threads: int) -> dict:
+def host_info(threads: int) -> dict:
+    """CPU model, cores used, numpy + BLAS (threadpoolctl) of the host the CPU
+    baseline runs on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    from paper_2508_13437_b200 import _native
+    return {"cpu_model": model, "cores_used": threads, "numpy": np.__version__, "blas": _native.host_blas()}
+
+
+def cpu_baseline(rows: int, iters: int, threads: int, keep: bool = False) -> dict:
     """The oracle (CPU restatement of the reference, bit-identical trajectories)
-    on `rows` rows of the same layer, all host threads."""
+    on rows 0..rows-1 of the layer for `iters` iterations, all host threads
+    (a bounded sample of the workload).  `keep` returns the oracle's traces
+    for the parity check."""
     from threadpoolctl import threadpool_limits
 
     from oracle import oracle as O
@@ -155,10 +176,59 @@ def cpu_baseline(rows: int, iters: int, threads: int) -> dict:
                   prm, states, threads=threads)
     dt = time.perf_counter() - t0
     moves = int(out["moves_scored"][:, 0].sum())
-    return {"value": moves / dt, "unit": "moves/s", "cores": threads, "kind": "port",
-            "sample": f"{rows} rows x {iters} ALNS iterations of the C5 layer (rows 0..{rows - 1}), "
-                      f"{moves} reference-equivalent moves in {dt:.2f} s",
-            "seconds": dt, "moves": moves}
+    res = {"value": moves / dt, "unit": "moves/s", "cores": threads, "kind": "port",
+           "sample": f"{rows} rows x {iters} ALNS iterations of the C5 layer (rows 0..{rows - 1}), "
+                     f"{moves} reference-equivalent moves in {dt:.2f} s",
+           "seconds": dt, "moves": moves,
+           "row_iteration_s_per_core": dt * threads / (rows * iters),
+           "host": host_info(threads)}
+    # the whole C5 job (14336 rows x 100 iterations) at this rate, extrapolated
+    res["extrapolated_full_layer_s"] = res["row_iteration_s_per_core"] * D_OUT * 100 / threads
+    if keep:
+        res["_out"] = out
+    return res
+
+
+def parity_check(o: dict, lo: int, hi: int, cpu: dict | None, iters: int) -> dict:
+    """Bitwise parity of the benchmarked run itself: (1) the first cpu-iters
+    trace entries of rows 0..k-1 against the oracle leg (same rows, seeds,
+    starts), (2) rows of this block that have full-depth goldens made by the
+    unmodified reference (tests/golden/layer_c5.npz, 100 iterations): best
+    objective, codes, iteration count and the whole trace."""
+    host = {k: o[k].cpu().numpy() for k in ("trace_current_t", "trace_best_t", "trace_pair", "trace_accepted",
+                                             "initial_objective", "best_objective", "best_idx", "iterations")}
+    fields = ("trace_current_t", "trace_best_t", "trace_pair", "trace_accepted")
+    out = {"bitwise": True, "mismatches": []}
+    if cpu is not None and lo == 0:
+        co = cpu["_out"]
+        k = min(co["trace_current_t"].shape[0], hi - lo)
+        it = co["trace_current_t"].shape[1]
+        for f in fields:
+            if not np.array_equal(host[f][:k, :it], co[f][:k, :it]):
+                out["mismatches"].append(f"oracle:{f}")
+        if not np.array_equal(host["initial_objective"][:k], co["initial_objective"][:k]):
+            out["mismatches"].append("oracle:initial_objective")
+        out["oracle_rows"] = k
+        out["oracle_iterations_compared"] = it
+    gpath = os.path.join(ROOT, "tests", "golden", "layer_c5.npz")
+    full = []
+    if os.path.exists(gpath) and iters == 100:
+        from tests.golden_io import load
+        for rec in load("layer_c5"):
+            r = int(rec["row"])
+            if not lo <= r < hi:
+                continue
+            k = r - lo
+            it = int(rec["iterations"])
+            ok = (int(host["iterations"][k]) == it and host["best_objective"][k] == rec["best_objective"]
+                  and np.array_equal(host["best_idx"][k], rec["best_idx"])
+                  and all(np.array_equal(host[f][k, :it], rec[f]) for f in fields))
+            if not ok:
+                out["mismatches"].append(f"golden_row_{r}")
+            full.append(r)
+    out["reference_golden_rows_full_depth"] = full
+    out["bitwise"] = not out["mismatches"]
+    return out
 
 
 def time_to_reference(names=("c1", "c2", "c5row"), reps: int = 3) -> list:
@@ -231,35 +301,41 @@ def run_reference(args, rank, world):
     for _ in range(args.warmup):
         cpu_baseline(min(args.cpu_rows, 4), 1, threads)
     for _ in range(args.steps):
-        vals.append(cpu_baseline(args.cpu_rows, args.iters, threads))
+        vals.append(cpu_baseline(args.cpu_rows, args.cpu_iters, threads))
     v = statistics.median([c["value"] for c in vals])
     ms = statistics.median([c["seconds"] for c in vals]) * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "moves/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C5: PTQ Llama-3-8B 4096->14336 int4 layer, 2048 calib tokens",
-                       "rows_per_step": args.cpu_rows, "iters_per_row": args.iters},
-            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "moves/s"},
+                       "rows_per_step": args.cpu_rows, "iters_per_row": args.cpu_iters,
+                       "sample_of": f"{args.rows} rows x {args.iters} iterations per GPU step"},
+            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample", "host",
+                                                       "row_iteration_s_per_core", "extrapolated_full_layer_s")}
+            | {"value": v, "unit": "moves/s"},
             "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def scorer_roofline(X, dev, flush, reps: int = 10, batch: int = 512) -> dict:
+def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
     """The standalone candidate-move scorer (amvm_score_moves, north star (c))
     on the C5 shapes: A = X (m=2048 x n=4096), 16 levels.
       * adjacent mode (the reference's one_opt set, |V_s| = 2), one instance,
-        L2 flushed before every launch: HBM roofline of one column stream;
-        algorithmic bytes = 8mn (A) + 8m (s) + 4n (idx) + 16n (scores).
+        L2 flushed before every launch: HBM roofline of one column stream
+        (k_score_adj: TMA bulk copies into a 4-stage smem ring, one CTA per
+        SM); algorithmic bytes = 8mn (A) + 8m (s) + 4n (idx) + 16n (scores).
       * all-levels mode over a batch of rows sharing A (|V| = 16): candidate
         moves scored per second; A is L2-resident across the batch, so this
         leg is FP64-pipe bound (2 flops = DMUL + DADD per candidate element).
-    Times are CUDA events on the launching stream around the scorer call
-    (ticket-counter memset + k_score_moves with the fused best-move reduction)."""
+    The timed call is the C-ABI entry itself (inputs validated once before,
+    outside the timing); CUDA events on the launching stream; one kernel per
+    call (no memset: the workspace counters are zeroed once at allocation)."""
     import torch
 
     from paper_2508_13437_b200 import _native as N
-    from paper_2508_13437_b200.scoring import score_moves_device
+    from paper_2508_13437_b200.scoring import MODES, score_moves_device
 
+    lib = N.load_library()
     m, n = X.shape
     nlev = 16
     g = torch.Generator(device="cpu").manual_seed(11)
@@ -272,36 +348,50 @@ def scorer_roofline(X, dev, flush, reps: int = 10, batch: int = 512) -> dict:
         s = (torch.randn((count, m), generator=g, dtype=torch.float64) * 0.1).to(dev)
         B = torch.zeros((count, m), dtype=torch.float64, device=dev)
         prob = N.Problem(m, n, nlev, count, At.data_ptr(), B.data_ptr(), lv.data_ptr())
-        ws = torch.empty(int(N.load_library().amvm_score_workspace_bytes(N.C.byref(prob))), dtype=torch.uint8,
-                         device=dev)
+        ws = torch.zeros(int(lib.amvm_score_workspace_bytes(N.C.byref(prob))), dtype=torch.uint8, device=dev)
+        t, best, best_t = score_moves_device(prob, idx, s, mode, ws)  # validated once
+        args = (N.C.byref(prob), N.ptr(idx), N.ptr(s), MODES[mode], N.ptr(t), N.ptr(best), N.ptr(best_t),
+                N.ptr(ws), ws.numel(), N.stream_handle())
         for _ in range(3):
-            score_moves_device(prob, idx, s, mode, ws)
+            N.check(lib.amvm_score_moves(*args), "amvm_score_moves")
         ms = []
         for _ in range(reps):
             if flush_each:
                 flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            score_moves_device(prob, idx, s, mode, ws)
+            N.check(lib.amvm_score_moves(*args), "amvm_score_moves")
             b.record(st)
             torch.cuda.synchronize()
             ms.append(a.elapsed_time(b))
-        return float(np.median(ms))
+        live = int(((idx > 0).sum() + (idx < nlev - 1).sum()).item())  # candidates that exist
+        return float(np.median(ms)), float(np.min(ms)), live
 
     pk = peaks()
-    ms1 = leg(1, "adjacent", True)
+    ms1, ms1_min, live1 = leg(1, "adjacent", True)
     alg = 8 * m * n + 8 * m + 4 * n + 16 * n
     gbs = alg / (ms1 / 1e3) / 1e9
-    msb = leg(batch, "all", False)
+    msb, _, _ = leg(batch, "all", False)
     moves = batch * n * (nlev - 1)
     return {
-        "adjacent_single": {"ms": round(ms1, 4), "bytes": alg, "achieved_GBps": round(gbs, 1),
-                            "peak_GBps": pk["hbm_gbs"], "frac": round(gbs / pk["hbm_gbs"], 4),
-                            "moves_per_s": 2 * n / (ms1 / 1e3), "l2": "flushed before every launch"},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": None,
+                     "kernel": "k_score_adj (north-star scorer (c): adjacent set |V_s| = 2, one C5 instance "
+                               "m=2048 x n=4096, L2 flushed before every launch, median of "
+                               f"{reps} launches)",
+                     "algorithmic_bytes": alg, "peak_source": pk["source"]},
+        "adjacent_single": {"ms": round(ms1, 4), "ms_min": round(ms1_min, 4), "bytes": alg,
+                            "achieved_GBps": round(gbs, 1), "peak_GBps": pk["hbm_gbs"],
+                            "frac": round(gbs / pk["hbm_gbs"], 4), "live_candidates": live1,
+                            "moves_per_s": live1 / (ms1 / 1e3), "l2": "flushed before every launch"},
         "all_levels_batch": {"rows": batch, "ms": round(msb, 3), "moves_per_s": moves / (msb / 1e3),
-                             "fp64_tflops": round(2 * batch * m * n * nlev / (msb / 1e3) / 1e12, 2)},
-        "kernel": "k_score_moves (best move fused; + a 4-byte-per-instance memset)",
+                             "fp64_tflops": round(2 * batch * m * n * nlev / (msb / 1e3) / 1e12, 2),
+                             "kernel": "k_score_moves<0> (warp per column)"},
     }
+
+
+PHASES = ["select+copy", "rand-destroy", "worst-destroy", "repair", "one_opt", "find_candidates",
+          "swap_eval", "accept"]
 
 
 def run_amvm(args, rank, world):
@@ -310,7 +400,6 @@ def run_amvm(args, rank, world):
 
     from paper_2508_13437_b200 import SolverConfig, ptq
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dev = torch.device("cuda", torch.cuda.current_device())
     lo = (rank * args.rows) % D_OUT
     hi = min(lo + args.rows, D_OUT)
@@ -323,8 +412,8 @@ def run_amvm(args, rank, world):
     st = torch.cuda.current_stream()
 
     def step():
-        o = lb.solve(cfg)
-        return o
+        # the trace (18 B per row-iteration) feeds the parity check of this very run
+        return lb.solve(cfg, trace=True)
 
     for _ in range(args.warmup):
         step()
@@ -333,8 +422,6 @@ def run_amvm(args, rank, world):
     if world > 1:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    moves = 0
-    phase = np.zeros(16)
     with Clocks(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         outs = []
@@ -347,41 +434,63 @@ def run_amvm(args, rank, world):
         torch.cuda.synchronize()
     lb.check_status()
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    moves = raw = 0
+    phase = np.zeros(16)
     for o in outs:
-        moves += int(o["moves_scored"][:, 0].sum().item())
+        ms_ = o["moves_scored"].sum(dim=0).cpu().numpy()
+        moves += int(ms_[0])
+        raw += int(ms_[1])
         phase += o["phase_cycles"].sum(dim=0).cpu().numpy()
     t_max = dev_ms
-    tot_moves = moves
+    tot_moves, tot_raw = moves, raw
     if world > 1:
         t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
-        mv = torch.tensor([moves], dtype=torch.float64, device=dev)
+        mv = torch.tensor([moves, raw], dtype=torch.float64, device=dev)
         dist.all_reduce(mv)
-        tot_moves = int(mv.item())
+        tot_moves, tot_raw = int(mv[0].item()), int(mv[1].item())
     value = tot_moves / (t_max / 1e3)
-    # roofline: scoring reads one A column (8*m bytes) per 2 adjacent-level
-    # candidates (|V_s| = 2); the dominant kernel is k_solve
     pk = peaks()
-    bytes_per_move = 8 * M_CALIB / 2
-    achieved = moves * bytes_per_move / (dev_ms / 1e3) / 1e9
     pc = phase[:8]
-    oo_frac = pc[4] / pc.sum() if pc.sum() else 0.0
-    roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(hi - lo, args.iters),
-            "peak_source": pk["source"], "achieved_kind": "effective (algorithmic bytes, SURVEY.md 8d)",
-            "kernel": "k_solve (fused ALNS iteration; all phases)",
-            "bytes_per_move": bytes_per_move, "V_s": 2,
-            "one_opt_phase_share": round(float(oo_frac), 4),
-            "one_opt_phase_GBps": achieved / oo_frac if oo_frac else None}
+    # k_solve (the dominant kernel of the step): SURVEY.md §8d's effective
+    # bytes (one A column, 8m B, per 2 adjacent-level candidates) beside the
+    # physical DRAM bytes ncu measured for this workload (scaled per
+    # row-iteration from profiles/r02_ksolve_traffic.json)
+    bytes_per_move = 8 * M_CALIB / 2
+    eff = moves * bytes_per_move / (dev_ms / 1e3) / 1e9
+    row_its = (hi - lo) * args.iters * args.steps
+    tr = ncu_traffic()
+    ksolve = {"kernel": "k_solve (persistent ALNS engine, all phases fused)",
+              "effective_GBps": round(eff, 1), "effective_frac": round(eff / pk["hbm_gbs"], 4),
+              "effective_kind": "algorithmic bytes per reference-equivalent move (8m/2), SURVEY.md 8d; "
+                                "exact row screens avoid streaming most columns, so this exceeds DRAM bytes",
+              "bytes_per_move": bytes_per_move, "V_s": 2,
+              "phase_share": {nm: round(float(v / pc.sum()), 4) for nm, v in zip(PHASES, pc)} if pc.sum() else {},
+              "busy_gcycles_per_step": round(float(pc.sum()) / 1e9 / args.steps, 3)}
+    if tr:
+        phys = tr["dram_bytes_per_row_iteration"] * row_its / (dev_ms / 1e3) / 1e9
+        ksolve.update({"physical_dram_GBps": round(phys, 1), "physical_frac": round(phys / pk["hbm_gbs"], 4),
+                       "dram_bytes_per_row_iteration": tr["dram_bytes_per_row_iteration"],
+                       "ncu": tr.get("source"), "fp64_pipe_pct": tr.get("fp64_pipe_pct"),
+                       "issue_active_pct": tr.get("issue_active_pct"), "bound": tr.get("bound")})
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, X, W, lo, hi, cfg, world)
+    cpu = None
+    if world == 1:
+        cpu = cpu_baseline(args.cpu_rows, args.cpu_iters, len(os.sched_getaffinity(0)), keep=True)
+    par = parity_check(outs[-1], lo, hi, cpu, args.iters)
+    if world > 1:
+        bad = torch.tensor([0 if par["bitwise"] else 1], dtype=torch.int64, device=dev)
+        dist.all_reduce(bad)
+        par["ranks_mismatching"] = int(bad.item())
+        par["bitwise"] = par["ranks_mismatching"] == 0
     if rank != 0:
+        if not par["bitwise"]:
+            sys.exit(3)
         return
     clocks = clk.summary()
-    names = ["select+copy", "rand-destroy", "worst-destroy", "repair", "one_opt", "find_candidates",
-             "swap_eval", "accept"]
     line = {
         "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -390,25 +499,30 @@ def run_amvm(args, rank, world):
                    "rows_per_gpu": hi - lo, "iters_per_row": args.iters, "m": M_CALIB, "n": D_IN,
                    "levels": 16, "parallelism": f"rows sharded over {world} GPU(s)",
                    "l2": "flushed (256 MB write) before every timed step"},
-        # per step (ncu launch list, profiles/r01_launches.csv): k_transpose (row-major A),
+        "moves_scored_raw": tot_raw,
+        "moves_scored_ref": tot_moves,
+        # per step (ncu launch list, profiles/): k_transpose (row-major A),
         # k_csc_count + k_csc_scan + k_csc_fill (sparse copy of A; dense X: counted, not filled), k_solve
         "gpu_launches": 5 * args.steps,
-        "roofline": roof,
-        "phase_share": {nm: round(float(v / pc.sum()), 4) for nm, v in zip(names, pc)} if pc.sum() else {},
-        "busy_gcycles_per_step": round(float(pc.sum()) / 1e9 / args.steps, 3),
+        "parity": par,
+        "k_solve": ksolve,
         "ms_steps": [round(a.elapsed_time(b), 2) for a, b in ev],
         "clocks": clocks,
     }
     if e2e:
         line["e2e"] = e2e
     if world == 1:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_rows, args.iters, len(os.sched_getaffinity(0)))
-        line["cpu_baseline"].pop("seconds", None)
-        line["cpu_baseline"].pop("moves", None)
+        cpu.pop("_out")
+        line["cpu_baseline"] = {k: v for k, v in cpu.items() if k not in ("seconds", "moves")}
         if not args.no_ttr:
             line["time_to_reference_linf"] = time_to_reference()
-        line["scorer"] = scorer_roofline(X, dev, flush)
+        sc = scorer_roofline(X, dev, flush)
+        line["roofline"] = sc.pop("roofline")
+        line["scorer"] = sc
     print(json.dumps(line), flush=True)
+    if not par["bitwise"]:
+        print(f"PARITY FAILURE: {par['mismatches']}", file=sys.stderr)
+        sys.exit(3)
 
 
 def run_e2e(args, X, W, lo, hi, cfg, world):
@@ -423,15 +537,14 @@ def run_e2e(args, X, W, lo, hi, cfg, world):
     Wh = torch.from_numpy(W).pin_memory()
     rows = np.arange(lo, hi)
     h2d = Xh.numel() * 8 + Wh.numel() * 8
-    for _ in range(max(1, args.warmup // 2)):
-        ptq.solve_layer(Xh, Wh, bits=4, cfg=cfg, seeds=rows)
+    ptq.solve_layer(Xh, Wh, bits=4, cfg=cfg, seeds=rows)  # warm (the device path is already warm)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     moves = 0
     d2h = 0
-    steps = max(1, args.steps // 2)
+    steps = max(1, min(args.steps, 2))
     for _ in range(steps):
         rep = ptq.solve_layer(Xh, Wh, bits=4, cfg=cfg, seeds=rows)
         rep.rows = rows

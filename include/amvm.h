@@ -105,8 +105,13 @@ typedef struct {
   uint8_t *trace_pair;      /* count x max_iters, PAIRS slot                  */
   uint8_t *trace_accepted;  /* count x max_iters                              */
   int64_t *moves_scored;    /* count x 2: [0] reference-equivalent candidate
-                               moves scored, [1] raw candidates scored
-                               (incl. speculative window work); may be NULL   */
+                               moves scored (the candidates the reference
+                               evaluates on this trajectory: 1-OPT neighbours
+                               up to the applied move, 2 per greedy variable,
+                               filtered swaps), [1] raw candidates the device
+                               scored over all m rows (one_opt columns that
+                               survive the exact row screens, greedy trials,
+                               swap evaluations); may be NULL                 */
   int64_t *phase_cycles;    /* count x 16: [0..7] SM-clock cycles per phase
                                (select+copy, random destroy, impact+worst
                                destroy, repair, one_opt, find_candidates,
@@ -154,6 +159,58 @@ AMVM_API int amvm_best_swap(const amvm_problem *prob, const amvm_params *prm,
                    const amvm_solution *sol, double *out4, void *ws,
                    size_t ws_bytes, void *stream);
 
+/* best_swap with FilterConfig.l2_tiebreak (localsearch.py:181-246): the
+ * candidates split like np.array_split(cands, min(workers, count)); each
+ * chunk's smallest improving t' wins its chunk, ties going to the smallest
+ * (l2, i, j) with l2 = np.linalg.norm(shifted, axis=1) (pairwise sum of
+ * squares; a lone winner carries np.linalg.norm = sqrt(ddot)); chunk
+ * winners merge by (t, l2, i, j).  out4 as amvm_best_swap.                 */
+AMVM_API int amvm_best_swap_l2(const amvm_problem *prob, const amvm_params *prm,
+                               const amvm_solution *sol, int32_t workers, double *out4,
+                               void *ws, size_t ws_bytes, void *stream);
+
+/* apply_shift (core.py:208-225): s += (lv[new] - lv[old]) * A[:, j]
+ * (DMUL, DADD), idx[j] = new, then _bump (core.py:200-205): the counter +1
+ * and objective = max|s|, or the dgemv-order refresh at refresh_period.
+ * Shifting to the current level is a no-op (no counter bump).  In place.  */
+AMVM_API int amvm_apply_shift(const amvm_problem *prob, const amvm_params *prm,
+                              amvm_solution *sol, int64_t j, int32_t new_level,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/* apply_swap (core.py:228-245): s += (x_i - x_j) * (A[:, j] - A[:, i]),
+ * levels exchanged, _bump.  i != j; the values must differ (checked by the
+ * host mirror, which owns the reference's error messages).  In place.     */
+AMVM_API int amvm_apply_swap(const amvm_problem *prob, const amvm_params *prm,
+                             amvm_solution *sol, int64_t i, int64_t j, void *ws,
+                             size_t ws_bytes, void *stream);
+
+/* accept (controller.py:168-183): verdict (device int32[1]) = 1 iff
+ * cand_objective < cur_objective, or l2_tiebreak and cand_objective <=
+ * cur_objective + tie_tol and ||cand||_2 < ||cur||_2 (np.linalg.norm =
+ * sqrt of the OpenBLAS SkylakeX ddot).  Residuals are m doubles; the
+ * objectives are device double[1].                                         */
+AMVM_API int amvm_accept(int64_t m, const double *cur_residual, const double *cur_objective,
+                         const double *cand_residual, const double *cand_objective,
+                         int32_t l2_tiebreak, double tie_tol, int32_t *verdict, void *stream);
+
+/* OperatorBank (controller.py:71-85) as device data; PAIRS slot order.     */
+typedef struct {
+  double weights[4], scores[4];
+  int64_t segment_uses[4], lifetime_uses[4], iteration;
+  double decay;
+} amvm_bank;
+
+/* select_operators (controller.py:88-90): *pair (device int32) =
+ * rng.choice(4, p=weights/sum(weights)); advances rng.                      */
+AMVM_API int amvm_select_operators(const amvm_bank *bank, amvm_pcg64 *rng, int32_t *pair,
+                                   void *stream);
+
+/* update_weights (controller.py:99-131): outcome 0 new best, 1 improved,
+ * 2 accepted, 3 rejected; sigma1..3, weight_floor and n_segment from prm,
+ * the decay from the bank (OperatorBank.decay).                            */
+AMVM_API int amvm_update_weights(amvm_bank *bank, const amvm_params *prm, int32_t pair,
+                                 int32_t outcome, void *stream);
+
 /* impact_scores, operators.py:54-74: d (device double[n]).                 */
 AMVM_API int amvm_impact_scores(const amvm_problem *prob, const amvm_params *prm,
                        const amvm_solution *sol, double *d, void *ws,
@@ -176,7 +233,9 @@ AMVM_API int amvm_repair(const amvm_problem *prob, const amvm_params *prm, int k
 
 /* compute_residual, core.py:183-197, as a device contraction for a batch:
  * residual[k] = A @ levels[k][idx[k]] - B[k], objective[k] = max|residual|.
- * (Summation order differs from host BLAS dgemv.)          */
+ * Summed in OpenBLAS 0.3.30's SkylakeX dgemv_t order (4 FMA accumulators
+ * per output over 2048-element blocks, ddot for m == 1): bitwise equal to
+ * numpy's `A @ x` on such a host with single-threaded BLAS. */
 AMVM_API int amvm_compute_residual(const amvm_problem *prob, amvm_solution *sol,
                           void *stream);
 
@@ -226,8 +285,15 @@ AMVM_API int amvm_is_improving(const amvm_problem *prob, const double *residual,
  * best[c] = flat index j*nv + v of the smallest (t, j, l) over candidates
  * that change the level (-1 if none), best_t[c] its t.  `idx` is count x n,
  * `residual` count x m; device pointers; replaces the Python loop of
- * localsearch.py:70-80 for scoring (no move is applied).  Workspace (8-byte
- * aligned) of amvm_score_workspace_bytes(prob): per-column bests.          */
+ * localsearch.py:70-80 for scoring (no move is applied).
+ * Preconditions: 0 <= idx < nlev; A, residual and levels finite (the
+ * abs-max drops NaN where numpy's propagates it).  Workspace (8-byte
+ * aligned) of amvm_score_workspace_bytes(prob): per-CTA best slots and one
+ * ticket counter per instance; it must be ZEROED before its first use (the
+ * kernels leave the counters at zero, so no per-call memset is needed).
+ * Adjacent mode with even m <= 8192 runs the TMA-bulk streaming kernel (one
+ * CTA per SM, every column of A read from HBM once per instance); other
+ * shapes and the all-levels mode run the warp-per-column kernel.          */
 AMVM_API size_t amvm_score_workspace_bytes(const amvm_problem *prob);
 AMVM_API int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual,
                               int mode, double *out_t, int64_t *best, double *best_t,

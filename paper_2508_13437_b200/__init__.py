@@ -16,13 +16,19 @@ from .controller import (  # noqa: F401
     ONE_OPT_MAX_SWEEPS,
     PAIRS,
     WEIGHT_FLOOR,
+    OUTCOME_ACCEPTED,
+    OUTCOME_IMPROVED,
+    OUTCOME_NEW_BEST,
+    OUTCOME_REJECTED,
     DestroySet,
     FilterConfig,
+    OperatorBank,
     ImpactScores,
     SolveReport,
     SolverConfig,
     SwapCandidate,
     TraceEntry,
+    accept,
     best_swap,
     find_candidates,
     greedy_repair,
@@ -33,7 +39,9 @@ from .controller import (  # noqa: F401
     random_destroy,
     random_repair,
     removal_count,
+    select_operators,
     solve,
+    update_weights,
     worst_remove_destroy,
 )
 from .exact import (  # noqa: F401
@@ -64,6 +72,8 @@ from .core import (  # noqa: F401
     RowScreen,
     Solution,
     ValueSet,
+    apply_shift,
+    apply_swap,
     compute_residual,
     round_to_nearest,
     row_screen,
@@ -80,5 +90,6 @@ __all__ = [
     "SwapCheckReport", "exhaustive_swap_check", "is_improving",
     "InstanceParseError", "RunArtifacts", "export_lp", "format_values", "instance_to_text",
     "read_instance", "write_instance", "write_run_artifacts", "write_solution",
-    "MoveScores", "score_moves",
+    "MoveScores", "score_moves", "apply_shift", "apply_swap", "OperatorBank", "select_operators",
+    "update_weights", "accept", "OUTCOME_NEW_BEST", "OUTCOME_IMPROVED", "OUTCOME_ACCEPTED", "OUTCOME_REJECTED",
 ]

@@ -26,7 +26,8 @@ EXPORTS = (
     "amvm_ls_start_workspace_bytes", "amvm_ls_start",
     "amvm_projector_workspace_bytes", "amvm_projector_indptr", "amvm_projector_fill",
     "amvm_csr_gemv", "amvm_sirt_workspace_bytes", "amvm_sirt", "amvm_is_improving", "amvm_swap_check",
-    "amvm_score_moves", "amvm_score_workspace_bytes",
+    "amvm_score_moves", "amvm_score_workspace_bytes", "amvm_best_swap_l2", "amvm_apply_shift",
+    "amvm_apply_swap", "amvm_accept", "amvm_select_operators", "amvm_update_weights",
 )
 
 
@@ -54,6 +55,12 @@ class Params(C.Structure):
 class PCG64State(C.Structure):
     _fields_ = [("state_hi", C.c_uint64), ("state_lo", C.c_uint64), ("inc_hi", C.c_uint64),
                 ("inc_lo", C.c_uint64), ("has_uint32", C.c_uint32), ("uinteger", C.c_uint32)]
+
+
+class Bank(C.Structure):
+    """amvm_bank: OperatorBank (controller.py:71-85) as device data."""
+    _fields_ = [("weights", C.c_double * 4), ("scores", C.c_double * 4), ("segment_uses", C.c_int64 * 4),
+                ("lifetime_uses", C.c_int64 * 4), ("iteration", C.c_int64), ("decay", C.c_double)]
 
 
 class SolutionPtrs(C.Structure):
@@ -116,12 +123,64 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_sirt_workspace_bytes.argtypes = [i64, i64, i64, i64]
     lib.amvm_sirt.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, i32, C.c_double, C.c_double, C.c_int, vp, vp,
                               sz, vp]
+    lib.amvm_best_swap_l2.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
+    lib.amvm_apply_shift.argtypes = [vp, vp, vp, i64, i32, vp, sz, vp]
+    lib.amvm_apply_swap.argtypes = [vp, vp, vp, i64, i64, vp, sz, vp]
+    lib.amvm_accept.argtypes = [i64, vp, vp, vp, vp, i32, C.c_double, vp, vp]
+    lib.amvm_select_operators.argtypes = [vp, vp, vp, vp]
+    lib.amvm_update_weights.argtypes = [vp, vp, i32, i32, vp]
     lib.amvm_strerror.restype = C.c_char_p
     lib.amvm_strerror.argtypes = [C.c_int]
     for name in EXPORTS:
         getattr(lib, name)
     _lib = lib
     return lib
+
+
+# Host BLAS kernels whose ddot / dgemv order the device emulates bitwise
+# (OpenBLAS 0.3.30 SkylakeX ddot + Haswell-microkernel dgemv_t; Cooperlake
+# and SapphireRapids build on the SkylakeX kernel list).  np.linalg.norm and
+# A @ x follow the host's kernel (controller.py:180, core.py:175,196).
+BLAS_ORDERS = ("SkylakeX", "Cooperlake", "SapphireRapids")
+_blas_checked: str | None = None
+
+
+class BlasOrderMismatch(RuntimeError):
+    pass
+
+
+def host_blas() -> dict:
+    """numpy's BLAS as threadpoolctl reports it (library, version, architecture)."""
+    import numpy  # noqa: F401  (threadpoolctl only sees libraries already loaded)
+    try:
+        from threadpoolctl import threadpool_info
+    except ImportError:
+        return {}
+    for info in threadpool_info():
+        if info.get("user_api") == "blas":
+            return {k: info.get(k) for k in ("internal_api", "version", "architecture", "num_threads")}
+    return {}
+
+
+def check_blas_order() -> str:
+    """Fail loudly when the host BLAS is not one whose summation order the
+    device reproduces: the reference's trajectory on such a host would differ
+    from this build's at the first rounding-decided l2 tie.
+    ``AMVM_ALLOW_BLAS_MISMATCH=1`` runs anyway (results stay valid solutions,
+    just not bitwise equal to that host's reference run)."""
+    global _blas_checked
+    if _blas_checked is not None:
+        return _blas_checked
+    info = host_blas()
+    arch = info.get("architecture") or "unknown"
+    ok = info.get("internal_api") == "openblas" and arch in BLAS_ORDERS
+    if not ok and os.environ.get("AMVM_ALLOW_BLAS_MISMATCH") != "1":
+        raise BlasOrderMismatch(
+            f"host BLAS is {info.get('internal_api')} {info.get('version')} ({arch}); the device reproduces the "
+            f"ddot/dgemv summation order of OpenBLAS {'/'.join(BLAS_ORDERS)} only, so this host's reference "
+            "trajectory would not be matched bit for bit (set AMVM_ALLOW_BLAS_MISMATCH=1 to run anyway)")
+    _blas_checked = arch
+    return arch
 
 
 def torch_cuda():

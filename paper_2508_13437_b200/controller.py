@@ -262,6 +262,7 @@ def solve(inst: Instance, cfg: SolverConfig | None = None, *, device_warm_start:
     (``initial_solution(device=True)``)."""
     cfg = cfg or SolverConfig()
     started = time.perf_counter()
+    N.check_blas_order()
     rng = np.random.default_rng(cfg.seed)
     current = initial_solution(inst, device=device_warm_start)
     initial_objective = current.objective
@@ -287,6 +288,7 @@ def solve_from(inst: Instance, start: Solution, cfg: SolverConfig | None = None)
     (warm restart; also how the parity tests feed the reference's own start)."""
     cfg = cfg or SolverConfig()
     started = time.perf_counter()
+    N.check_blas_order()
     rng = np.random.default_rng(cfg.seed)
     if cfg.max_iters == 0 or start.objective == 0.0:
         return SolveReport(best=start.copy(), trace=[], wall_time=0.0, iterations=0,
@@ -358,6 +360,122 @@ def _solve_device(inst, cfg, current, rng, max_iters, budget) -> dict:
     }
 
 
+# --------------------------------------------- incremental residual algebra
+def _device_update(inst: Instance, sol: Solution, kind: str, a: int, b: int) -> Solution:
+    """apply_shift / apply_swap (core.py:208-245) on the GPU, in place."""
+    D = _Dev(inst, sol)
+    prm = make_params(None, inst.n)
+    ws, wsb = D.ws(prm)
+    if kind == "shift":
+        rc = D.lib.amvm_apply_shift(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), a, b, ws, wsb,
+                                    N.stream_handle())
+    else:
+        rc = D.lib.amvm_apply_swap(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), a, b, ws, wsb,
+                                   N.stream_handle())
+    D.finish(rc, f"amvm_apply_{kind}", ws)
+    return D.write_back(sol)
+
+
+# ------------------------------------------- operator bank and acceptance
+OUTCOME_NEW_BEST = "new_best"
+OUTCOME_IMPROVED = "improved"
+OUTCOME_ACCEPTED = "accepted"
+OUTCOME_REJECTED = "rejected"
+_OUTCOMES = (OUTCOME_NEW_BEST, OUTCOME_IMPROVED, OUTCOME_ACCEPTED, OUTCOME_REJECTED)
+
+
+class OperatorBank:
+    """Adaptive weights, segment scores and usage counts per operator pair
+    (controller.py:71-85).  The arrays live on the host like the reference's;
+    ``select_operators`` / ``update_weights`` run the same arithmetic as the
+    solve kernel's device bank (``amvm_select_operators`` /
+    ``amvm_update_weights``)."""
+
+    def __init__(self, decay: float = 0.8) -> None:
+        if not 0 < decay <= 1:
+            raise ValueError("decay must lie in (0, 1]")
+        self.decay = float(decay)
+        self.weights = np.ones(len(PAIRS))
+        self.scores = np.zeros(len(PAIRS))
+        self.segment_uses = np.zeros(len(PAIRS), dtype=int)
+        self.lifetime_uses = np.zeros(len(PAIRS), dtype=int)
+        self.iteration = 0
+
+    def probabilities(self) -> np.ndarray:
+        return self.weights / self.weights.sum()
+
+    def _to_device(self, device):
+        torch = N.torch_cuda()
+        st = N.Bank((N.C.c_double * 4)(*self.weights), (N.C.c_double * 4)(*self.scores),
+                    (N.C.c_int64 * 4)(*self.segment_uses), (N.C.c_int64 * 4)(*self.lifetime_uses),
+                    int(self.iteration), float(self.decay))
+        raw = np.frombuffer(bytes(st), dtype=np.uint8).copy()
+        return torch.from_numpy(raw).to(device)
+
+    def _from_device(self, buf) -> None:
+        st = N.Bank.from_buffer_copy(buf.cpu().numpy().tobytes())
+        self.weights = np.array(st.weights[:], dtype=float)
+        self.scores = np.array(st.scores[:], dtype=float)
+        self.segment_uses = np.array(st.segment_uses[:], dtype=int)
+        self.lifetime_uses = np.array(st.lifetime_uses[:], dtype=int)
+        self.iteration = int(st.iteration)
+
+
+def select_operators(bank: OperatorBank, rng: np.random.Generator) -> int:
+    """Roulette-wheel pick of a destroy/repair pair (controller.py:88-90); one
+    ``random()`` of ``rng``'s PCG64 stream, drawn on the GPU (the generator's
+    state is advanced exactly as numpy's ``rng.choice(4, p=...)``)."""
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bb = bank._to_device(dev)
+    rb, _ = _rng_struct(rng, dev)
+    out = torch.empty(1, dtype=torch.int32, device=dev)
+    N.check(lib.amvm_select_operators(N.ptr(bb), N.ptr(rb), N.ptr(out), N.stream_handle()),
+            "amvm_select_operators")
+    _rng_sync_back(rng, rb)
+    return int(out.item())
+
+
+def update_weights(bank: OperatorBank, pair_id: int, outcome: str,
+                   cfg: SolverConfig | None = None) -> OperatorBank:
+    """Score the pair for this iteration's outcome; decay at segment ends
+    (controller.py:99-131), on the GPU.  Mutates and returns ``bank``."""
+    cfg = cfg or SolverConfig()
+    if outcome not in _OUTCOMES:
+        raise KeyError(outcome)
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bb = bank._to_device(dev)
+    prm = make_params(cfg, 1)
+    N.check(lib.amvm_update_weights(N.ptr(bb), N.C.byref(prm), int(pair_id), _OUTCOMES.index(outcome),
+                                    N.stream_handle()), "amvm_update_weights")
+    bank._from_device(bb)
+    return bank
+
+
+def accept(current: Solution, candidate: Solution, cfg: SolverConfig) -> bool:
+    """Strict improvement, or with ``cfg.l2_tiebreak`` a tie within
+    ACCEPT_TIE_TOL and a strictly smaller l2 residual (controller.py:168-183);
+    the norms are the host BLAS ddot order, on the GPU (``amvm_accept``)."""
+    torch = N.torch_cuda()
+    lib = N.load_library()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cur = np.ascontiguousarray(current.residual, dtype=np.float64)
+    cand = np.ascontiguousarray(candidate.residual, dtype=np.float64)
+    if cur.shape != cand.shape or cur.ndim != 1 or cur.size == 0:
+        raise ValueError("current and candidate residuals must be non-empty vectors of equal length")
+    t = torch.from_numpy(np.concatenate([cur, cand, [current.objective, candidate.objective]])).to(dev)
+    m = cur.size
+    out = torch.empty(1, dtype=torch.int32, device=dev)
+    base = t.data_ptr()
+    N.check(lib.amvm_accept(m, N.C.c_void_p(base), N.C.c_void_p(base + 8 * 2 * m), N.C.c_void_p(base + 8 * m),
+                            N.C.c_void_p(base + 8 * (2 * m + 1)), int(bool(cfg.l2_tiebreak)), ACCEPT_TIE_TOL,
+                            N.ptr(out), N.stream_handle()), "amvm_accept")
+    return bool(out.item())
+
+
 # ------------------------------------------------------ component functions
 def one_opt(inst: Instance, sol: Solution, max_sweeps: int = ONE_OPT_MAX_SWEEPS) -> Solution:
     """Adjacent-level first-improvement sweeps on the GPU (localsearch.py:59-88)."""
@@ -406,18 +524,25 @@ def find_candidates(inst: Instance, sol: Solution, cfg: FilterConfig) -> list[Sw
 
 
 def best_swap(inst: Instance, sol: Solution, cfg: FilterConfig) -> SwapCandidate | None:
-    """Best strictly improving filtered swap (localsearch.py:211-246)."""
+    """Best strictly improving filtered swap (localsearch.py:211-246).  With
+    ``cfg.l2_tiebreak`` the candidates are chunked over ``cfg.workers`` and
+    chunk winners merge by (t, l2, i, j) exactly as the reference's threads
+    do (``amvm_best_swap_l2``); without it the merge key is (t, i, j) and the
+    result does not depend on ``workers``."""
     if sol.objective <= 0:
         return None
-    if cfg.l2_tiebreak:
-        raise NotImplementedError("the l2 swap tie-break is not on the solve path (controller.py:65-68)")
     D = _Dev(inst, sol)
     torch = D.torch
     prm = make_params(None, inst.n, fcfg=cfg)
     out = torch.zeros(4, dtype=torch.float64, device=D.device)
     ws, wsb = D.ws(prm)
-    D.finish(D.lib.amvm_best_swap(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), N.ptr(out), ws, wsb,
-                                  N.stream_handle()), "amvm_best_swap", ws)
+    if cfg.l2_tiebreak:
+        rc = D.lib.amvm_best_swap_l2(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), int(cfg.workers),
+                                     N.ptr(out), ws, wsb, N.stream_handle())
+        D.finish(rc, "amvm_best_swap_l2", ws)
+    else:
+        D.finish(D.lib.amvm_best_swap(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), N.ptr(out), ws, wsb,
+                                      N.stream_handle()), "amvm_best_swap", ws)
     v = out.cpu().numpy()
     if v[0] < 0:
         return None

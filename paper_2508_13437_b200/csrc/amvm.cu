@@ -157,6 +157,39 @@ __global__ void __launch_bounds__(NT) k_op(KArgs a) {
   E.run_op(a);
 }
 
+// accept (controller.py:168-183) for one (current, candidate) pair: strict
+// improvement, or (l2) a tie within tol and a strictly smaller
+// np.linalg.norm = sqrt(OpenBLAS ddot).  64 threads: warp 0 the candidate's
+// norm, warp 1 the current one's.
+__global__ void k_accept(int64_t m, const double *__restrict__ cur_r, const double *__restrict__ cur_obj,
+                         const double *__restrict__ cand_r, const double *__restrict__ cand_obj, int l2, double tol,
+                         int32_t *verdict) {
+  __shared__ double nrm[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double co = *cur_obj, ca = *cand_obj;
+  const bool need = !(ca < co) && l2 && ca <= amvm::dadd(co, tol);
+  if (need) {
+    const double *x = warp == 0 ? cand_r : cur_r;
+    const double dd = warp_ddot_skx([&](int64_t i) { return x[i]; }, [&](int64_t i) { return x[i]; }, m, lane);
+    if (lane == 0) nrm[warp] = __dsqrt_rn(dd);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *verdict = ca < co ? 1 : (need && nrm[0] < nrm[1] ? 1 : 0);
+}
+
+// select_operators / update_weights (controller.py:88-131) on a device bank.
+__global__ void k_bank_select(const amvm_bank *bank, amvm_pcg64 *rng, int32_t *pair) {
+  Pcg g = pcg_load(rng);
+  *pair = bank_select(bank->weights, g);
+  pcg_store(g, rng);
+}
+
+__global__ void k_bank_update(amvm_bank *bank, int pair, int outcome, double s1, double s2, double s3,
+                              double floor_w, int n_segment) {
+  bank_update(bank->weights, bank->scores, bank->segment_uses, bank->lifetime_uses, &bank->iteration, pair,
+              outcome, s1, s2, s3, bank->decay, floor_w, n_segment);
+}
+
 // compute_residual (core.py:183-197) for a batch sharing A: residual[k] =
 // A @ levels_k[idx_k] - B[k] in numpy's OpenBLAS dgemv order, objective[k] =
 // max |residual[k]|.  CTA = kRI instances x NT rows (grid: instance groups x
@@ -589,6 +622,19 @@ bool sol_ok(const amvm_solution *s) { return s && s->idx && s->residual && s->ob
 
 }  // namespace
 
+namespace {
+template <int CB>
+int launch_adj(const amvm_problem *prob, const int32_t *idx, const double *residual, double *out_t, int64_t *best,
+               double *best_t, double *blk_t, int64_t *blk_i, unsigned *done, int G, cudaStream_t st) {
+  const size_t smem = adj_smem_bytes(prob->m);
+  if (cudaFuncSetAttribute(k_score_adj<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return AMVM_ERR_CUDA;
+  k_score_adj<CB><<<G, kAdjThreads, smem, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At, prob->levels,
+                                                idx, residual, out_t, blk_t, blk_i, done, best, best_t);
+  return cuda_rc(cudaGetLastError());
+}
+}  // namespace
+
 // ================================================================== C-ABI
 extern "C" {
 
@@ -682,6 +728,68 @@ int amvm_best_swap(const amvm_problem *prob, const amvm_params *prm, const amvm_
   a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
   a.x_out4 = out4;
   return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_best_swap_l2(const amvm_problem *prob, const amvm_params *prm, const amvm_solution *sol, int32_t workers,
+                      double *out4, void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !sol_ok(sol) || !out4 || workers < 1) return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_BEST_SWAP;
+  a.kind = workers;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  a.x_out4 = out4;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_apply_shift(const amvm_problem *prob, const amvm_params *prm, amvm_solution *sol, int64_t j,
+                     int32_t new_level, void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !prm || !sol_ok(sol) || j < 0 || j >= prob->n || new_level < 0 || new_level >= prob->nlev)
+    return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_APPLY_SHIFT;
+  a.x_r = (int32_t)j;
+  a.kind = new_level;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_apply_swap(const amvm_problem *prob, const amvm_params *prm, amvm_solution *sol, int64_t i, int64_t j,
+                    void *ws, size_t ws_bytes, void *stream) {
+  if (!prob || !prm || !sol_ok(sol) || i == j || i < 0 || j < 0 || i >= prob->n || j >= prob->n)
+    return AMVM_ERR_INVALID;
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.op = OP_APPLY_SWAP;
+  a.x_r = (int32_t)i;
+  a.kind = (int)j;
+  a.s_idx = sol->idx; a.s_r = sol->residual; a.s_obj = sol->objective; a.s_cnt = sol->updates;
+  return run_op(prob, prm, a, ws, ws_bytes, stream);
+}
+
+int amvm_accept(int64_t m, const double *cur_residual, const double *cur_objective, const double *cand_residual,
+                const double *cand_objective, int32_t l2_tiebreak, double tie_tol, int32_t *verdict,
+                void *stream) {
+  if (m < 1 || !cur_residual || !cur_objective || !cand_residual || !cand_objective || !verdict)
+    return AMVM_ERR_INVALID;
+  k_accept<<<1, 64, 0, (cudaStream_t)stream>>>(m, cur_residual, cur_objective, cand_residual, cand_objective,
+                                                l2_tiebreak, tie_tol, verdict);
+  return cuda_rc(cudaGetLastError());
+}
+
+int amvm_select_operators(const amvm_bank *bank, amvm_pcg64 *rng, int32_t *pair, void *stream) {
+  if (!bank || !rng || !pair) return AMVM_ERR_INVALID;
+  k_bank_select<<<1, 1, 0, (cudaStream_t)stream>>>(bank, rng, pair);
+  return cuda_rc(cudaGetLastError());
+}
+
+int amvm_update_weights(amvm_bank *bank, const amvm_params *prm, int32_t pair, int32_t outcome, void *stream) {
+  if (!bank || !prm || pair < 0 || pair > 3 || outcome < 0 || outcome > 3 || prm->n_segment < 1)
+    return AMVM_ERR_INVALID;
+  k_bank_update<<<1, 1, 0, (cudaStream_t)stream>>>(bank, pair, outcome, prm->sigma1, prm->sigma2, prm->sigma3,
+                                                    prm->weight_floor, prm->n_segment);
+  return cuda_rc(cudaGetLastError());
 }
 
 int amvm_impact_scores(const amvm_problem *prob, const amvm_params *prm, const amvm_solution *sol, double *d,
@@ -970,9 +1078,11 @@ int amvm_swap_check(const amvm_problem *prob, const int32_t *idx, const double *
 size_t amvm_score_workspace_bytes(const amvm_problem *prob) {
   if (!prob || prob->n < 1 || prob->count < 1) return 0;
   const int cpb = score_cols_per_cta(1) < score_cols_per_cta(0) ? score_cols_per_cta(1) : score_cols_per_cta(0);
-  const size_t nblk = (size_t)((prob->n + cpb - 1) / cpb);  // the larger grid of the two modes
+  size_t nblk = (size_t)((prob->n + cpb - 1) / cpb);  // the larger grid of the two k_score_moves modes
+  if (nblk < kScoreMaxSlabs) nblk = kScoreMaxSlabs;     // k_score_adj: one slab per SM
   return (size_t)prob->count * (nblk * 16 + 4) + 16;
 }
+
 
 int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual, int mode,
                      double *out_t, int64_t *best, double *best_t, void *ws, size_t ws_bytes, void *stream) {
@@ -983,12 +1093,36 @@ int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double 
   if (prob->count > 65535 || (prob->n + cpb - 1) / cpb > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
   if (!ws || ws_bytes < amvm_score_workspace_bytes(prob) || ((uintptr_t)ws & 7)) return AMVM_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  // workspace: per-CTA bests (t, flat) and one ticket counter per instance
-  const int64_t nblk = (prob->n + cpb - 1) / cpb;
+  // workspace: per-CTA bests (t, flat) and one ticket counter per instance;
+  // the counters must be zero before the first call on a workspace (the
+  // kernels leave them zero), so there is no per-call memset
+  size_t nslot = (size_t)((prob->n + score_cols_per_cta(1) - 1) / score_cols_per_cta(1));
+  {
+    const size_t n0 = (size_t)((prob->n + score_cols_per_cta(0) - 1) / score_cols_per_cta(0));
+    if (n0 > nslot) nslot = n0;
+    if (nslot < kScoreMaxSlabs) nslot = kScoreMaxSlabs;
+  }
   double *blk_t = (double *)ws;
-  int64_t *blk_i = (int64_t *)(blk_t + prob->count * nblk);
-  unsigned *done = (unsigned *)(blk_i + prob->count * nblk);
-  if (cudaMemsetAsync(done, 0, (size_t)prob->count * 4, st) != cudaSuccess) return AMVM_ERR_CUDA;
+  int64_t *blk_i = (int64_t *)(blk_t + prob->count * nslot);
+  unsigned *done = (unsigned *)(blk_i + prob->count * nslot);
+  // adjacent set, even m <= 8192: the TMA-bulk streaming scorer, one CTA per SM
+  if (mode == 1 && prob->m % 2 == 0 && prob->m <= (int64_t)kAdjThreads * kAdjMaxR) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return AMVM_ERR_CUDA;
+    const int cb = adj_cols_per_stage(prob->m);
+    int64_t G = sms < kScoreMaxSlabs ? sms : kScoreMaxSlabs;
+    const int64_t slabs = (prob->n + cb - 1) / cb;  // every slab holds at least one column
+    if (G > slabs) G = slabs;
+    switch (cb) {
+      case 1: return launch_adj<1>(prob, idx, residual, out_t, best, best_t, blk_t, blk_i, done, (int)G, st);
+      case 2: return launch_adj<2>(prob, idx, residual, out_t, best, best_t, blk_t, blk_i, done, (int)G, st);
+      case 3: return launch_adj<3>(prob, idx, residual, out_t, best, best_t, blk_t, blk_i, done, (int)G, st);
+      default: return launch_adj<4>(prob, idx, residual, out_t, best, best_t, blk_t, blk_i, done, (int)G, st);
+    }
+  }
+  const int64_t nblk = (prob->n + cpb - 1) / cpb;
   const dim3 grid((unsigned)nblk, (unsigned)prob->count);
   if (mode == 1)
     k_score_moves<1><<<grid, 32 * kScoreWarps, 0, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At,

@@ -12,6 +12,8 @@
 
 #include <cstdint>
 
+#include "../../include/amvm.h"
+
 #define AMVM_FULL 0xffffffffu
 
 namespace amvm {
@@ -73,6 +75,72 @@ __device__ __forceinline__ uint64_t pcg_bounded(Pcg &g, uint64_t rng) {
   return m >> 32;
 }
 
+
+// ------------------------------------------------ PCG64 state <-> amvm_pcg64
+__device__ __forceinline__ Pcg pcg_load(const amvm_pcg64 *st) {
+  // L2 reads: a chunked solve may have parked the state from another SM
+  const unsigned long long *q = (const unsigned long long *)st;
+  Pcg g;
+  g.s = ((unsigned __int128)__ldcg(q) << 64) | __ldcg(q + 1);
+  g.inc = ((unsigned __int128)__ldcg(q + 2) << 64) | __ldcg(q + 3);
+  g.has32 = __ldcg(&st->has_uint32);
+  g.u32 = __ldcg(&st->uinteger);
+  return g;
+}
+
+__device__ __forceinline__ void pcg_store(const Pcg &g, amvm_pcg64 *st) {
+  st->state_hi = (uint64_t)(g.s >> 64);
+  st->state_lo = (uint64_t)g.s;
+  st->inc_hi = (uint64_t)(g.inc >> 64);
+  st->inc_lo = (uint64_t)g.inc;
+  st->has_uint32 = g.has32;
+  st->uinteger = g.u32;
+}
+
+// ------------------------------------------------------- operator bank
+// select_operators (controller.py:88-90): rng.choice(4, p=w/sum(w)) = one
+// random(), numpy's sequential cdf of p (sum(w) is a pairwise sum; n < 8 so
+// sequential), normalised by cdf[-1], searchsorted(side='right').
+__device__ inline int bank_select(const double *w, Pcg &g) {
+  double s = 0.0;
+  for (int k = 0; k < 4; ++k) s = dadd(s, w[k]);
+  double cdf[4], acc = 0.0;
+  for (int k = 0; k < 4; ++k) {
+    acc = dadd(acc, ddiv(w[k], s));
+    cdf[k] = acc;
+  }
+  const double u = pcg_random(g);
+  int lo = 0, hi = 4;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (u < ddiv(cdf[mid], cdf[3])) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// update_weights (controller.py:99-131): outcome 0 new best, 1 improved,
+// 2 accepted, 3 rejected; every n_segment iterations
+// w = max(decay*w + (1-decay)*(scores/uses or 0), floor), segment reset.
+__device__ inline void bank_update(double *w, double *sc, int64_t *seg, int64_t *life, int64_t *bit, int pair,
+                                   int outcome, double s1, double s2, double s3, double decay, double floor_w,
+                                   int n_segment) {
+  const double pts = outcome == 0 ? s1 : outcome == 1 ? s2 : outcome == 2 ? s3 : 0.0;
+  sc[pair] = dadd(sc[pair], pts);
+  seg[pair] += 1;
+  life[pair] += 1;
+  *bit += 1;
+  if (*bit % n_segment == 0) {
+    const double keep = dsub(1.0, decay);
+    for (int k = 0; k < 4; ++k) {
+      const double nrm = seg[k] > 0 ? ddiv(sc[k], (double)seg[k]) : 0.0;
+      const double v = dadd(dmul(decay, w[k]), dmul(keep, nrm));
+      w[k] = v < floor_w ? floor_w : v;
+      sc[k] = 0.0;
+      seg[k] = 0;
+    }
+  }
+}
 
 // ----------------------------------------------------- exp for x <= 0
 // Table-driven exp (Tang, ACM TOMS 15, 1989): x = (32m + j) ln2/32 + r,

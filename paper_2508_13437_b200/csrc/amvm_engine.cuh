@@ -125,7 +125,8 @@ struct KArgs {
   int32_t x_cap, x_r;
 };
 
-enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR };
+enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR,
+       OP_APPLY_SHIFT, OP_APPLY_SWAP };
 
 struct WsHeader {  // 256 bytes
   int32_t status;
@@ -645,6 +646,8 @@ struct Engine {
 #ifndef AMVM_FC_STATS
             if (tid == 0) sh->c.pc[11] += 1;
 #endif
+            // raw count: candidates actually scored over all m rows
+            if (tid == 0) sh->c.mv_raw += (k > 0) + (k + 1 < nlev);
             int rm, rp;
             exact_pair_max(At + j * m, dm, dp, tm, tpv, rm, rp);
             int lvl = -1;
@@ -687,7 +690,6 @@ struct Engine {
             for (int w = 0; w < NW; ++w) cnt += sh->wsum[wpar][w];
           }
           sh->c.mv_ref += cnt;
-          sh->c.mv_raw += cnt;
           sh->c.pc[13] += 1;
         }
         wpar ^= 1;
@@ -1480,6 +1482,110 @@ struct Engine {
     bump_known(t);
   }
 
+  // apply_swap (core.py:228-245) when the new objective is not known:
+  // s += (x_i - x_j) * (A[:, j] - A[:, i]) (DSUB, DMUL, DADD), levels
+  // exchanged, then _bump (max |s|, or the refresh at REFRESH_PERIOD).
+  __device__ void apply_swap_reduce(int i, int j) {
+    AMVM_LOCALS
+    const int ki = cidx[i], kj = cidx[j];
+    const double d = dsub(lv[ki], lv[kj]);
+    const double *ci = At + (int64_t)i * m;
+    const double *cj = At + (int64_t)j * m;
+    double mx = 0.0;
+    for (int64_t r = tid; r < m; r += NT) {
+      const double y = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
+      cr[r] = y;
+      mx = fmax(mx, fabs(y));
+    }
+    const double t = block_max_own(mx);
+    if (tid == 0) {
+      cidx[i] = kj;
+      cidx[j] = ki;
+    }
+    __syncthreads();
+    ccnt += 1;
+    if (ccnt >= prm->refresh_period) refresh();
+    else cobj = t;
+  }
+
+  // ---------------------------------------- best_swap with the l2 tie-break
+  // localsearch.py:181-246 with FilterConfig.l2_tiebreak (not on the solve
+  // path: SolverConfig.filter_config does not forward it).  The candidate
+  // list (reference order) is split like np.array_split(.., min(workers,
+  // cnt)); each chunk's winner is its smallest improving t', ties inside
+  // the chunk going to the smallest (l2, i, j) with l2 =
+  // np.linalg.norm(shifted[tied], axis=1) = sqrt(pairwise sum of y*y); a
+  // chunk with a single tied candidate carries np.linalg.norm(shifted[k])
+  // = sqrt(ddot).  Winners merge by (t, l2, i, j).  Block-uniform loops,
+  // exact full scans: a correctness path, not a hot one.
+  __device__ double swap_t_block(const Cand &e) {
+    AMVM_LOCALS
+    const double *ci = At + (int64_t)e.i * m, *cj = At + (int64_t)e.j * m;
+    double mx = 0.0;
+    for (int64_t r = tid; r < m; r += NT) mx = fmax(mx, fabs(dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r))))));
+    return block_max_own(mx);
+  }
+
+  __device__ double swap_l2(const Cand &e, bool pairwise) {
+    AMVM_LOCALS
+    const double *ci = At + (int64_t)e.i * m, *cj = At + (int64_t)e.j * m;
+    auto y = [&](int64_t r) { return dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r)))); };
+    if (pairwise) {
+      const double s2 = block_pairwise([&](int64_t r) { const double v = y(r); return dmul(v, v); }, m, lf_lo,
+                                       lf_len, nleaf_m);
+      return __dsqrt_rn(s2);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const double dd = warp_ddot_skx(y, y, m, lane);
+      if (lane == 0) sh->bc_d[0] = __dsqrt_rn(dd);
+    }
+    __syncthreads();
+    const double v = sh->bc_d[0];
+    __syncthreads();
+    return v;
+  }
+
+  __device__ bool best_swap_l2(int workers, int &bi, int &bj, double &bd, double &bt) {
+    AMVM_LOCALS
+    if (!(cobj > 0.0)) return false;
+    const int cnt = find_candidates(true);
+    if (cnt == 0) return false;
+    const double t0 = cobj;
+    const int K = workers < cnt ? workers : cnt;
+    const int q = cnt / K, qr = cnt % K;
+    bool found = false;
+    double gl2 = 0.0;
+    for (int c = 0; c < K; ++c) {
+      const int c0 = c * q + (c < qr ? c : qr), c1 = c0 + q + (c < qr ? 1 : 0);
+      double tmin = t0;
+      int ntied = 0;
+      for (int e = c0; e < c1; ++e) {
+        const double tp = swap_t_block(cbuf[e]);
+        if (tp < t0) {
+          if (tp < tmin) { tmin = tp; ntied = 1; }
+          else if (tp == tmin) ++ntied;
+        }
+      }
+      if (ntied == 0) continue;
+      int wi = -1, wj = -1;
+      double wl2 = 0.0, wd = 0.0;
+      for (int e = c0; e < c1; ++e) {
+        const Cand ce = cbuf[e];
+        if (swap_t_block(ce) != tmin) continue;
+        const double l2 = swap_l2(ce, ntied > 1);
+        if (wi < 0 || l2 < wl2 || (l2 == wl2 && (ce.i < wi || (ce.i == wi && ce.j < wj)))) {
+          wi = ce.i; wj = ce.j; wl2 = l2; wd = ce.d;
+        }
+      }
+      if (!found || tmin < bt ||
+          (tmin == bt && (wl2 < gl2 || (wl2 == gl2 && (wi < bi || (wi == bi && wj < bj)))))) {
+        found = true; bt = tmin; gl2 = wl2; bi = wi; bj = wj; bd = wd;
+      }
+    }
+    return found;
+  }
+
   // local_search, localsearch.py:249-269
   __device__ void local_search() {
     AMVM_LOCALS
@@ -1927,44 +2033,14 @@ struct Engine {
   }
 
   // select_operators, controller.py:88-90 (thread 0)
-  __device__ int select_pair() {
-    AMVM_LOCALS
-    double s = 0.0;
-    for (int k = 0; k < 4; ++k) s = dadd(s, sh->c.w[k]);  // pairwise_sum, n < 8
-    double cdf[4], acc = 0.0;
-    for (int k = 0; k < 4; ++k) {
-      acc = dadd(acc, ddiv(sh->c.w[k], s));
-      cdf[k] = acc;
-    }
-    const double u = pcg_random(sh->rng);
-    int lo = 0, hi = 4;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (u < ddiv(cdf[mid], cdf[3])) hi = mid;
-      else lo = mid + 1;
-    }
-    return lo;
-  }
+  __device__ int select_pair() { return bank_select(sh->c.w, sh->rng); }
 
-  // update_weights, controller.py:99-131 (replicated in every thread)
+  // update_weights, controller.py:99-131 (thread 0 owns the bank)
   __device__ void update_weights(int pair, int outcome) {
     AMVM_LOCALS
     if (tid != 0) return;
-    const double pts = outcome == 0 ? prm->sigma1 : outcome == 1 ? prm->sigma2 : outcome == 2 ? prm->sigma3 : 0.0;
-    sh->c.sc[pair] = dadd(sh->c.sc[pair], pts);
-    sh->c.seg[pair] += 1;
-    sh->c.life[pair] += 1;
-    sh->c.bit += 1;
-    if (sh->c.bit % prm->n_segment == 0) {
-      const double keep = dsub(1.0, prm->decay);
-      for (int k = 0; k < 4; ++k) {
-        const double nrm = sh->c.seg[k] > 0 ? ddiv(sh->c.sc[k], (double)sh->c.seg[k]) : 0.0;
-        const double v = dadd(dmul(prm->decay, sh->c.w[k]), dmul(keep, nrm));
-        sh->c.w[k] = v < prm->weight_floor ? prm->weight_floor : v;
-        sh->c.sc[k] = 0.0;
-        sh->c.seg[k] = 0;
-      }
-    }
+    bank_update(sh->c.w, sh->c.sc, sh->c.seg, sh->c.life, &sh->c.bit, pair, outcome, prm->sigma1, prm->sigma2,
+                prm->sigma3, prm->decay, prm->weight_floor, prm->n_segment);
   }
 
   __device__ void cand_from_cur() {
@@ -2071,25 +2147,12 @@ struct Engine {
 
   __device__ void load_rng(const amvm_pcg64 *st) {
     AMVM_LOCALS
-    if (tid == 0) {  // L2 reads: a chunked solve may have parked it from another SM
-      const unsigned long long *q = (const unsigned long long *)st;
-      sh->rng.s = ((unsigned __int128)__ldcg(q) << 64) | __ldcg(q + 1);
-      sh->rng.inc = ((unsigned __int128)__ldcg(q + 2) << 64) | __ldcg(q + 3);
-      sh->rng.has32 = __ldcg(&st->has_uint32);
-      sh->rng.u32 = __ldcg(&st->uinteger);
-    }
+    if (tid == 0) sh->rng = pcg_load(st);
   }
 
   __device__ void store_rng(amvm_pcg64 *st) {
     AMVM_LOCALS
-    if (tid == 0) {
-      st->state_hi = (uint64_t)(sh->rng.s >> 64);
-      st->state_lo = (uint64_t)sh->rng.s;
-      st->inc_hi = (uint64_t)(sh->rng.inc >> 64);
-      st->inc_lo = (uint64_t)sh->rng.inc;
-      st->has_uint32 = sh->rng.has32;
-      st->uinteger = sh->rng.u32;
-    }
+    if (tid == 0) pcg_store(sh->rng, st);
   }
 
   // ------------------------------------------------------- solve (one inst)
@@ -2293,10 +2356,10 @@ struct Engine {
         if (tid == 0) *a.x_cnt = k;
         break;
       }
-      case OP_BEST_SWAP: {
+      case OP_BEST_SWAP: {  // kind = workers with the l2 tie-break, 0 without
         int bi = -1, bj = -1;
         double bd = 0, bt = 0;
-        const bool f = best_swap(bi, bj, bd, bt);
+        const bool f = a.kind > 0 ? best_swap_l2(a.kind, bi, bj, bd, bt) : best_swap(bi, bj, bd, bt);
         if (tid == 0) {
           a.x_out4[0] = f ? bi : -1;
           a.x_out4[1] = f ? bj : -1;
@@ -2321,6 +2384,14 @@ struct Engine {
         if (a.kind == 0) random_repair(a.x_i, a.x_saved, a.x_r);
         else greedy_repair(a.x_i, a.x_saved, a.x_r);
         store_rng(a.rng);
+        store_sol(a);
+        break;
+      case OP_APPLY_SHIFT:  // x_r = j, kind = new level (core.py:208-225)
+        apply_shift_reduce(a.x_r, a.kind);
+        store_sol(a);
+        break;
+      case OP_APPLY_SWAP:  // x_r = i, kind = j (core.py:228-245)
+        apply_swap_reduce(a.x_r, a.kind);
         store_sol(a);
         break;
       default:

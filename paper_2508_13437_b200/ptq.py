@@ -45,6 +45,7 @@ class LayerBatch:
 
     def __init__(self, X, W, bits: int = 4, rows=None, device=None):
         torch = N.torch_cuda()
+        N.check_blas_order()
         self.torch = torch
         self.lib = N.load_library()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)

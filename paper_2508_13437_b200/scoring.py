@@ -48,20 +48,40 @@ def score_moves_device(prob: "N.Problem", idx, residual, mode: str = "adjacent",
     idx int32 [count, n], residual float64 [count, m] -> (t [count, n, nv],
     best flat index int64 [count], best_t float64 [count]), all on device,
     asynchronous on the current stream.  ``ws``: optional uint8 device
-    workspace of at least ``amvm_score_workspace_bytes`` (allocated if
-    absent or short)."""
+    workspace of at least ``amvm_score_workspace_bytes``, zeroed before its
+    first use (allocated zeroed if absent or short).  Inputs are validated
+    (dtype, shape, contiguity, device, level range, finite residual; this
+    costs a device sync -- keep ``ws`` and call the C-ABI directly to time
+    the kernel alone)."""
     torch = N.torch_cuda()
     lib = N.load_library()
     if mode not in MODES:
         raise ValueError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
-    nv = 2 if mode == "adjacent" else int(prob.nlev)
+    count, m, n = int(prob.count), int(prob.m), int(prob.n)
     dev = idx.device
-    t = torch.empty((int(prob.count), int(prob.n), nv), dtype=torch.float64, device=dev)
-    best = torch.empty(int(prob.count), dtype=torch.int64, device=dev)
-    best_t = torch.empty(int(prob.count), dtype=torch.float64, device=dev)
+    # the kernel reads raw pointers: check dtype, shape, layout and device first
+    if idx.dtype != torch.int32 or tuple(idx.shape) != (count, n) or not idx.is_contiguous():
+        raise ValueError(f"idx must be a contiguous int32 tensor of shape ({count}, {n}), got "
+                         f"{idx.dtype} {tuple(idx.shape)}")
+    if (residual.dtype != torch.float64 or tuple(residual.shape) != (count, m)
+            or not residual.is_contiguous()):
+        raise ValueError(f"residual must be a contiguous float64 tensor of shape ({count}, {m}), got "
+                         f"{residual.dtype} {tuple(residual.shape)}")
+    if dev.type != "cuda" or residual.device != dev:
+        raise ValueError("idx and residual must be CUDA tensors on the same device")
+    if count and (int(idx.min()) < 0 or int(idx.max()) >= int(prob.nlev)):
+        raise ValueError(f"idx entries must lie in [0, {int(prob.nlev)})")
+    if not bool(torch.isfinite(residual).all()):
+        raise ValueError("residual must be finite")
+    nv = 2 if mode == "adjacent" else int(prob.nlev)
+    t = torch.empty((count, n, nv), dtype=torch.float64, device=dev)
+    best = torch.empty(count, dtype=torch.int64, device=dev)
+    best_t = torch.empty(count, dtype=torch.float64, device=dev)
     wsb = int(lib.amvm_score_workspace_bytes(N.C.byref(prob)))
     if ws is None or ws.numel() < wsb:
-        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)  # ticket counters start at zero
+    elif ws.dtype != torch.uint8 or ws.device != dev:
+        raise ValueError("ws must be a uint8 tensor on the same device (zeroed before its first use)")
     N.check(lib.amvm_score_moves(N.C.byref(prob), N.ptr(idx), N.ptr(residual), MODES[mode], N.ptr(t),
                                  N.ptr(best), N.ptr(best_t), N.ptr(ws), ws.numel(), N.stream_handle()),
             "amvm_score_moves")
@@ -75,6 +95,9 @@ def score_moves(inst: Instance, sol, mode: str = "adjacent") -> MoveScores:
     idx_h = np.asarray(sol.idx)
     if idx_h.shape != (inst.n,):
         raise ValueError(f"solution has {idx_h.size} indices, instance has n={inst.n}")
+    nlev = len(inst.values)
+    if idx_h.size and (idx_h.min() < 0 or idx_h.max() >= nlev):
+        raise ValueError(f"idx entries must lie in [0, {nlev})")
     res_h = np.asarray(sol.residual, dtype=np.float64)
     if res_h.shape != (inst.m,):
         raise ValueError(f"residual has {res_h.size} entries, instance has m={inst.m}")

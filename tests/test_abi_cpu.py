@@ -81,3 +81,55 @@ def test_seed_states_match_numpy_seedsequence():
     st = _native.seed_states(seeds)
     for k, s in enumerate(seeds):
         assert _native.pcg_to_state(st[k]) == np.random.default_rng(int(s)).bit_generator.state
+
+
+def test_blas_order_guard(monkeypatch):
+    """solve() refuses a host BLAS whose ddot/dgemv order the device does not
+    reproduce (the reference's trajectory there would differ), unless the
+    caller opts out."""
+    import paper_2508_13437_b200 as P
+    from paper_2508_13437_b200 import _native
+
+    inst = P.Instance(np.eye(2), np.array([0.3, 0.2]), P.ValueSet([0.0, 1.0]))
+    monkeypatch.setattr(_native, "_blas_checked", None)
+    monkeypatch.setattr(_native, "host_blas", lambda: {"internal_api": "openblas", "version": "0.3.30",
+                                                       "architecture": "Zen", "num_threads": 8})
+    monkeypatch.delenv("AMVM_ALLOW_BLAS_MISMATCH", raising=False)
+    with pytest.raises(_native.BlasOrderMismatch, match="Zen"):
+        P.solve(inst, P.SolverConfig(max_iters=0))
+    monkeypatch.setattr(_native, "host_blas", lambda: {"internal_api": "mkl", "architecture": None})
+    with pytest.raises(_native.BlasOrderMismatch):
+        P.solve(inst, P.SolverConfig(max_iters=0))
+    monkeypatch.setenv("AMVM_ALLOW_BLAS_MISMATCH", "1")
+    assert P.solve(inst, P.SolverConfig(max_iters=0)).iterations == 0
+    monkeypatch.setattr(_native, "_blas_checked", None)
+    monkeypatch.delenv("AMVM_ALLOW_BLAS_MISMATCH")
+    monkeypatch.setattr(_native, "host_blas", lambda: {"internal_api": "openblas", "architecture": "SkylakeX"})
+    assert _native.check_blas_order() == "SkylakeX"
+
+
+def test_api_validation_matches_reference():
+    """apply_shift / apply_swap / OperatorBank / update_weights reject bad
+    arguments with the reference's messages before touching the device
+    (core.py:215-238, controller.py:74-76, 115-120)."""
+    import paper_2508_13437_b200 as P
+
+    inst = P.Instance(np.eye(3), np.zeros(3), P.ValueSet([0.0, 1.0, 2.0]))
+    sol = P.Solution.from_indices(inst, np.array([0, 1, 1]))
+    with pytest.raises(ValueError, match="variable index 3 out of range for n=3"):
+        P.apply_shift(inst, sol, 3, 0)
+    with pytest.raises(ValueError, match="level index 3 out of range for 3 levels"):
+        P.apply_shift(inst, sol, 0, 3)
+    assert P.apply_shift(inst, sol, 1, 1) is sol and sol.updates_since_refresh == 0  # no-op, no device
+    with pytest.raises(ValueError, match="two distinct variables"):
+        P.apply_swap(inst, sol, 1, 1)
+    with pytest.raises(ValueError, match=r"swap indices \(0, 5\) out of range for n=3"):
+        P.apply_swap(inst, sol, 0, 5)
+    with pytest.raises(ValueError, match="swap of equal values"):
+        P.apply_swap(inst, sol, 1, 2)
+    with pytest.raises(ValueError, match="decay"):
+        P.OperatorBank(0.0)
+    bank = P.OperatorBank()
+    np.testing.assert_array_equal(bank.probabilities(), [0.25] * 4)
+    with pytest.raises(KeyError):
+        P.update_weights(bank, 0, "bogus")
