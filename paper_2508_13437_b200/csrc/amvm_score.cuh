@@ -43,7 +43,9 @@ __host__ __device__ constexpr int score_cols_per_cta(int mode) { return kScoreWa
 // here where numpy's max(abs(.)) propagates it.  Instance validates
 // finiteness; score_moves_device checks its residuals.
 __device__ __forceinline__ double score_amax(double m, double y) {
-  const double ay = fabs(y);
+  // |y| by clearing the sign bit (one LOP3 on the high word; fabs() can
+  // lower to a DADD -0, |y| on the FP64 pipe)
+  const double ay = __longlong_as_double(__double_as_longlong(y) & 0x7fffffffffffffffLL);
   return ay > m ? ay : m;
 }
 
@@ -211,35 +213,59 @@ __global__ void __launch_bounds__(256, MODE == 1 ? (AMVM_SCORE_UNROLL > 8 ? 2 : 
 // Adjacent-set scorer, HBM-streaming form (the north-star scorer (c) for the
 // reference's one_opt candidate set {idx-1, idx+1}, localsearch.py:70-80).
 //
-// Persistent grid (one 512-thread CTA per SM); CTA b owns a contiguous slab
-// of columns.  Columns are contiguous in the column-major At, so a stage of
-// CB columns is ONE contiguous CB*8m-byte chunk: thread 0 arms an mbarrier
-// with the byte count and issues a single cp.async.bulk (TMA bulk copy,
-// UBLKCP) of the chunk into a kScoreStages-deep shared-memory ring, so every
-// byte of A is read from HBM exactly once and ~100 KB per SM stay in flight.
-// Thread t owns rows t, t+512, ... (R <= kAdjMaxR): its residual entries
-// s_r live in registers for the whole call (read once), the column entries
-// come from shared memory (consecutive threads, consecutive doubles: no bank
-// conflicts).  Per element and candidate: DMUL, DADD (unfused, numpy's
-// order) and a compare+select abs-max.  The 2*CB maxima of a stage are
-// reduced in a warp by a transpose butterfly (each xor step halves the
-// values a lane carries: V-1 + 5-log2(V) shuffles for V = 2*CB maxima
-// instead of 5*V), then across the 16 warps through shared memory; one
-// __syncthreads per stage both publishes those partial maxima and frees the
-// stage's slot for the next bulk copy.  Best move per instance as in
-// k_score_moves (CTA slot + ticket, counter left at 0 for the next call).
-constexpr int kAdjThreads = 512;
+// Persistent grid (one CTA per SM); CTA b owns a contiguous slab of columns.
+// Columns are contiguous in the column-major At, so a stage of CB columns is
+// ONE contiguous CB*8m-byte chunk moved by a single cp.async.bulk (TMA bulk
+// copy, UBLKCP) into an S-deep shared-memory ring: every byte of A is read
+// from HBM once and ~128 KB per SM stay in flight.  Warp-specialised: one
+// producer warp arms each slot's `full` mbarrier with the byte count and
+// issues the copy once the slot's `empty` mbarrier says all 16 consumer
+// warps are done with it; consumers never wait on each other inside a slab.
+// Consumer thread t owns rows t, t+512, ...: its residual entries stay in
+// registers for the whole instance, the column entries come from shared
+// memory (consecutive threads, consecutive doubles: conflict-free).  Per
+// element and candidate: DMUL, DADD (unfused, numpy's order) and a
+// compare+select abs-max.  The 2*CB maxima of a stage are reduced in the
+// warp by a transpose butterfly (V-1 + 5-log2 V shuffles for V values
+// instead of 5V) and folded into per-column shared slots by 64-bit
+// atomicMax on the bit pattern (|y| >= 0: integer order = value order).
+// The candidate deltas (lv[idx±1] - lv[idx]) of the whole slab are built
+// once per instance in shared memory.  At the end of an instance's slab the
+// consumers finalise every column in parallel and the CTA's best move goes
+// to a workspace slot; the instance's last CTA (ticket) reduces the slots.
+#ifdef AMVM_SCORE_TIMELINE  // diagnostic builds: per-CTA %globaltimer stamps
+__device__ unsigned long long g_adj_tl[1024][8];
+__device__ unsigned long long g_adj_st[1024][2][16];  // per stage: producer issue, consumer warp 0 data ready
+__device__ __forceinline__ unsigned long long adj_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ADJ_TL(k) do { if (threadIdx.x == 0) g_adj_tl[blockIdx.x][k] = adj_now(); } while (0)
+#else
+#define ADJ_TL(k) do { } while (0)
+#endif
+constexpr int kAdjThreads = 512;      // consumer threads (largest variant; 256 also built)
 constexpr int kScoreMaxSlabs = 1024;  // persistent-grid cap (>= SM count)
-constexpr int kAdjMaxR = 16;         // rows per thread held in registers: m <= 8192
-constexpr int kScoreStages = 4;      // bulk-copy ring depth
-constexpr int kAdjStageTarget = 32768;  // bytes per stage (CB columns)
+constexpr int kAdjMaxR = 16;          // rows per thread held in registers: m <= 8192
+constexpr int kAdjMaxStages = 8;      // bulk-copy ring depth (max)
+#ifndef AMVM_SCORE_STAGE_BYTES
+#define AMVM_SCORE_STAGE_BYTES 65536
+#endif
+constexpr int kAdjStageTarget = AMVM_SCORE_STAGE_BYTES;  // bytes per stage (CB columns)
+constexpr size_t kAdjRingBudget = 196 * 1024;
 
 __host__ __device__ inline int adj_cols_per_stage(int64_t m) {
   const int64_t cb = kAdjStageTarget / (8 * m);
   return cb < 1 ? 1 : (cb > 4 ? 4 : (int)cb);
 }
-__host__ __device__ inline size_t adj_smem_bytes(int64_t m) {
-  return (size_t)kScoreStages * adj_cols_per_stage(m) * 8 * m + 64;
+__host__ __device__ inline int adj_stages(int64_t m, int cb) {
+  const int64_t st = (int64_t)kAdjRingBudget / ((int64_t)cb * 8 * m);
+  return st > kAdjMaxStages ? kAdjMaxStages : (int)st;  // >= 2 for m <= 8192
+}
+// ring + 2 x (delta pairs, column maxima) for the slab's columns + levels
+__host__ __device__ inline size_t adj_smem_bytes(int64_t m, int cb, int64_t slab_cols, int64_t nlev) {
+  return (size_t)adj_stages(m, cb) * cb * 8 * m + (size_t)2 * 32 * slab_cols + 8 * (size_t)nlev;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -251,6 +277,9 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
@@ -271,174 +300,227 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// named barrier among the consumer warps only (the producer warp runs free)
+template <int NC>
+__device__ __forceinline__ void adj_consumer_sync_n() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
+}
 
-// one butterfly step of the transpose reduction: a lane with bit `o` clear
-// keeps the lower half of its V values and sends the upper half, its partner
-// the reverse; both take the max of what they keep and what they receive.
-template <int V>
+// one butterfly step of the transpose reduction: a lane with bit `o` set
+// keeps the upper half of its VV values and sends the lower half, its
+// partner the reverse; both keep the max of what they hold and receive.
+template <int VV>
 __device__ __forceinline__ void adj_tr_step(double (&x)[8], int lane, int o) {
   const bool up = lane & o;
 #pragma unroll
-  for (int q = 0; q < V / 2; ++q) {
-    const double send = up ? x[q] : x[q + V / 2];
-    const double keep = up ? x[q + V / 2] : x[q];
+  for (int q = 0; q < VV / 2; ++q) {
+    const double send = up ? x[q] : x[q + VV / 2];
+    const double keep = up ? x[q + VV / 2] : x[q];
     const double got = __shfl_xor_sync(0xffffffffu, send, o);
     x[q] = got > keep ? got : keep;
   }
 }
 
-template <int CB>
-__global__ void __launch_bounds__(kAdjThreads, 1)
+template <int CB, int RT, int NC>
+__global__ void __launch_bounds__(NC + 32, 1)
     k_score_adj(int64_t m, int64_t n, int64_t nlev, int64_t count, const double *__restrict__ At,
                 const double *__restrict__ lvs, const int32_t *__restrict__ idxs, const double *__restrict__ S,
                 double *__restrict__ out_t, double *__restrict__ blk_t, int64_t *__restrict__ blk_i,
                 unsigned *__restrict__ done, int64_t *__restrict__ best, double *__restrict__ best_t) {
-  constexpr int NW = kAdjThreads / 32;
   constexpr int V = 2 * CB;  // maxima per stage: (column, lower/upper)
+  constexpr int NWc = NC / 32;
   extern __shared__ __align__(128) unsigned char adj_smem[];
-  __shared__ uint64_t full[kScoreStages];
-  __shared__ double red[2][NW][V];
-  __shared__ double sbt[V];
-  __shared__ int64_t sbi[V];
-  __shared__ bool last;
-  double *ring = (double *)adj_smem;
+  __shared__ uint64_t full[kAdjMaxStages], empty[kAdjMaxStages];
+  __shared__ double wbt[NWc];
+  __shared__ int64_t wbi[NWc];
+  __shared__ int last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t G = gridDim.x, b = blockIdx.x;
   const int64_t j0 = b * n / G, j1 = (b + 1) * n / G;  // this CTA's slab of columns
-  const int64_t ncol = j1 - j0;
-  const int64_t nst = (ncol + CB - 1) / CB;           // stages per instance
-  const int64_t stage_elems = (int64_t)CB * m;
-  const int R = (int)((m + kAdjThreads - 1) / kAdjThreads);
+  const int ncol = (int)(j1 - j0);
+  const int slab_max = (int)((n + G - 1) / G);
+  const int NS = adj_stages(m, CB);
+  const int nst = (ncol + CB - 1) / CB;  // stages per instance
+  const int m32 = (int)m;
+  const int stage_elems = CB * m32;
+  double *ring = (double *)adj_smem;
+  double2 *dtab = (double2 *)(ring + NS * stage_elems);                   // [2][slab_max] (dm, dp)
+  unsigned long long *cmax = (unsigned long long *)(dtab + 2 * slab_max);  // [2][slab_max][2]
+  double *slv = (double *)(cmax + 4 * slab_max);                          // [nlev] this instance's levels
   if (tid == 0) {
-    for (int q = 0; q < kScoreStages; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NWc);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t total = nst * count;  // (instance, stage) pairs, instance-major
-  auto issue = [&](int64_t g) {       // thread 0: bulk copy of pair g into its ring slot
-    const int64_t st = g % nst;
-    const int64_t jc = j0 + st * CB;
-    const int64_t nc = (j1 - jc) < CB ? (j1 - jc) : CB;
-    uint64_t *bar = &full[g % kScoreStages];
-    const uint32_t bytes = (uint32_t)(nc * m * 8);
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(ring + (g % kScoreStages) * stage_elems, At + jc * m, bytes, bar);
-  };
-  if (tid == 0)
-    for (int64_t g = 0; g < kScoreStages && g < total; ++g) issue(g);
-  // per-thread best (t, flat) over the values it finalises (tid < V)
-  double my_bt = 0.0;
-  int64_t my_bi = -1;
-  double s[kAdjMaxR];
-  int64_t cur_c = -1;
-  for (int64_t g = 0; g < total; ++g) {
-    const int64_t c = g / nst, st = g % nst;
-    if (c != cur_c) {  // new instance: its residual rows into registers
-      cur_c = c;
-#pragma unroll
-      for (int q = 0; q < kAdjMaxR; ++q) {
-        const int64_t r = tid + (int64_t)q * kAdjThreads;
-        s[q] = (q < R && r < m) ? __ldg(S + c * m + r) : 0.0;
+  ADJ_TL(0);
+  if (warp == NWc) {  // ---------------- producer warp: one lane issues every copy
+    // the consumers' first-instance loads (residual rows, levels, level
+    // indices: a few KB) go first; issued behind ~28 MB of bulk copies they
+    // would queue for microseconds (measured: 6 us vs ~1.5 us)
+    asm volatile("bar.sync 2, %0;" ::"n"(NC + 32) : "memory");
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t ph = 0;
+      int64_t issued = 0;
+      for (int64_t c = 0; c < count; ++c) {
+        for (int st = 0; st < nst; ++st, ++issued) {
+          if (issued >= NS) mbar_wait(&empty[slot], ph ^ 1u);
+          const int64_t jc = j0 + (int64_t)st * CB;
+          const int nc = (int)((j1 - jc) < CB ? (j1 - jc) : CB);
+          const uint32_t bytes = (uint32_t)nc * (uint32_t)m32 * 8u;
+          mbar_expect_tx(&full[slot], bytes);
+          bulk_g2s(ring + slot * stage_elems, At + jc * m, bytes, &full[slot]);
+#ifdef AMVM_SCORE_TIMELINE
+          if (issued < 16) g_adj_st[blockIdx.x][0][issued] = adj_now();
+#endif
+          if (++slot == NS) { slot = 0; ph ^= 1u; }
+        }
       }
     }
-    const int64_t jc = j0 + st * CB;
-    const int nc = (int)((j1 - jc) < CB ? (j1 - jc) : CB);
-    const double *lv = lvs + c * nlev;
-    double d[V];
+    return;
+  }
+  // ---------------- consumer warps (RT rows per thread, RT * NC >= m)
+  double s[RT];
+  int slot = 0;
+  uint32_t ph = 0;
+  for (int64_t c = 0; c < count; ++c) {
+    const int par = (int)(c & 1);
+    double2 *dt = dtab + par * slab_max;
+    unsigned long long *cm = cmax + par * 2 * slab_max;
+    // residual rows, the slab's level indices and the levels: independent
+    // loads issued together (one memory round trip), then the delta table
 #pragma unroll
-    for (int cc = 0; cc < CB; ++cc) {
-      const int k = cc < nc ? __ldg(idxs + c * n + jc + cc) : 0;
-      const double lk = __ldg(lv + k);
-      d[2 * cc] = (cc < nc && k > 0) ? __dsub_rn(__ldg(lv + k - 1), lk) : 0.0;
-      d[2 * cc + 1] = (cc < nc && k + 1 < nlev) ? __dsub_rn(__ldg(lv + k + 1), lk) : 0.0;
+    for (int q = 0; q < RT; ++q) {
+      const int r = tid + q * NC;
+      s[q] = r < m32 ? __ldg(S + c * m + r) : 0.0;
     }
-    double x[8];
+    for (int q = tid; q < nlev; q += NC) slv[q] = __ldg(lvs + c * nlev + q);
+    int kq = tid < ncol ? __ldg(idxs + c * n + j0 + tid) : 0;
+    adj_consumer_sync_n<NC>();  // levels staged
+    for (int q = tid; q < ncol; q += NC) {
+      const int k = q == tid ? kq : __ldg(idxs + c * n + j0 + q);
+      const double lk = slv[k];
+      dt[q] = make_double2(k > 0 ? __dsub_rn(slv[k - 1], lk) : 0.0, k + 1 < nlev ? __dsub_rn(slv[k + 1], lk) : 0.0);
+      cm[2 * q] = 0ull;
+      cm[2 * q + 1] = 0ull;
+    }
+    adj_consumer_sync_n<NC>();  // delta table and zeroed maxima visible
+    if (c == 0) asm volatile("bar.arrive 2, %0;" ::"n"(NC + 32) : "memory");  // release the producer
+    ADJ_TL(1);
+    for (int st = 0; st < nst; ++st) {
+      const int lc0 = st * CB;  // local column of the stage's first column
+      double2 d[CB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = 0.0;
-    mbar_wait(&full[g % kScoreStages], (uint32_t)((g / kScoreStages) & 1));
-    const double *col = ring + (g % kScoreStages) * stage_elems;
+      for (int cc = 0; cc < CB; ++cc) d[cc] = dt[lc0 + cc < ncol ? lc0 + cc : lc0];
+      double x[8];
 #pragma unroll
-    for (int q = 0; q < kAdjMaxR; ++q) {
-      const int64_t r = tid + (int64_t)q * kAdjThreads;
-      if (q < R && r < m) {
+      for (int u = 0; u < 8; ++u) x[u] = 0.0;
+      mbar_wait(&full[slot], ph);
+      if (st == 0) ADJ_TL(2);
+#ifdef AMVM_SCORE_TIMELINE
+      if (tid == 0 && c == 0 && st < 16) g_adj_st[blockIdx.x][1][st] = adj_now();
+#endif
+      const double *col = ring + slot * stage_elems + tid;
+      // all shared-memory loads of the stage first, then the arithmetic;
+      // rows past m contribute s = a = 0, i.e. |0| (no effect on a max >= 0);
+      // columns past the slab end read stale data that is never used
+      double a[CB][RT];
+#pragma unroll
+      for (int q = 0; q < RT; ++q) {
+        const bool ok = tid + q * NC < m32;
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) a[cc][q] = ok ? col[cc * m32 + q * NC] : 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp's reads of the slot are done
+      if (++slot == NS) { slot = 0; ph ^= 1u; }
+#ifdef AMVM_SCORE_NOCOMPUTE  // diagnostic build: stream only
+      if (a[0][0] == 12345.0) x[0] = 1.0;
+      else continue;
+#endif
+#pragma unroll
+      for (int q = 0; q < RT; ++q) {
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc) {
-          const double a = col[cc * m + r];  // rows beyond nc read stale smem: never used
-          x[2 * cc] = score_amax(x[2 * cc], __dadd_rn(s[q], __dmul_rn(d[2 * cc], a)));
-          x[2 * cc + 1] = score_amax(x[2 * cc + 1], __dadd_rn(s[q], __dmul_rn(d[2 * cc + 1], a)));
+          x[2 * cc] = score_amax(x[2 * cc], __dadd_rn(s[q], __dmul_rn(d[cc].x, a[cc][q])));
+          x[2 * cc + 1] = score_amax(x[2 * cc + 1], __dadd_rn(s[q], __dmul_rn(d[cc].y, a[cc][q])));
         }
       }
-    }
-    // warp: transpose butterfly, V values -> lane groups
-    int o = 16;
-    if (V >= 8) { adj_tr_step<8>(x, lane, o); o >>= 1; }
-    if (V >= 4) { adj_tr_step<4>(x, lane, o); o >>= 1; }
-    if (V >= 2) { adj_tr_step<2>(x, lane, o); o >>= 1; }
-    for (; o; o >>= 1) {
-      const double y = __shfl_xor_sync(0xffffffffu, x[0], o);
-      x[0] = y > x[0] ? y : x[0];
-    }
-    // lane's value index: its top log2(V) lane bits (bit 4 selects the upper half first)
-    const int vb = V == 8 ? 3 : V == 4 ? 2 : 1;
-    const int vid = lane >> (5 - vb);  // step o = 16 decided the top bit of the value index, and so on
-    if ((lane & ((32 >> vb) - 1)) == 0) red[g & 1][warp][vid] = x[0];
-    __syncthreads();  // partial maxima visible; every thread is done with this ring slot
-    if (tid == 0 && g + kScoreStages < total) issue(g + kScoreStages);
-    if (tid < V) {
-      const int cc = tid >> 1, u = tid & 1;
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) t = red[g & 1][w][tid] > t ? red[g & 1][w][tid] : t;
-      if (cc < nc) {
-        const int64_t j = jc + cc;
-        const int k = __ldg(idxs + c * n + j);
-        const bool live = u == 0 ? k > 0 : k + 1 < nlev;
-        out_t[(c * n + j) * 2 + u] = live ? t : __longlong_as_double(0x7ff0000000000000LL);
-        if (live && score_better(t, j * 2 + u, my_bt, my_bi)) { my_bt = t; my_bi = j * 2 + u; }
+      int o = 16;
+      if (V >= 8) { adj_tr_step<8>(x, lane, o); o >>= 1; }
+      if (V >= 4) { adj_tr_step<4>(x, lane, o); o >>= 1; }
+      adj_tr_step<2>(x, lane, o);
+      o >>= 1;
+      for (; o; o >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, x[0], o);
+        x[0] = y > x[0] ? y : x[0];
       }
+      // value index = the lane bits decided by the halving steps (o = 16 the top one)
+      constexpr int vb = V == 8 ? 3 : V == 4 ? 2 : 1;
+      const int vid = lane >> (5 - vb);
+      if ((lane & ((32 >> vb) - 1)) == 0 && lc0 + (vid >> 1) < ncol)
+        atomicMax(&cm[2 * (lc0 + (vid >> 1)) + (vid & 1)], (unsigned long long)__double_as_longlong(x[0]));
     }
-    if (st == nst - 1) {  // instance c done in this slab: CTA best -> slot, ticket
-      if (tid < V) { sbt[tid] = my_bt; sbi[tid] = my_bi; }
-      __syncthreads();
+    ADJ_TL(3);
+    adj_consumer_sync_n<NC>();  // every column's maxima complete
+    ADJ_TL(4);
+    // the CTA's best over level-changing moves, from the shared maxima only
+    // (a neighbour level exists iff its delta is nonzero: levels strictly
+    // increase), so the ticket below orders no other global store
+    double bt = 0.0;
+    int64_t bi = -1;
+    for (int q = tid; q < 2 * ncol; q += NC) {
+      const int64_t j = j0 + (q >> 1);
+      const int u = q & 1;
+      const bool live = (u == 0 ? dt[q >> 1].x : dt[q >> 1].y) != 0.0;
+      const double t = __longlong_as_double((long long)cm[q]);
+      if (live && score_better(t, j * 2 + u, bt, bi)) { bt = t; bi = j * 2 + u; }
+    }
+    score_warp_best(bt, bi);
+    if (lane == 0) { wbt[warp] = bt; wbi[warp] = bi; }
+    adj_consumer_sync_n<NC>();
+    if (tid == 0) {
+      for (int w = 1; w < NWc; ++w)
+        if (!score_better(bt, bi, wbt[w], wbi[w])) { bt = wbt[w]; bi = wbi[w]; }
+      blk_t[c * G + b] = bt;
+      blk_i[c * G + b] = bi;
+      unsigned prev;  // release: the slot above is visible before the ticket; acquire: all earlier slots
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done + c) : "memory");
+      last = prev == (unsigned)(G - 1);
+    }
+    // the scores themselves, while the ticket is in flight
+    for (int q = tid; q < 2 * ncol; q += NC) {
+      const int64_t j = j0 + (q >> 1);
+      const int u = q & 1;
+      const bool live = (u == 0 ? dt[q >> 1].x : dt[q >> 1].y) != 0.0;
+      out_t[(c * n + j) * 2 + u] = live ? __longlong_as_double((long long)cm[q])
+                                        : __longlong_as_double(0x7ff0000000000000LL);
+    }
+    adj_consumer_sync_n<NC>();
+    ADJ_TL(5);
+    if (last) {  // the instance's last CTA: reduce every slab's best
+      bt = 0.0;
+      bi = -1;
+      for (int64_t e = tid; e < G; e += NC) {
+        const double xv = __ldcg(blk_t + c * G + e);
+        const int64_t iv = __ldcg(blk_i + c * G + e);
+        if (score_better(xv, iv, bt, bi)) { bt = xv; bi = iv; }
+      }
+      score_warp_best(bt, bi);
+      if (lane == 0) { wbt[warp] = bt; wbi[warp] = bi; }
+      adj_consumer_sync_n<NC>();
       if (tid == 0) {
-        double bt = sbt[0];
-        int64_t bi = sbi[0];
-        for (int q = 1; q < V; ++q)
-          if (!score_better(bt, bi, sbt[q], sbi[q])) { bt = sbt[q]; bi = sbi[q]; }
-        blk_t[c * G + b] = bt;
-        blk_i[c * G + b] = bi;
-        __threadfence();
-        last = atomicAdd(&done[c], 1u) == (unsigned)(G - 1);
+        for (int w = 1; w < NWc; ++w)
+          if (!score_better(bt, bi, wbt[w], wbi[w])) { bt = wbt[w]; bi = wbi[w]; }
+        ADJ_TL(6);
+        best[c] = bi;
+        best_t[c] = bi < 0 ? __longlong_as_double(0x7ff0000000000000LL) : bt;
+        done[c] = 0u;  // ready for the next call on this workspace
       }
-      __syncthreads();
-      my_bt = 0.0;
-      my_bi = -1;
-      if (last) {  // the instance's last CTA: reduce every slab's best
-        __threadfence();
-        double bt = 0.0;
-        int64_t bi = -1;
-        for (int64_t e = tid; e < G; e += kAdjThreads) {
-          const double xv = __ldcg(blk_t + c * G + e);
-          const int64_t iv = __ldcg(blk_i + c * G + e);
-          if (score_better(xv, iv, bt, bi)) { bt = xv; bi = iv; }
-        }
-        score_warp_best(bt, bi);
-        if (lane == 0) { red[0][warp][0] = bt; ((int64_t *)red[1][warp])[0] = bi; }
-        __syncthreads();
-        if (tid == 0) {
-          bt = red[0][0][0];
-          bi = ((int64_t *)red[1][0])[0];
-          for (int w = 1; w < NW; ++w) {
-            const double xv = red[0][w][0];
-            const int64_t iv = ((int64_t *)red[1][w])[0];
-            if (!score_better(bt, bi, xv, iv)) { bt = xv; bi = iv; }
-          }
-          best[c] = bi;
-          best_t[c] = bi < 0 ? __longlong_as_double(0x7ff0000000000000LL) : bt;
-          done[c] = 0u;
-        }
-        __syncthreads();
-      }
+      adj_consumer_sync_n<NC>();
     }
   }
 }

@@ -27,7 +27,10 @@ def P():
 
 
 CASES = [(64, 16, 5), (1, 7, 4), (31, 9, 3), (33, 1, 6), (100, 40, 16), (257, 33, 17), (5, 6, 1),
-         (2048, 96, 16), (300, 20, 1024), (128, 64, 2)]
+         (2048, 96, 16), (300, 20, 1024), (128, 64, 2),
+         # k_score_adj (adjacent set, even m <= 8192): 1..4 columns per stage,
+         # up to 16 rows per thread, more slabs than SMs, fewer columns than SMs
+         (8192, 37, 16), (4096, 300, 16), (1500, 600, 16), (1000, 1000, 8), (6000, 5, 3), (2, 3, 4)]
 
 
 def _instance(P, m, n, nlev, seed, integer=False):
@@ -107,3 +110,60 @@ def test_bad_mode_is_a_value_error(P):
     inst, sol = _instance(P, 8, 4, 3, 1)
     with pytest.raises(ValueError, match="mode must be one of"):
         P.score_moves(inst, sol, "every")
+
+
+def test_adjacent_batch_and_workspace_reuse(P):
+    """Several instances per k_score_adj launch (every slab CTA walks all of
+    them; per-instance tickets) and back-to-back calls on one workspace (the
+    kernel leaves its ticket counters at zero)."""
+    import torch
+
+    from paper_2508_13437_b200 import _native as N
+    from paper_2508_13437_b200.scoring import score_moves_device
+
+    rng = np.random.default_rng(9)
+    m, n, nlev, count = 2048, 700, 16, 3
+    A = rng.normal(0, 1, (m, n))
+    LV = np.sort(rng.normal(0, 1, (count, nlev)), axis=1)
+    dev = torch.device("cuda", 0)
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).to(dev)
+    lv = torch.from_numpy(LV).to(dev)
+    B = torch.zeros((count, m), dtype=torch.float64, device=dev)
+    prob = N.Problem(m, n, nlev, count, At.data_ptr(), B.data_ptr(), lv.data_ptr())
+    ws = torch.zeros(int(N.load_library().amvm_score_workspace_bytes(N.C.byref(prob))), dtype=torch.uint8,
+                     device=dev)
+    for rep in range(3):
+        IDX = rng.integers(0, nlev, (count, n))
+        S = rng.normal(0, 0.5, (count, m))
+        t, best, best_t = score_moves_device(prob, torch.from_numpy(IDX.astype(np.int32)).to(dev),
+                                             torch.from_numpy(S).to(dev), "adjacent", ws)
+        t = t.cpu().numpy()
+        for c in range(count):
+            tr, br, btr = O.score_moves(A, S[c], LV[c], IDX[c], "adjacent")
+            np.testing.assert_array_equal(t[c], tr)
+            j, v = divmod(int(best[c]), 2)
+            assert (j, IDX[c, j] + (-1 if v == 0 else 1)) == br and float(best_t[c]) == btr, (rep, c)
+
+
+def test_device_api_rejects_bad_inputs(P):
+    import torch
+
+    from paper_2508_13437_b200 import _native as N
+    from paper_2508_13437_b200.scoring import score_moves_device
+
+    dev = torch.device("cuda", 0)
+    m, n, nlev = 16, 8, 4
+    At = torch.zeros((n, m), dtype=torch.float64, device=dev)
+    lv = torch.arange(nlev, dtype=torch.float64, device=dev)[None]
+    B = torch.zeros((1, m), dtype=torch.float64, device=dev)
+    prob = N.Problem(m, n, nlev, 1, At.data_ptr(), B.data_ptr(), lv.data_ptr())
+    s = torch.zeros((1, m), dtype=torch.float64, device=dev)
+    idx = torch.zeros((1, n), dtype=torch.int32, device=dev)
+    with pytest.raises(ValueError, match="int32"):
+        score_moves_device(prob, idx.long(), s)
+    with pytest.raises(ValueError, match="float64"):
+        score_moves_device(prob, idx, s.float())
+    with pytest.raises(ValueError, match="lie in"):
+        score_moves_device(prob, idx + nlev, s)
+    with pytest.raises(ValueError, match="finite"):
+        score_moves_device(prob, idx, s * float("nan"))

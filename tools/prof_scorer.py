@@ -11,4 +11,4 @@ import bench  # noqa: E402
 X, _ = bench.layer_rows(0, 1)
 dev = torch.device("cuda", 0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-print(bench.scorer_roofline(X, dev, flush, reps=1, batch=64))
+print(bench.scorer_roofline(X, dev, flush, reps=int(os.environ.get("REPS", "20")), batch=64))
