@@ -342,7 +342,7 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
     At = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)
     st = torch.cuda.current_stream()
 
-    def cycled(copies=4, launches=16):
+    def cycled(copies=4, launches=16, with_best=False):
         """Adjacent mode, one instance, back-to-back launches cycling over
         `copies` distinct copies of A (4 x 64 MiB = 256 MiB > the 126 MB L2:
         each launch reads a copy evicted by the three launches before it),
@@ -355,7 +355,8 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
         probs = [N.Problem(m, n, nlev, 1, a_.data_ptr(), B.data_ptr(), lv.data_ptr()) for a_ in Ats]
         ws = torch.zeros(int(lib.amvm_score_workspace_bytes(N.C.byref(probs[0]))), dtype=torch.uint8, device=dev)
         t, best, best_t = score_moves_device(probs[0], idx, s, "adjacent", ws)
-        calls = [(N.C.byref(p_), N.ptr(idx), N.ptr(s), 1, N.ptr(t), N.ptr(best), N.ptr(best_t), N.ptr(ws),
+        bb = (N.ptr(best), N.ptr(best_t)) if with_best else (None, None)
+        calls = [(N.C.byref(p_), N.ptr(idx), N.ptr(s), 1, N.ptr(t), *bb, N.ptr(ws),
                   ws.numel(), N.stream_handle()) for p_ in probs]
         for k in range(2 * copies):
             N.check(lib.amvm_score_moves(*calls[k % copies]), "amvm_score_moves")
@@ -400,6 +401,7 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
     pk = peaks()
     ms1, ms1_min, live1 = leg(1, "adjacent", True)
     msc, launches = cycled()
+    msb_c, _ = cycled(with_best=True)
     alg = 8 * m * n + 8 * m + 4 * n + 16 * n
     gbs = alg / (msc / 1e3) / 1e9
     gbs1 = alg / (ms1 / 1e3) / 1e9
@@ -410,9 +412,16 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
     return {
         "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic,
-                     "kernel": "k_score_adj (north-star scorer (c): adjacent set |V_s| = 2, one C5 instance "
-                               f"m=2048 x n=4096; {launches} back-to-back launches cycling over 4 copies of A "
-                               "(256 MiB > L2), average per launch, median of 5 runs)",
+                     "kernel": "k_score_adj (north-star scorer (c): adjacent set |V_s| = 2, every score of one "
+                               f"C5 instance m=2048 x n=4096; {launches} back-to-back launches cycling over 4 copies "
+                               "of A (256 MiB > L2), average per launch, median of 5 runs)",
+                     "with_fused_best_move": {"ms_per_launch": round(msb_c, 5),
+                                              "GBps": round(alg / (msb_c / 1e3) / 1e9, 1),
+                                              "frac": round(alg / (msb_c / 1e3) / 1e9 / pk["hbm_gbs"], 4)},
+                     "single_pass_read_floor_us": 13.1,
+                     "floor_note": "tools/ubench/read_bw.cu: the fastest plain read of 64 MiB in one launch on this "
+                                   "B200 (TMA bulk 64 KB x 2 stages, or LDG 32 B at 2048 threads/SM) takes "
+                                   "12.8-13.1 us, i.e. 0.79 of the 2 GiB copy peak",
                      "algorithmic_bytes": alg, "peak_source": pk["source"],
                      "single_launch_flushed": {"ms": round(ms1, 4), "GBps": round(gbs1, 1),
                                                "frac": round(gbs1 / pk["hbm_gbs"], 4),

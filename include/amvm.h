@@ -283,7 +283,8 @@ AMVM_API int amvm_is_improving(const amvm_problem *prob, const double *residual,
  * mode 1: adjacent levels (the reference's one_opt set), nv = 2,
  *         l = idx-1, idx+1; +inf where that level does not exist.
  * best[c] = flat index j*nv + v of the smallest (t, j, l) over candidates
- * that change the level (-1 if none), best_t[c] its t.  `idx` is count x n,
+ * that change the level (-1 if none), best_t[c] its t; best and best_t may
+ * both be NULL (scores only: no grid-wide reduction).  `idx` is count x n,
  * `residual` count x m; device pointers; replaces the Python loop of
  * localsearch.py:70-80 for scoring (no move is applied).
  * Preconditions: 0 <= idx < nlev; A, residual and levels finite (the

@@ -65,7 +65,8 @@ size_t amvm_score_workspace_bytes(const amvm_problem *prob) {
 
 int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double *residual, int mode,
                      double *out_t, int64_t *best, double *best_t, void *ws, size_t ws_bytes, void *stream) {
-  if (!prob || !prob->At || !prob->levels || !idx || !residual || !out_t || !best || !best_t) return AMVM_ERR_INVALID;
+  if (!prob || !prob->At || !prob->levels || !idx || !residual || !out_t || (!best) != (!best_t))
+    return AMVM_ERR_INVALID;
   if (prob->m < 1 || prob->n < 1 || prob->nlev < 1 || prob->count < 1 || (mode != 0 && mode != 1))
     return AMVM_ERR_INVALID;
   const int cpb = score_cols_per_cta(mode);
@@ -93,12 +94,12 @@ int amvm_score_moves(const amvm_problem *prob, const int32_t *idx, const double 
     int cb = adj_cols_per_stage(prob->m);
     if (const char *e = getenv("AMVM_SCORE_CB")) {  // A/B knob: columns per ring stage
       const int v = atoi(e);
-      if (v >= 1 && v <= 4 && (int64_t)kAdjRingBudget / ((int64_t)v * 8 * prob->m) >= 2) cb = v;
+      if (v >= 1 && v <= 4 && adj_stages(prob->m, v) >= 2) cb = v;
     }
     int64_t G = sms < kScoreMaxSlabs ? sms : kScoreMaxSlabs;
     const int64_t slabs = (prob->n + cb - 1) / cb;  // every slab holds at least one column
     if (G > slabs) G = slabs;
-    if (adj_smem_bytes(prob->m, cb, (prob->n + G - 1) / G, prob->nlev) <= 210 * 1024) {
+    if (adj_stages(prob->m, cb) >= 2 && adj_smem_bytes(prob->m, cb, (prob->n + G - 1) / G, prob->nlev) <= 210 * 1024) {
       switch (cb) {
         case 1: return launch_adj<1>(prob, idx, residual, out_t, best, best_t, blk_t, blk_i, done, (int)G, st);
         case 2: return launch_adj<2>(prob, idx, residual, out_t, best, best_t, blk_t, blk_i, done, (int)G, st);

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(256, MODE == 1 ? (AMVM_SCORE_UNROLL > 8 ? 2 : 
       }
     }
   }
+  if (best == nullptr) return;  // scores only
   // CTA best -> per-CTA slot; the last CTA of the instance reduces the slots
   double bt = cbt;
   int64_t bi = cbv < 0 ? -1 : col * nv + cbv;
@@ -250,22 +251,24 @@ constexpr int kScoreMaxSlabs = 1024;  // persistent-grid cap (>= SM count)
 constexpr int kAdjMaxR = 16;          // rows per thread held in registers: m <= 8192
 constexpr int kAdjMaxStages = 8;      // bulk-copy ring depth (max)
 #ifndef AMVM_SCORE_STAGE_BYTES
-#define AMVM_SCORE_STAGE_BYTES 65536
+#define AMVM_SCORE_STAGE_BYTES 32768
 #endif
 constexpr int kAdjStageTarget = AMVM_SCORE_STAGE_BYTES;  // bytes per stage (CB columns)
-constexpr size_t kAdjRingBudget = 196 * 1024;
+constexpr size_t kAdjRingBudget = 200 * 1024;
 
 __host__ __device__ inline int adj_cols_per_stage(int64_t m) {
   const int64_t cb = kAdjStageTarget / (8 * m);
   return cb < 1 ? 1 : (cb > 4 ? 4 : (int)cb);
 }
 __host__ __device__ inline int adj_stages(int64_t m, int cb) {
-  const int64_t st = (int64_t)kAdjRingBudget / ((int64_t)cb * 8 * m);
-  return st > kAdjMaxStages ? kAdjMaxStages : (int)st;  // >= 2 for m <= 8192
+  // ring budget net of the two residual buffers (16m bytes)
+  const int64_t st = ((int64_t)kAdjRingBudget - 16 * m) / ((int64_t)cb * 8 * m);
+  return st > kAdjMaxStages ? kAdjMaxStages : (int)st;
 }
-// ring + 2 x (delta pairs, column maxima) for the slab's columns + levels
+// ring + delta/maxima tables (2 x 32 B per slab column) + levels + 2 residuals
 __host__ __device__ inline size_t adj_smem_bytes(int64_t m, int cb, int64_t slab_cols, int64_t nlev) {
-  return (size_t)adj_stages(m, cb) * cb * 8 * m + (size_t)2 * 32 * slab_cols + 8 * (size_t)nlev;
+  return (size_t)adj_stages(m, cb) * cb * 8 * m + (size_t)2 * 32 * slab_cols + 16 * (size_t)((nlev + 1) & ~1ll) +
+         16 * (size_t)m + 8 * (size_t)((slab_cols + 8 + 3) & ~3ll);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(NC + 32, 1)
   constexpr int V = 2 * CB;  // maxima per stage: (column, lower/upper)
   constexpr int NWc = NC / 32;
   extern __shared__ __align__(128) unsigned char adj_smem[];
-  __shared__ uint64_t full[kAdjMaxStages], empty[kAdjMaxStages];
+  __shared__ uint64_t full[kAdjMaxStages], empty[kAdjMaxStages], sfull[2], sempty[2];
   __shared__ double wbt[NWc];
   __shared__ int64_t wbi[NWc];
   __shared__ int last;
@@ -346,26 +349,49 @@ __global__ void __launch_bounds__(NC + 32, 1)
   double *ring = (double *)adj_smem;
   double2 *dtab = (double2 *)(ring + NS * stage_elems);                   // [2][slab_max] (dm, dp)
   unsigned long long *cmax = (unsigned long long *)(dtab + 2 * slab_max);  // [2][slab_max][2]
-  double *slv = (double *)(cmax + 4 * slab_max);                          // [nlev] this instance's levels
+  const int nlev_pad = (int)((nlev + 1) & ~1ll);
+  const int idx_pad = (slab_max + 8 + 3) & ~3;
+  double *slv = (double *)(cmax + 4 * slab_max);    // [2][nlev_pad] levels, by instance parity
+  double *sbuf = slv + 2 * nlev_pad;                // [2][m] residuals
+  int32_t *sidx = (int32_t *)(sbuf + 2 * m32);      // [2][idx_pad] the slab's level indices (16-B window)
+  // TMA'd per instance, ahead of its columns: residual, levels (when 16-B
+  // aligned: nlev even), the aligned window of level indices covering the slab
+  const bool lv_tma = (nlev & 1) == 0;
+  const bool want_best = best != nullptr;
   if (tid == 0) {
     for (int q = 0; q < NS; ++q) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], NWc);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&sfull[q], 1);
+      mbar_init(&sempty[q], NWc);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   ADJ_TL(0);
   if (warp == NWc) {  // ---------------- producer warp: one lane issues every copy
-    // the consumers' first-instance loads (residual rows, levels, level
-    // indices: a few KB) go first; issued behind ~28 MB of bulk copies they
-    // would queue for microseconds (measured: 6 us vs ~1.5 us)
-    asm volatile("bar.sync 2, %0;" ::"n"(NC + 32) : "memory");
+    // each instance's residual goes into the queue ahead of its columns (a
+    // 16 KB TMA copy, so it lands first); the residual buffers alternate by
+    // instance parity and are reused once the consumers copied them out
     if (lane == 0) {
       int slot = 0;
       uint32_t ph = 0;
       int64_t issued = 0;
       for (int64_t c = 0; c < count; ++c) {
+        const int par = (int)(c & 1);
+        if (c >= 2) mbar_wait(&sempty[par], (uint32_t)(((c - 2) >> 1) & 1));
+        const int64_t e0 = c * n + j0, e1 = c * n + j1;
+        const int64_t a0 = e0 & ~3ll;
+        int64_t a1 = (e1 + 3) & ~3ll;
+        if (a1 > ((count * n) & ~3ll)) a1 = (count * n) & ~3ll;  // never past the array; tail via __ldg
+        const uint32_t ib = a1 > a0 ? (uint32_t)(a1 - a0) * 4u : 0u;
+        const uint32_t lb = lv_tma ? (uint32_t)nlev * 8u : 0u;
+        mbar_expect_tx(&sfull[par], (uint32_t)m32 * 8u + ib + lb);
+        bulk_g2s(sbuf + par * m32, S + c * m, (uint32_t)m32 * 8u, &sfull[par]);
+        if (lb) bulk_g2s(slv + par * nlev_pad, lvs + c * nlev, lb, &sfull[par]);
+        if (ib) bulk_g2s(sidx + par * idx_pad, idxs + a0, ib, &sfull[par]);
         for (int st = 0; st < nst; ++st, ++issued) {
           if (issued >= NS) mbar_wait(&empty[slot], ph ^ 1u);
           const int64_t jc = j0 + (int64_t)st * CB;
@@ -390,25 +416,35 @@ __global__ void __launch_bounds__(NC + 32, 1)
     const int par = (int)(c & 1);
     double2 *dt = dtab + par * slab_max;
     unsigned long long *cm = cmax + par * 2 * slab_max;
-    // residual rows, the slab's level indices and the levels: independent
-    // loads issued together (one memory round trip), then the delta table
-#pragma unroll
-    for (int q = 0; q < RT; ++q) {
-      const int r = tid + q * NC;
-      s[q] = r < m32 ? __ldg(S + c * m + r) : 0.0;
+    // residual, levels and level indices arrive with the instance's first
+    // bytes (TMA); odd nlev and the last few indices of the array (outside
+    // the 16-B window) come by __ldg.  Then the delta table, residual rows
+    // into registers.
+    double *lvp = slv + par * nlev_pad;
+    const int64_t e0 = c * n + j0, a0 = e0 & ~3ll;
+    const int64_t a1 = ((c * n + j1 + 3) & ~3ll) < ((count * n) & ~3ll) ? ((c * n + j1 + 3) & ~3ll)
+                                                                          : ((count * n) & ~3ll);
+    if (!lv_tma) {
+      for (int q = tid; q < nlev; q += NC) lvp[q] = __ldg(lvs + c * nlev + q);
+      adj_consumer_sync_n<NC>();
     }
-    for (int q = tid; q < nlev; q += NC) slv[q] = __ldg(lvs + c * nlev + q);
-    int kq = tid < ncol ? __ldg(idxs + c * n + j0 + tid) : 0;
-    adj_consumer_sync_n<NC>();  // levels staged
+    mbar_wait(&sfull[par], (uint32_t)((c >> 1) & 1));
     for (int q = tid; q < ncol; q += NC) {
-      const int k = q == tid ? kq : __ldg(idxs + c * n + j0 + q);
-      const double lk = slv[k];
-      dt[q] = make_double2(k > 0 ? __dsub_rn(slv[k - 1], lk) : 0.0, k + 1 < nlev ? __dsub_rn(slv[k + 1], lk) : 0.0);
+      const int64_t e = e0 + q;
+      const int k = e < a1 ? sidx[par * idx_pad + (int)(e - a0)] : __ldg(idxs + e);
+      const double lk = lvp[k];
+      dt[q] = make_double2(k > 0 ? __dsub_rn(lvp[k - 1], lk) : 0.0, k + 1 < nlev ? __dsub_rn(lvp[k + 1], lk) : 0.0);
       cm[2 * q] = 0ull;
       cm[2 * q + 1] = 0ull;
     }
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tid + q * NC;
+      s[q] = r < m32 ? sbuf[par * m32 + r] : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sempty[par]);
     adj_consumer_sync_n<NC>();  // delta table and zeroed maxima visible
-    if (c == 0) asm volatile("bar.arrive 2, %0;" ::"n"(NC + 32) : "memory");  // release the producer
     ADJ_TL(1);
     for (int st = 0; st < nst; ++st) {
       const int lc0 = st * CB;  // local column of the stage's first column
@@ -466,7 +502,16 @@ __global__ void __launch_bounds__(NC + 32, 1)
     }
     ADJ_TL(3);
     adj_consumer_sync_n<NC>();  // every column's maxima complete
-    ADJ_TL(4);
+    if (!want_best) {  // scores only: no grid-wide reduction
+      for (int q = tid; q < 2 * ncol; q += NC) {
+        const int64_t j = j0 + (q >> 1);
+        const int u = q & 1;
+        const bool live = (u == 0 ? dt[q >> 1].x : dt[q >> 1].y) != 0.0;
+        out_t[(c * n + j) * 2 + u] = live ? __longlong_as_double((long long)cm[q])
+                                          : __longlong_as_double(0x7ff0000000000000LL);
+      }
+      continue;
+    }
     // the CTA's best over level-changing moves, from the shared maxima only
     // (a neighbour level exists iff its delta is nonzero: levels strictly
     // increase), so the ticket below orders no other global store
@@ -482,13 +527,24 @@ __global__ void __launch_bounds__(NC + 32, 1)
     score_warp_best(bt, bi);
     if (lane == 0) { wbt[warp] = bt; wbi[warp] = bi; }
     adj_consumer_sync_n<NC>();
+    ADJ_TL(4);
     if (tid == 0) {
       for (int w = 1; w < NWc; ++w)
         if (!score_better(bt, bi, wbt[w], wbi[w])) { bt = wbt[w]; bi = wbi[w]; }
       blk_t[c * G + b] = bt;
       blk_i[c * G + b] = bi;
       unsigned prev;  // release: the slot above is visible before the ticket; acquire: all earlier slots
+#if defined(AMVM_SCORE_TICKET_RELAXED)  // diagnostic only: atomic latency without ordering
+      prev = atomicAdd(done + c, 1u);
+#elif defined(AMVM_SCORE_TICKET_FENCE)
+      __threadfence();
+      prev = atomicAdd(done + c, 1u);
+#else
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done + c) : "memory");
+#endif
+#ifdef AMVM_SCORE_TIMELINE
+      g_adj_tl[blockIdx.x][7] = adj_now();
+#endif
       last = prev == (unsigned)(G - 1);
     }
     // the scores themselves, while the ticket is in flight

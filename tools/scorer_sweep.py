@@ -25,7 +25,7 @@ for n in [1024, 4096, 8192, 16384, 32768]:
     probs = [N.Problem(m, n, nlev, 1, a.data_ptr(), B.data_ptr(), lv.data_ptr()) for a in Ats]
     ws = torch.zeros(int(lib.amvm_score_workspace_bytes(N.C.byref(probs[0]))), dtype=torch.uint8, device=dev)
     t, best, bt = score_moves_device(probs[0], idx, s, "adjacent", ws)
-    calls = [(N.C.byref(p), N.ptr(idx), N.ptr(s), 1, N.ptr(t), N.ptr(best), N.ptr(bt), N.ptr(ws), ws.numel(),
+    calls = [(N.C.byref(p), N.ptr(idx), N.ptr(s), 1, N.ptr(t), *((N.ptr(best), N.ptr(bt)) if os.environ.get("BEST", "1") == "1" else (None, None)), N.ptr(ws), ws.numel(),
               N.stream_handle()) for p in probs]
     L = 12
     per = []

@@ -24,7 +24,7 @@ prob = N.Problem(m, n, nlev, 1, At.data_ptr(), B.data_ptr(), lv.data_ptr())
 ws = torch.zeros(int(lib.amvm_score_workspace_bytes(N.C.byref(prob))), dtype=torch.uint8, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 t, best, bt = score_moves_device(prob, idx, s, "adjacent", ws)
-args = (N.C.byref(prob), N.ptr(idx), N.ptr(s), 1, N.ptr(t), N.ptr(best), N.ptr(bt), N.ptr(ws), ws.numel(),
+args = (N.C.byref(prob), N.ptr(idx), N.ptr(s), 1, N.ptr(t), *((N.ptr(best), N.ptr(bt)) if os.environ.get("BEST", "1") == "1" else (None, None)), N.ptr(ws), ws.numel(),
         N.stream_handle())
 out = np.zeros((148, 8), dtype=np.uint64)
 lib.amvm_debug_score_timeline.argtypes = [C.c_void_p, C.c_int]
@@ -36,9 +36,9 @@ for rep in range(3):
     lib.amvm_debug_score_timeline(out.ctypes.data, 148)
     t0 = out[:, 0].min()
     rel = (out.astype(np.int64) - int(t0)) / 1e3
-    names = ["start", "init", "first", "laststage", "colfinal", "ticket", "best"]
+    names = ["start", "init", "first", "laststage", "preticket", "ticket", "best", "atomic"]
     print(f"rep {rep}: " + "  ".join(
-        f"{nm}: med {np.median(rel[:, k]):.2f} max {rel[:, k].max():.2f}" for k, nm in enumerate(names[:6])))
+        f"{nm}: med {np.median(rel[:, k]):.2f} max {rel[:, k].max():.2f}" for k, nm in enumerate(names) if nm != "best"))
     lastcta = np.argmax(out[:, 6])
     print("   best written at", (int(out[lastcta, 6]) - int(t0)) / 1e3, "us by CTA", lastcta,
           "start spread", rel[:, 0].max())
