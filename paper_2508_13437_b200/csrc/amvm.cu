@@ -440,6 +440,7 @@ struct Plan {
   size_t slot_bytes;
   int64_t slots;
   size_t ist_bytes;  // per parked instance (chunked solve), 0 otherwise
+  size_t icache_bytes;  // per instance impact-score cache (solve), 0 for ops
   int chunk_iters;
   size_t ws_bytes;
 };
@@ -538,8 +539,10 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   // iterations so instances migrate between CTAs and the tail is one chunk
   P->chunk_iters = (!op && p->count > P->slots && prm->max_iters > kChunkIters) ? kChunkIters : 0;
   P->ist_bytes = P->chunk_iters ? inst_layout(p->m, p->n).total : 0;
+  P->icache_bytes = op ? 0 : al256((size_t)8 * p->n);
   P->ws_bytes = sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
-                (size_t)P->slots * P->slot_bytes + (size_t)p->count * P->ist_bytes;
+                (size_t)P->slots * P->slot_bytes + (size_t)p->count * P->ist_bytes +
+                (size_t)p->count * P->icache_bytes + (op ? 0 : al256((size_t)4 * p->count));
   return AMVM_OK;
 }
 
@@ -566,6 +569,13 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
   a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
                             (size_t)P.slots * P.slot_bytes
                       : nullptr;
+  if (P.icache_bytes) {
+    unsigned char *ib = a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
+                        (size_t)P.slots * P.slot_bytes + (size_t)p->count * P.ist_bytes;
+    a.icache = ib;
+    a.icache_bytes = P.icache_bytes;
+    a.ivalid = (int32_t *)(ib + (size_t)p->count * P.icache_bytes);
+  }
   a.cr_smem = P.cr_smem; a.tab = P.tab; a.cap = P.cap;
   a.time_budget_ns = prm->time_limit_s < 0 ? -1 : (int64_t)(prm->time_limit_s * 1e9);
   return a;

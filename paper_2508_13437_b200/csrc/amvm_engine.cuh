@@ -123,6 +123,11 @@ struct KArgs {
   int32_t *x_saved;
   double *x_d, *x_out4;
   int32_t x_cap, x_r;
+  // impact-score cache (solve only): per instance the scores of its CURRENT
+  // solution and a valid flag; null for the component ops
+  unsigned char *icache;
+  size_t icache_bytes;
+  int32_t *ivalid;
 };
 
 enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR,
@@ -329,6 +334,8 @@ struct Shared {
   uint64_t skey[NT];
   int sidx[NT];
   int64_t task_inst, task_chunk;  // k_solve: the task being run (kept out of registers)
+  double *ic;                      // this instance's impact cache (null: no caching)
+  int32_t *iv;                     // ... and its valid flag
   int nfilter_rows, srt_rows_sorted;  // select_rows result (rows[] count, ordered by |s| desc)
   int task_live, task_skip;
   Pcg rng;
@@ -1869,10 +1876,26 @@ struct Engine {
       random_destroy(r);
       return;
     }
-    impact_scores(alpha);
+    // The candidate is a copy of the CURRENT solution here (cand_from_cur, or
+    // cand_is_cur after an accept), and the current one changes only on an
+    // accept (a few % of iterations), so the scores of the current solution
+    // are cached per instance and reused until the next accept: same inputs,
+    // same deterministic computation, same bits.
+    double *const ic = sh->ic;
+    if (ic && __ldcg(sh->iv) == 1) {
+      for (int64_t k = tid; k < n; k += NT) dbuf[k] = __ldcg(ic + k);
+      __syncthreads();
+    } else {
+      impact_scores(alpha);
 #ifndef AMVM_FC_STATS
-    if (tid == 0) sh->c.pc[14] += 1;
+      if (tid == 0) sh->c.pc[14] += 1;
 #endif
+      if (ic) {
+        for (int64_t k = tid; k < n; k += NT) ic[k] = dbuf[k];
+        __syncthreads();
+        if (tid == 0) *sh->iv = 1;
+      }
+    }
     auto gd = [&](int64_t k) { return dbuf[k]; };
     if (block_pairwise(gd, n, lf_lo + nleaf_m, lf_len + nleaf_m, nleaf_n) <= 0.0) {
       random_destroy(r);
@@ -2171,6 +2194,11 @@ struct Engine {
     const InstLayout IL = inst_layout(m, n);
     int it = 0;
     int64_t elapsed = 0;
+    if (tid == 0) {
+      sh->ic = a.icache ? (double *)(a.icache + inst * a.icache_bytes) : nullptr;
+      sh->iv = a.icache ? a.ivalid + inst : nullptr;
+      if (a.icache && chunk == 0) *sh->iv = 0;  // a new start solution
+    }
     if (chunk == 0) {
       for (int64_t i = tid; i < m; i += NT) ur[i] = a.s_r[inst * m + i];
       for (int64_t j = tid; j < n; j += NT) uidx[j] = a.s_idx[inst * n + j];
@@ -2257,6 +2285,7 @@ struct Engine {
       if (acc) {
         cur_from_cand();
         cand_is_cur = true;
+        if (tid == 0 && sh->iv) *sh->iv = 0;  // the cached scores belonged to the old current
         __syncthreads();
         if (uobj < bobj) write_best(inst, res);
       }
@@ -2335,6 +2364,7 @@ struct Engine {
 
   __device__ void run_op(const KArgs &a) {
     AMVM_LOCALS
+    if (tid == 0) { sh->ic = nullptr; sh->iv = nullptr; }
     load_sol(a);
     switch (a.op) {
       case OP_ONE_OPT:
