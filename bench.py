@@ -56,6 +56,7 @@ def parse():
                          "~5 s per C5 row-iteration per core)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttr", action="store_true", help="skip the wall-time-to-reference-l_inf leg")
+    ap.add_argument("--no-legs", action="store_true", help="skip the C4-layer and C3-slices legs")
     return ap.parse_args()
 
 
@@ -517,7 +518,11 @@ def run_amvm(args, rank, world):
                                 "exact row screens avoid streaming most columns, so this exceeds DRAM bytes",
               "bytes_per_move": bytes_per_move, "V_s": 2,
               "phase_share": {nm: round(float(v / pc.sum()), 4) for nm, v in zip(PHASES, pc)} if pc.sum() else {},
-              "busy_gcycles_per_step": round(float(pc.sum()) / 1e9 / args.steps, 3)}
+              "busy_gcycles_per_step": round(float(pc.sum()) / 1e9 / args.steps, 3),
+              "events_per_row_iteration": {nm: round(float(v) / row_its, 3) for nm, v in zip(
+                  ["find_candidates_calls", "fc_survivors", "swaps_applied", "one_opt_exact_scans", "one_opt_moves",
+                   "one_opt_windows", "impact_computations", "refreshes"], phase[8:16])},
+              "cycles_per_row_iteration": {nm: round(float(v) / row_its) for nm, v in zip(PHASES, pc)}}
     if tr:
         phys = tr["dram_bytes_per_row_iteration"] * row_its / (dev_ms / 1e3) / 1e9
         ksolve.update({"physical_dram_GBps": round(phys, 1), "physical_frac": round(phys / pk["hbm_gbs"], 4),
@@ -569,10 +574,141 @@ def run_amvm(args, rank, world):
         sc = scorer_roofline(X, dev, flush)
         line["roofline"] = sc.pop("roofline")
         line["scorer"] = sc
+        if not args.no_legs:
+            line["workloads"] = {"c4_layer": c4_leg(dev), "c3_slices": c3_leg(dev)}
     print(json.dumps(line), flush=True)
     if not par["bitwise"]:
         print(f"PARITY FAILURE: {par['mismatches']}", file=sys.stderr)
         sys.exit(3)
+
+
+def c4_leg(dev) -> dict:
+    """BASELINE configs[3]: PTQ of the OPT-125M-shaped 768x3072 layer (int4,
+    2048 calibration tokens), the WHOLE layer (3072 rows x 100 iterations)
+    in one batched solve, device time; bitwise parity of rows 0 and 3071
+    (full-depth goldens from the unmodified reference); CPU port sample."""
+    import torch
+
+    from paper_2508_13437_b200 import SolverConfig, ptq
+
+    X = np.random.default_rng(0).standard_normal((2048, 768))
+    W = np.random.default_rng(1).standard_normal((3072, 768)) * 0.02
+    lb = ptq.LayerBatch(X, W, bits=4, device=dev)
+    lb.prepare()
+    cfg = SolverConfig(max_iters=100)
+    lb.solve(cfg)  # warm-up
+    lb.check_status()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    o = lb.solve(cfg, trace=True)
+    b.record()
+    torch.cuda.synchronize()
+    lb.check_status()
+    ms = a.elapsed_time(b)
+    mv = o["moves_scored"].sum(dim=0).cpu().numpy()
+    par = {"rows": [], "bitwise": True}
+    from tests.golden_io import load
+    for rec in load("layer_c4"):
+        r = int(rec["row"])
+        it = int(rec["iterations"])
+        ok = (int(o["iterations"][r]) == it and float(o["best_objective"][r]) == rec["best_objective"]
+              and np.array_equal(o["best_idx"][r].cpu().numpy(), rec["best_idx"])
+              and np.array_equal(o["trace_current_t"][r, :it].cpu().numpy(), rec["trace_current_t"]))
+        par["rows"].append(r)
+        par["bitwise"] &= bool(ok)
+    # CPU port: 16 rows x 2 iterations, all host threads
+    from threadpoolctl import threadpool_limits
+
+    from oracle import oracle as O
+    threads = len(os.sched_getaffinity(0))
+    rows = 16
+    B, L, I0, R0, OB = [], [], [], [], []
+    with threadpool_limits(1):
+        for w in W[:rows]:
+            lv = np.linspace(w.min(), w.max(), 16)
+            bb = X @ w
+            idx = np.argmin(np.abs(w[:, None] - lv[None, :]), axis=1)
+            rr = X @ lv[idx] - bb
+            B.append(bb); L.append(lv); I0.append(idx); R0.append(rr); OB.append(float(np.max(np.abs(rr))))
+    prm = O.make_params(768, max_iters=2)
+    t0 = time.perf_counter()
+    co = O.solve(X, np.stack(B), np.stack(L), np.stack(I0), np.stack(R0), np.array(OB), np.zeros(rows), prm,
+                 [O.pcg_from_seed(r) for r in range(rows)], threads=threads)
+    dt = time.perf_counter() - t0
+    cmv = int(co["moves_scored"][:, 0].sum())
+    prefix_ok = all(np.array_equal(o["trace_current_t"][r, :2].cpu().numpy(), co["trace_current_t"][r, :2])
+                    for r in range(rows))
+    par["oracle_prefix_rows"] = rows
+    par["bitwise"] &= bool(prefix_ok)
+    return {"metric": METRIC, "value": float(mv[0]) / (ms / 1e3), "unit": "moves/s",
+            "config": "C4: PTQ OPT-125M-shaped 768x3072 int4 layer, 2048 synthetic calib tokens, "
+                      "all 3072 rows x 100 ALNS iterations, one GPU",
+            "device_ms": round(ms, 2), "row_iterations_per_s": 3072 * 100 / (ms / 1e3),
+            "moves_scored_raw": int(mv[1]), "parity": par,
+            "cpu_baseline": {"value": cmv / dt, "unit": "moves/s", "cores": threads, "kind": "port",
+                             "sample": f"{rows} rows x 2 iterations of the C4 layer in {dt:.2f} s"}}
+
+
+def c3_leg(dev, side: int = 128, n_angles: int = 64, slices: int = 148, iters: int = 3) -> dict:
+    """BASELINE configs[2] family: discrete tomography slices (3 grey levels,
+    squares/disk/checker phantoms, eta = 5% of the max row sum, 100 SIRT
+    iterations) sharing one parallel-beam projector, at 128^2 x 64 angles
+    (m=8192, n=16384; the full 256^2 x 180 slice needs the dense engine's
+    48 GB), `slices` slices x `iters` iterations in one
+    batched solve.  Slice 0 (seed 0, squares) is the reference's own C3m
+    instance: bitwise parity with its golden.  CPU: the port on the 64^2 x 45
+    reference instance (C3s golden), 1 core."""
+    import torch
+
+    from paper_2508_13437_b200 import SolverConfig, tomo
+    from tests.golden_io import load, stored_A
+
+    import warnings
+
+    csr = tomo.projection_csr_device(side, n_angles, dev)
+    m, n = n_angles * side, side * side
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        A = torch.sparse_csr_tensor(*csr, size=(m, n), dtype=torch.float64).to_dense()
+    # eta = 5% of the max row sum, in numpy's order on the dense matrix (make_golden.py)
+    eta = 0.05 * float(A.cpu().numpy().sum(axis=1).max())
+    kinds = ("squares", "disk", "checker")
+    t0 = time.perf_counter()
+    fe = tomo.build_tomo_device(side, (0.0, 1.0, 2.0), n_angles, eta, seeds=tuple(range(slices)),
+                                phantom_kinds=kinds, sirt_iters=100, device=dev)
+    sb = tomo.SliceBatch(A, fe["B"].cpu().numpy(), fe["levels"], fe["idx0"].cpu().numpy(), device=dev)
+    del A
+    torch.cuda.synchronize()
+    fe_s = time.perf_counter() - t0
+    cfg = SolverConfig(max_iters=iters)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    o = sb.solve(cfg, seeds=np.arange(slices))
+    b.record()
+    torch.cuda.synchronize()
+    sb.check_status()
+    ms = a.elapsed_time(b)
+    mv = o["moves_scored"].sum(dim=0).cpu().numpy()
+    rec = load("solve_c3m")[0]
+    par = {"slice": 0, "bitwise": bool(
+        int(o["iterations"][0]) == int(rec["iterations"]) and float(o["best_objective"][0]) == rec["best_objective"]
+        and np.array_equal(o["best_idx"][0].cpu().numpy(), rec["best_idx"]))}
+    from oracle import oracle as O
+    r3 = load("solve_c3s")[0]
+    A3 = stored_A(r3)
+    prm = O.make_params(A3.shape[1], max_iters=1)
+    t1 = time.perf_counter()
+    O.solve(A3, r3["b"], r3["levels"], r3["idx0"], r3["r0"], r3["obj0"], 0, prm, O.pcg_from_seed(0), threads=1)
+    cdt = time.perf_counter() - t1
+    return {"metric": "slice-iterations/s", "value": slices * iters / (ms / 1e3), "unit": "slice-iterations/s",
+            "config": f"C3 family: {slices} tomography slices {side}^2 x {n_angles} angles (m={m}, n={n}, "
+                      f"3 grey levels) sharing one projector, {iters} ALNS iterations each, one GPU",
+            "device_ms": round(ms, 2), "moves_scored_per_s": float(mv[0]) / (ms / 1e3),
+            "front_end_s": round(fe_s, 2), "parity": par,
+            "seeds": "slice k: phantom kinds[k % 3], noise seed k, ALNS seed k (slice 0 = the reference's C3m run)",
+            "cpu_baseline": {"value": 1.0 / cdt, "unit": "slice-iterations/s", "cores": 1, "kind": "port",
+                             "sample": f"1 iteration of the 64^2 x 45 C3s reference instance in {cdt:.2f} s "
+                                       "(the 128^2 slice costs ~48 s per iteration in the Python reference)"}}
 
 
 def run_e2e(args, X, W, lo, hi, cfg, world):

@@ -150,6 +150,25 @@ class LayerBatch:
         N.check(self.lib.amvm_status(N.ptr(self._ws), N.stream_handle()), "amvm_solve")
 
 
+def layer_report(rows, host: dict, levels: np.ndarray, seconds: dict | None = None) -> LayerReport:
+    """Assemble a LayerReport from per-row HOST arrays in the device result
+    layout (best_idx, best_objective, initial_objective, iterations,
+    moves_scored, optionally the trace_* arrays): codes narrowed to int8 for
+    <= 128 levels (int16 otherwise)."""
+    nlev = levels.shape[1]
+    code_t = np.int8 if nlev <= 128 else np.int16
+    rep = LayerReport(
+        rows=np.asarray(rows), codes=np.asarray(host["best_idx"]).astype(code_t),
+        levels=np.asarray(levels), objective=np.asarray(host["best_objective"]),
+        initial_objective=np.asarray(host["initial_objective"]), iterations=np.asarray(host["iterations"]),
+        moves_scored=np.asarray(host["moves_scored"]), seconds=dict(seconds or {}),
+    )
+    if "trace_current_t" in host:
+        rep.seconds["trace"] = {k: host[k] for k in ("trace_current_t", "trace_best_t", "trace_pair",
+                                                     "trace_accepted")}
+    return rep
+
+
 def solve_layer(X, W, bits: int = 4, cfg: SolverConfig | None = None, rows=None, seeds=None,
                 device=None, trace: bool = False) -> LayerReport:
     """Quantize the rows of W (all, or ``rows``) against calibration X on the GPU."""
@@ -167,73 +186,24 @@ def solve_layer(X, W, bits: int = 4, cfg: SolverConfig | None = None, rows=None,
     host = {k: o[k].cpu().numpy() for k in keep}
     code_t = torch.int8 if lb.nlev <= 128 else torch.int16
     host["best_idx"] = o["best_idx"].to(code_t).cpu().numpy()
-    rep = LayerReport(
-        rows=lb.rows, codes=host["best_idx"],
-        levels=lb.L.cpu().numpy(), objective=host["best_objective"],
-        initial_objective=host["initial_objective"], iterations=host["iterations"],
-        moves_scored=host["moves_scored"], seconds={"device_pipeline": t1 - t0},
-    )
-    if trace:
-        rep.seconds["trace"] = {k: host[k] for k in ("trace_current_t", "trace_best_t", "trace_pair",
-                                                     "trace_accepted")}
-    del torch
-    return rep
+    return layer_report(lb.rows, host, lb.L.cpu().numpy(), {"device_pipeline": t1 - t0})
 
 
 def shard_rows(total: int, rank: int, world: int) -> np.ndarray:
     """Contiguous row shard of ``rank``: rows [r*T/W, (r+1)*T/W)."""
-    lo = (total * rank) // world
-    hi = (total * (rank + 1)) // world
-    return np.arange(lo, hi)
+    from .shard import shard_rows as _s
+
+    return _s(total, rank, world)
 
 
-def gather_layer(rep: LayerReport, total_rows: int, group=None) -> LayerReport | None:
+def gather_layer(rep: LayerReport, total_rows: int, group=None) -> LayerReport:
     """All-gather every rank's shard results (the only inter-GPU traffic, one
-    collective at the end).  Works on NCCL (GPU tensors) and gloo (CPU)."""
-    import torch
-    import torch.distributed as dist
+    collective per field at the end; NCCL on GPUs, gloo on CPU)."""
+    from .shard import gather_rows
 
-    if not dist.is_initialized():
-        return rep
-    world = dist.get_world_size(group)
-    backend = dist.get_backend(group)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    n = rep.codes.shape[1]
-    nlev = rep.levels.shape[1]
-    maxr = (total_rows + world - 1) // world
-    k = rep.rows.size
-
-    def pad(a, width, dtype):
-        out = torch.zeros((maxr, width), dtype=dtype, device=dev)
-        out[:k] = torch.as_tensor(np.asarray(a).reshape(k, width), dtype=dtype).to(dev)
-        return out
-
-    payload = [
-        pad(rep.rows, 1, torch.int64),
-        # codes travel as uint8 for <= 256 levels (int4: 58.7 MB for all of C5), else int32
-        (pad(rep.codes.astype(np.uint8), n, torch.uint8) if nlev <= 256
-         else pad(rep.codes.astype(np.int32), n, torch.int32)),
-        pad(rep.levels, nlev, torch.float64), pad(rep.objective, 1, torch.float64),
-        pad(rep.initial_objective, 1, torch.float64), pad(rep.iterations, 1, torch.int64),
-        pad(rep.moves_scored, 2, torch.int64),
-    ]
-    counts = torch.tensor([k], dtype=torch.int64, device=dev)
-    all_counts = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(all_counts, counts, group=group)
-    gathered = []
-    for t in payload:
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t, group=group)
-        gathered.append(parts)
-    cnts = [int(c.item()) for c in all_counts]
-
-    def cat(i):
-        return np.concatenate([gathered[i][w][:cnts[w]].cpu().numpy() for w in range(world)])
-
-    rows = cat(0)[:, 0]
-    order = np.argsort(rows, kind="stable")
-    return LayerReport(
-        rows=rows[order], codes=cat(1)[order].astype(rep.codes.dtype), levels=cat(2)[order],
-        objective=cat(3)[order, 0], initial_objective=cat(4)[order, 0], iterations=cat(5)[order, 0],
-        moves_scored=cat(6)[order], seconds=dict(rep.seconds),
-    )
+    rows, f = gather_rows(rep.rows, {"codes": rep.codes, "levels": rep.levels, "objective": rep.objective,
+                                     "initial_objective": rep.initial_objective, "iterations": rep.iterations,
+                                     "moves_scored": rep.moves_scored}, total_rows, group)
+    return LayerReport(rows=rows, codes=f["codes"], levels=f["levels"], objective=f["objective"],
+                       initial_objective=f["initial_objective"], iterations=f["iterations"],
+                       moves_scored=f["moves_scored"], seconds=dict(rep.seconds))

@@ -18,6 +18,9 @@ the GPU through ``solve`` / ``solve_from``.
 
 from __future__ import annotations
 
+import time
+from dataclasses import dataclass, field
+
 import numpy as np
 
 _EPS = 1e-12  # builders.py:195 — degenerate-direction and zero-length cut-off
@@ -275,3 +278,77 @@ def build_tomo_device(side: int, gray_levels, n_angles: int, noise: float, seeds
     lvd = torch.from_numpy(lv).to(dev)
     idx0 = torch.argmin(torch.abs(warm[:, :, None] - lvd[None, None, :]), dim=2).to(torch.int32)
     return {"csr": csr, "B": B, "warm": warm, "idx0": idx0, "truth": truth, "levels": lv, "m": m, "n": n}
+
+
+# ----------------------------------------------------------- many slices
+@dataclass
+class SliceReport:
+    """Per-slice results of a tomography batch (one reference ``solve`` per
+    slice, builders.py:302-318): slice ids, best level indices (int8), best
+    and initial l_inf, iterations, candidate moves scored (reference-
+    equivalent, raw)."""
+
+    slices: np.ndarray
+    codes: np.ndarray
+    objective: np.ndarray
+    initial_objective: np.ndarray
+    iterations: np.ndarray
+    moves_scored: np.ndarray
+    seconds: dict = field(default_factory=dict)
+
+
+def slice_report(slices, host: dict, seconds: dict | None = None) -> SliceReport:
+    """Assemble a SliceReport from per-slice HOST arrays in the device result
+    layout (best_idx, best_objective, initial_objective, iterations,
+    moves_scored)."""
+    return SliceReport(slices=np.asarray(slices), codes=np.asarray(host["best_idx"]).astype(np.int8),
+                       objective=np.asarray(host["best_objective"]),
+                       initial_objective=np.asarray(host["initial_objective"]),
+                       iterations=np.asarray(host["iterations"]), moves_scored=np.asarray(host["moves_scored"]),
+                       seconds=dict(seconds or {}))
+
+
+def solve_slices(side: int, gray_levels, n_angles: int, noise: float, slices, phantom_kinds=("disk",),
+                 cfg=None, sirt_iters: int = 500, device=None) -> SliceReport:
+    """Solve the tomography slices ``slices`` (global ids: slice k uses
+    phantom_kinds[k % len], noise seed k and ALNS seed k) of one projector
+    geometry on this GPU: device front end (projector, projections, SIRT
+    start), one batched ALNS solve, report.  Shard ``slices`` across ranks
+    with ``shard.shard_rows`` and assemble with :func:`gather_slices`."""
+    from . import _native as N
+    from .controller import SolverConfig
+
+    torch = N.torch_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    slices = np.asarray(slices, dtype=np.int64)
+    kinds = tuple(phantom_kinds[int(k) % len(phantom_kinds)] for k in slices)
+    t0 = time.perf_counter()
+    fe = build_tomo_device(side, gray_levels, n_angles, noise, seeds=tuple(int(k) for k in slices),
+                           phantom_kinds=kinds, sirt_iters=sirt_iters, device=dev)
+    m, n = fe["m"], fe["n"]
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        A = torch.sparse_csr_tensor(*fe["csr"], size=(m, n), dtype=torch.float64).to_dense()
+    sb = SliceBatch(A, fe["B"].cpu().numpy(), fe["levels"], fe["idx0"].cpu().numpy(), device=dev)
+    del A
+    o = sb.solve(cfg or SolverConfig(), seeds=slices)
+    sb.check_status()
+    t1 = time.perf_counter()
+    host = {k: o[k].cpu().numpy() for k in ("best_objective", "initial_objective", "iterations", "moves_scored")}
+    host["best_idx"] = o["best_idx"].to(torch.int8).cpu().numpy()
+    return slice_report(slices, host, {"device_pipeline": t1 - t0})
+
+
+def gather_slices(rep: SliceReport, total: int, group=None) -> SliceReport:
+    """All-gather every rank's slice results (one collective per field; NCCL
+    on GPUs, gloo on CPU) into one report ordered by slice id."""
+    from .shard import gather_rows
+
+    ids, f = gather_rows(rep.slices, {"codes": rep.codes, "objective": rep.objective,
+                                      "initial_objective": rep.initial_objective, "iterations": rep.iterations,
+                                      "moves_scored": rep.moves_scored}, total, group)
+    return SliceReport(slices=ids, codes=f["codes"], objective=f["objective"],
+                       initial_objective=f["initial_objective"], iterations=f["iterations"],
+                       moves_scored=f["moves_scored"], seconds=dict(rep.seconds))
