@@ -393,7 +393,9 @@ struct Engine {
   __device__ void refresh() {
     AMVM_LOCALS
 #ifndef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
     if (tid == 0) sh->c.pc[15] += 1;
+#endif
 #endif
     __syncthreads();  // publish cidx
     if (m == 1) {
@@ -651,7 +653,9 @@ struct Engine {
             const double dp = k + 1 < nlev ? dsub(lv[k + 1], lk) : 0.0;
             double tm, tpv;
 #ifndef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
             if (tid == 0) sh->c.pc[11] += 1;
+#endif
 #endif
             // raw count: candidates actually scored over all m rows
             if (tid == 0) sh->c.mv_raw += (k > 0) + (k + 1 < nlev);
@@ -664,7 +668,9 @@ struct Engine {
             if (lvl >= 0) {
               applied = w;
 #ifndef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
               if (tid == 0) sh->c.pc[12] += 1;
+#endif
 #endif
               const double d = dsub(lv[lvl], lk);
               const double *col = At + j * m;
@@ -697,7 +703,9 @@ struct Engine {
             for (int w = 0; w < NW; ++w) cnt += sh->wsum[wpar][w];
           }
           sh->c.mv_ref += cnt;
+#ifndef AMVM_FC_PROFILE
           sh->c.pc[13] += 1;
+#endif
         }
         wpar ^= 1;
         if (applied >= 0) {
@@ -731,20 +739,49 @@ struct Engine {
         for (int e = tid; e < 256; e += NT) sh->hist[e] = 0;
         __syncthreads();
         const uint64_t hm = shift == 56 ? 0ull : (~0ull << (shift + 8));
-        for (int64_t i = tid; i < m; i += NT) {
-          uint64_t key = abs_key(cr[i]);
-          if ((key & hm) == prefix) atomicAdd(&sh->hist[(key >> shift) & 255], 1u);
+        // warp-aggregated histogram: |s| values of one instance share their
+        // high digits, so plain per-thread atomics would serialise on a bin
+        for (int64_t i0 = (int64_t)warp * 32; i0 < m; i0 += NT) {
+          const int64_t i = i0 + lane;
+          const uint64_t key = i < m ? abs_key(cr[i]) : 0ull;
+          const bool in = i < m && (key & hm) == prefix;
+          const unsigned act = __ballot_sync(AMVM_FULL, in);
+          if (in) {
+            const unsigned bin = (unsigned)(key >> shift) & 255u;
+            const unsigned peers = __match_any_sync(act, bin);
+            if (lane == __ffs(peers) - 1) atomicAdd(&sh->hist[bin], (unsigned)__popc(peers));
+          }
         }
         __syncthreads();
-        if (tid == 0) {
-          int64_t cum = 0;
-          int d = 255;
-          for (; d >= 0; --d) {
-            if (cum + sh->hist[d] >= remaining) break;
-            cum += sh->hist[d];
+        if (warp == 0) {
+          // the digit d where the count of keys with a larger digit first
+          // reaches `remaining`, scanning from digit 255 down: lane l holds
+          // digits 255-8l .. 248-8l; shuffle-scan of the lane totals
+          unsigned h[8], tot = 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            h[e] = sh->hist[255 - 8 * lane - e];
+            tot += h[e];
           }
-          sh->bc_i[0] = d;
-          sh->bc_i[1] = (int)cum;
+          unsigned incl = tot;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(AMVM_FULL, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int64_t before = (int64_t)(incl - tot);  // keys in the lanes above (larger digits)
+          const bool here = before < remaining && before + (int64_t)tot >= remaining;
+          const unsigned who = __ballot_sync(AMVM_FULL, here);
+          if (lane == __ffs(who) - 1) {
+            int64_t cum = before;
+            int e = 0;
+            for (; e < 8; ++e) {
+              if (cum + (int64_t)h[e] >= remaining) break;
+              cum += h[e];
+            }
+            sh->bc_i[0] = 255 - 8 * lane - e;
+            sh->bc_i[1] = (int)cum;
+          }
         }
         __syncthreads();
         prefix |= (uint64_t)sh->bc_i[0] << shift;
@@ -876,6 +913,25 @@ struct Engine {
     return true;
   }
 
+  // fc_rest with the remaining rows split across the warp's lanes (the test
+  // is an AND over rows, so the order is free): one pair per warp, ~nr/32
+  // bound divisions per lane instead of nr in one thread.  Warp-uniform result.
+  __device__ bool fc_rest_warp(int64_t i, int32_t j, double delta, int nr, int g) {
+    AMVM_LOCALS
+    bool ok = true;
+    for (int q0 = g; q0 < nr; q0 += 32) {
+      const int q = q0 + lane;
+      if (q < nr) {
+        const int64_t rq = rows[q];
+        const double da = dsub(__ldg(Ar + rq * n + j), __ldg(Ar + rq * n + i));
+        const double bq = ddiv(reps[q], delta);
+        ok = rsgn[q] ? (da < bq) : (da > -bq);
+      }
+      if (!__all_sync(AMVM_FULL, ok)) return false;
+    }
+    return true;
+  }
+
   // Pairs alive after the staged rows (queued by every tile): each of the
   // next kRowPasses rows tests the whole queue (independent loads from the
   // contiguous row of Ar) and compacts it (one atomic per warp) into the
@@ -947,12 +1003,14 @@ struct Engine {
       QEnt *t = src; src = dst; dst = t;
     }
 #ifdef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
     if (tid == 0) sh->c.pc[12] += qn;
 #endif
-    for (int e = tid; e < qn; e += NT) {
+#endif
+    for (int e = warp; e < qn; e += NW) {  // the last survivors: one pair per warp
       const QEnt c = src[e];
       const double delta = dsub(lv[c.ki], lv[c.kj]);
-      if (fc_rest(c.i, c.j, delta, nr, q)) fc_append(c.i, c.j, delta, counting);
+      if (fc_rest_warp(c.i, c.j, delta, nr, q) && lane == 0) fc_append(c.i, c.j, delta, counting);
     }
     __syncthreads();
     if (tid == 0) sh->qcount = 0;
@@ -979,7 +1037,9 @@ struct Engine {
     constexpr bool counting = MODE == FC_COUNT;
     // i-groups: 32 consecutive positions of ONE level bucket, so idx_i (and
     // with it every staged row's bound for a given j-bucket) is warp-uniform;
-    // within a bucket the lanes' b0 ascend, so their prefixes nest
+    // within a bucket the lanes' b0 ascend, so their prefixes nest.  The
+    // j-buckets are walked through the skip list of non-empty levels.
+    const int32_t *nxt = lst + (nlev + 1);
     const int64_t ngrp = (n + 31) / 32 + nlev;
     for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
       const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
@@ -1014,7 +1074,7 @@ struct Engine {
 #pragma unroll
         for (int q = 0; q < kG; ++q) bi[q] = (have && q < g) ? ag[(int64_t)q * n + ip] : 0.0;
         const double xi = lv[ki];
-        for (int kj = 0; kj < ki; ++kj) {
+        for (int kj = nxt[nlev]; kj < ki; kj = nxt[kj]) {
           const int64_t s0 = (int64_t)lst[kj] > p0 ? (int64_t)lst[kj] : p0;
           const int64_t s1 = (int64_t)lst[kj + 1] < p1 ? (int64_t)lst[kj + 1] : p1;
           if (s0 >= s1) continue;
@@ -1043,10 +1103,14 @@ struct Engine {
           }
           const int e0 = (int)(s0 - p0), e1 = (int)(wend - p0), emine = (int)(mine - p0);
 #ifdef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
           if (lane == 0) atomicAdd((unsigned long long *)&sh->c.pc[14], (unsigned long long)(e1 - e0));
+#endif
           {
             const int u = __reduce_add_sync(AMVM_FULL, emine - e0);
+#ifndef AMVM_FC_PROFILE
             if (lane == 0) atomicAdd((unsigned long long *)&sh->c.pc[15], (unsigned long long)u);
+#endif
           }
 #endif
           // survivors of the staged rows: straight into the candidate list when
@@ -1069,7 +1133,9 @@ struct Engine {
               int bse = 0;
               if (lane == 0) bse = atomicAdd(&sh->qcount, __popc(bal));
 #ifdef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
               if (lane == 0) atomicAdd((unsigned long long *)&sh->c.pc[11], (unsigned long long)__popc(bal));
+#endif
 #endif
               bse = __shfl_sync(AMVM_FULL, bse, 0);
               if (alive) {
@@ -1132,7 +1198,9 @@ struct Engine {
               int bse = 0;
               if (lane == 0) bse = atomicAdd(nr <= g ? &sh->counter : &sh->qcount, tot);
 #ifdef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
               if (lane == 0 && nr > g) atomicAdd((unsigned long long *)&sh->c.pc[11], (unsigned long long)tot);
+#endif
 #endif
               int pos = __shfl_sync(AMVM_FULL, bse, 0) + incl - c;
               while (msk) {
@@ -1163,13 +1231,26 @@ struct Engine {
       }
       __syncthreads();
     }
+#ifdef AMVM_FC_PROFILE
+    const long long fd0 = clock64();
+#endif
     if (nr > g) fc_drain(nr, g, counting);
     __syncthreads();
+#ifdef AMVM_FC_PROFILE
+    if (tid == 0 && MODE == FC_ALL) sh->c.pc[12] += clock64() - fd0;
+#endif
   }
 
   __device__ int find_candidates(bool always_sort) {
     AMVM_LOCALS
+#ifdef AMVM_FC_PROFILE  // diagnostic: sub-phase cycles in pc[8..13]
+    long long fq0 = clock64(), fq1;
+#define FC_PROF(k) do { fq1 = clock64(); if (tid == 0) sh->c.pc[8 + (k)] += fq1 - fq0; fq0 = fq1; } while (0)
+#else
+#define FC_PROF(k) do { } while (0)
+#endif
     const int nr = select_rows();
+    FC_PROF(0);
     const int g = nr < kG ? nr : kG;
     int32_t *lst = (int32_t *)scr;
     int32_t *lfl = lst + (nlev + 1);
@@ -1195,6 +1276,24 @@ struct Engine {
     }
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) perm[atomicAdd(&lfl[cidx[j]], 1)] = (int32_t)j;
+    __syncthreads();
+    // lfl (free again) becomes a skip list over empty level buckets:
+    // lfl[k] = the smallest non-empty level > k (nlev if none), lfl[nlev] =
+    // the lowest non-empty level; the pair loops step through it (C2: 127
+    // variables over 1024 levels)
+    if (warp == 0) {
+      int nxt = (int)nlev;
+      for (int64_t top = nlev - 1; top >= 0; top -= 32) {
+        const int64_t k = top - lane;
+        const bool ne = k >= 0 && lst[k + 1] > lst[k];
+        const unsigned bal = __ballot_sync(AMVM_FULL, ne);  // bit l: level top - l non-empty
+        // next non-empty above k: the nearest set bit below lane l (higher level), else nxt
+        const unsigned above = bal & ((1u << lane) - 1u);
+        if (k >= 0) lfl[k] = above ? (int)(top - (31 - __clz(above))) : nxt;
+        if (bal) nxt = (int)(top - (31 - __clz(bal)));  // the lowest non-empty level in this chunk
+      }
+      if (lane == 0) lfl[nlev] = nxt;
+    }
     __syncthreads();
     // sort every level bucket by the tightest row's folded value b0 (eps_0 = 0:
     // that row defines t), so each i's row-0 survivors in a bucket are a prefix
@@ -1274,6 +1373,7 @@ struct Engine {
         __syncthreads();
       }
     }
+    FC_PROF(1);
     // staged rows in level-sorted order, sign folded: ag[q*n + pos]
     for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
       const int64_t q = e / n, ps = e - q * n;
@@ -1293,7 +1393,9 @@ struct Engine {
       sh->qcount = 0;
     }
     __syncthreads();
+    FC_PROF(2);
     fc_pass<FC_ALL>(nr, g, 0.0, 0);
+    FC_PROF(3);
     int cnt = sh->counter;
     __syncthreads();
     const int maxc = prm->max_candidates;
@@ -1308,6 +1410,8 @@ struct Engine {
       sort_cands(cnt);
       if (maxc > 0 && cnt > maxc) cnt = maxc;
     }
+    FC_PROF(5);
+#undef FC_PROF
     return cnt;
   }
 
@@ -1389,8 +1493,12 @@ struct Engine {
     const int cnt = find_candidates(false);
     const long long tf1 = clock64();
     if (tid == 0) sh->c.pc[5] += tf1 - tf0;
+#ifndef AMVM_FC_PROFILE
     if (tid == 0) sh->c.pc[8] += 1;
+#endif
+#ifndef AMVM_FC_PROFILE
     if (tid == 0) sh->c.pc[9] += cnt;
+#endif
     if (cnt == 0) return false;
     double wt = 0.0, wd = 0.0;
     int wi = -1, wj = -1;
@@ -1601,7 +1709,9 @@ struct Engine {
       int bi = -1, bj = -1;
       double bd = 0, bt = 0;
       if (!best_swap(bi, bj, bd, bt)) break;
+#ifndef AMVM_FC_PROFILE
       if (tid == 0) sh->c.pc[10] += 1;
+#endif
       apply_swap_known(bi, bj, bd, bt);
       one_opt();
     }
@@ -1888,7 +1998,9 @@ struct Engine {
     } else {
       impact_scores(alpha);
 #ifndef AMVM_FC_STATS
+#ifndef AMVM_FC_PROFILE
       if (tid == 0) sh->c.pc[14] += 1;
+#endif
 #endif
       if (ic) {
         for (int64_t k = tid; k < n; k += NT) ic[k] = dbuf[k];
