@@ -134,6 +134,27 @@ AMVM_API int amvm_solve(const amvm_problem *prob, const amvm_params *prm,
                const amvm_solution *start, amvm_pcg64 *rng,
                amvm_result *res, void *ws, size_t ws_bytes, void *stream);
 
+/* ---- whole solve on a SPARSE A (tomography: density <= 1/8) ------------
+ * Same semantics and results as amvm_solve (bit for bit: every zero entry
+ * the dense path would add is exact), with A given only as CSC and CSR
+ * (device arrays, both ascending within a column / row) -- no dense copy of
+ * A anywhere, so the workspace is O(slots * (m + n)) plus the parked
+ * instances.  one_opt scores each candidate from its column's nonzeros plus
+ * the largest |s| among untouched rows (a top list of 2*max_col_nnz + 1
+ * rows by |s|); max_col_nnz = the largest column nonzero count.           */
+typedef struct {
+  int64_t m, n, nlev, count, nnz, max_col_nnz;
+  const int64_t *cptr; const int32_t *crow; const double *cval;  /* CSC, n + 1 / nnz / nnz */
+  const int64_t *rptr; const int32_t *rcol; const double *rval;  /* CSR, m + 1 / nnz / nnz */
+  const double *B;      /* count x m targets b                                    */
+  const double *levels; /* count x nlev                                           */
+} amvm_sparse_problem;
+
+AMVM_API size_t amvm_sparse_workspace_bytes(const amvm_sparse_problem *prob, const amvm_params *prm);
+AMVM_API int amvm_solve_sparse(const amvm_sparse_problem *prob, const amvm_params *prm,
+                               const amvm_solution *start, amvm_pcg64 *rng, amvm_result *res,
+                               void *ws, size_t ws_bytes, void *stream);
+
 /* ---- component calls (count == 1; the Solution is updated in place) ---- */
 
 /* one_opt, localsearch.py:59-88 */

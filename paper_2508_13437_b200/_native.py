@@ -28,6 +28,7 @@ EXPORTS = (
     "amvm_csr_gemv", "amvm_sirt_workspace_bytes", "amvm_sirt", "amvm_is_improving", "amvm_swap_check",
     "amvm_score_moves", "amvm_score_workspace_bytes", "amvm_best_swap_l2", "amvm_apply_shift",
     "amvm_apply_swap", "amvm_accept", "amvm_select_operators", "amvm_update_weights",
+    "amvm_sparse_workspace_bytes", "amvm_solve_sparse",
 )
 
 
@@ -38,6 +39,15 @@ class NativeUnavailable(RuntimeError):
 class Problem(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("nlev", C.c_int64), ("count", C.c_int64),
                 ("At", C.c_void_p), ("B", C.c_void_p), ("levels", C.c_void_p)]
+
+
+class SparseProblem(C.Structure):
+    """amvm_sparse_problem: A as CSC + CSR device arrays (include/amvm.h)."""
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("nlev", C.c_int64), ("count", C.c_int64),
+                ("nnz", C.c_int64), ("max_col_nnz", C.c_int64),
+                ("cptr", C.c_void_p), ("crow", C.c_void_p), ("cval", C.c_void_p),
+                ("rptr", C.c_void_p), ("rcol", C.c_void_p), ("rval", C.c_void_p),
+                ("B", C.c_void_p), ("levels", C.c_void_p)]
 
 
 class Params(C.Structure):
@@ -129,6 +139,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.amvm_accept.argtypes = [i64, vp, vp, vp, vp, i32, C.c_double, vp, vp]
     lib.amvm_select_operators.argtypes = [vp, vp, vp, vp]
     lib.amvm_update_weights.argtypes = [vp, vp, i32, i32, vp]
+    lib.amvm_sparse_workspace_bytes.restype = sz
+    lib.amvm_sparse_workspace_bytes.argtypes = [vp, vp]
+    lib.amvm_solve_sparse.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp]
     lib.amvm_strerror.restype = C.c_char_p
     lib.amvm_strerror.argtypes = [C.c_int]
     for name in EXPORTS:

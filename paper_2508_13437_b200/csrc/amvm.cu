@@ -16,10 +16,10 @@ using namespace amvm;
 // ------------------------------------------------------------------ kernels
 // Persistent solve: one CTA per resident slot, instances pulled from a
 // counter so uneven iteration counts balance across SMs.
-template <int NT>
+template <int NT, bool SP>
 __global__ void __launch_bounds__(NT, AMVM_MIN_BLOCKS) k_solve(KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Engine<NT> E;
+  Engine<NT, SP> E;
   E.bind(a, smem, blockIdx.x);
   WsHeader *hdr = (WsHeader *)a.ws;
   // Tasks: without chunking, task t = instance t.  Chunked: task t = (chunk
@@ -441,6 +441,7 @@ struct Plan {
   int64_t slots;
   size_t ist_bytes;  // per parked instance (chunked solve), 0 otherwise
   size_t icache_bytes;  // per instance impact-score cache (solve), 0 for ops
+  int sparse, ktop;     // sparse engine (amvm_solve_sparse)
   int chunk_iters;
   size_t ws_bytes;
 };
@@ -459,8 +460,8 @@ size_t smem_bytes(int64_t m, int64_t nlev, int cr_smem, int tab) {
 }
 
 template <int NT>
-int occupancy(size_t smem, bool op, int *blocks) {
-  auto fn = op ? k_op<NT> : k_solve<NT>;
+int occupancy(size_t smem, bool op, int *blocks, bool sp) {
+  auto fn = op ? k_op<NT> : (sp ? k_solve<NT, true> : k_solve<NT, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, NT, smem);
@@ -473,9 +474,9 @@ size_t smem_for(int nt, int64_t m, int64_t nlev, int cr_smem, int tab) {
   return smem_bytes<AMVM_NT>(m, nlev, cr_smem, tab);
 }
 
-int occupancy_for(int nt, size_t smem, bool op, int *blocks) {
+int occupancy_for(int nt, size_t smem, bool op, int *blocks, bool sp = false) {
   (void)nt;
-  return occupancy<AMVM_NT>(smem, op, blocks);
+  return occupancy<AMVM_NT>(smem, op, blocks, sp);
 }
 
 constexpr size_t kSmemMax = 220 * 1024;
@@ -484,8 +485,10 @@ constexpr size_t kSmemMax = 220 * 1024;
 #endif
 constexpr int kChunkIters = AMVM_CHUNK_ITERS;  // chunked solve: ALNS iterations per task
 
-int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
+int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, int sparse = 0, int ktop = 0) {
   if (!p || !prm) return AMVM_ERR_INVALID;
+  P->sparse = sparse;
+  P->ktop = ktop;
   if (p->m < 1 || p->n < 1 || p->nlev < 1 || p->count < 1) return AMVM_ERR_INVALID;
   if (p->n > 0x7fffffff || p->m > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
   if (prm->r < 1 || prm->r > p->n || prm->k_eps < 1 || prm->max_iters < 0 || prm->refresh_period < 1 ||
@@ -522,7 +525,7 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
     P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
   }
   if (P->smem > kSmemMax) return AMVM_ERR_UNSUPPORTED;  // nlev too large for the smem level table
-  const SlotLayout L = slot_layout(p->m, p->n, prm->k_eps, prm->r, cap);
+  const SlotLayout L = slot_layout(p->m, p->n, prm->k_eps, prm->r, cap, sparse ? ktop : 0);
   P->slot_bytes = al256(L.total);
   if (op) {
     P->slots = 1;
@@ -530,7 +533,7 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
     int dev = 0, sms = 0, blocks = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return AMVM_ERR_NO_DEVICE;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return AMVM_ERR_CUDA;
-    int rc = occupancy_for(nt, P->smem, false, &blocks);
+    int rc = occupancy_for(nt, P->smem, false, &blocks, sparse != 0);
     if (rc) return rc;
     if (blocks < 1) return AMVM_ERR_UNSUPPORTED;
     P->slots = std::min<int64_t>(p->count, (int64_t)blocks * sms);
@@ -540,7 +543,7 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P) {
   P->chunk_iters = (!op && p->count > P->slots && prm->max_iters > kChunkIters) ? kChunkIters : 0;
   P->ist_bytes = P->chunk_iters ? inst_layout(p->m, p->n).total : 0;
   P->icache_bytes = op ? 0 : al256((size_t)8 * p->n);
-  P->ws_bytes = sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
+  P->ws_bytes = sizeof(WsHeader) + ws_dense_bytes(p->m, p->n, sparse) +
                 (size_t)P->slots * P->slot_bytes + (size_t)p->count * P->ist_bytes +
                 (size_t)p->count * P->icache_bytes + (op ? 0 : al256((size_t)4 * p->count));
   return AMVM_OK;
@@ -558,20 +561,21 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
   a.slot_bytes = P.slot_bytes;
   a.chunk_iters = P.chunk_iters;
   a.ist_bytes = P.ist_bytes;
-  a.Ar = (const double *)(a.ws + sizeof(WsHeader));
-  {
+  a.sparse = P.sparse;
+  a.ktop = P.ktop;
+  if (!P.sparse) {  // the dense part: row-major Ar and the CSC copy (sparse: the caller's CSC / CSR)
+    a.Ar = (const double *)(a.ws + sizeof(WsHeader));
     unsigned char *cb = a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n);
     const CscLayout CL = csc_layout(p->m, p->n);
     a.cptr = (const int64_t *)(cb + CL.ptr);
     a.crow = (const int32_t *)(cb + CL.row);
     a.cval = (const double *)(cb + CL.val);
   }
-  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
-                            (size_t)P.slots * P.slot_bytes
-                      : nullptr;
+  const size_t dense = ws_dense_bytes(p->m, p->n, P.sparse);
+  a.ist = P.ist_bytes ? a.ws + sizeof(WsHeader) + dense + (size_t)P.slots * P.slot_bytes : nullptr;
   if (P.icache_bytes) {
-    unsigned char *ib = a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n) + csc_layout(p->m, p->n).total +
-                        (size_t)P.slots * P.slot_bytes + (size_t)p->count * P.ist_bytes;
+    unsigned char *ib = a.ws + sizeof(WsHeader) + dense + (size_t)P.slots * P.slot_bytes +
+                        (size_t)p->count * P.ist_bytes;
     a.icache = ib;
     a.icache_bytes = P.icache_bytes;
     a.ivalid = (int32_t *)(ib + (size_t)p->count * P.icache_bytes);
@@ -589,13 +593,13 @@ int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
     if (e != cudaSuccess) return AMVM_ERR_CUDA;
   }
   int blocks = 0;
-  int rc = occupancy_for(P.nt, P.smem, op, &blocks);  // also sets the smem attribute
+  int rc = occupancy_for(P.nt, P.smem, op, &blocks, P.sparse != 0);  // also sets the smem attribute
   if (rc) return rc;
-  {  // row-major copy of A for the row gathers (filter rows, screening rows)
+  if (!a.sparse) {  // row-major copy of A for the row gathers (filter rows, screening rows)
     const dim3 tg((unsigned)((a.n + 31) / 32), (unsigned)((a.m + 31) / 32)), tb(32, 8);
     k_transpose<<<tg, tb, 0, st>>>(a.At, (double *)a.Ar, a.m, a.n);
   }
-  {  // CSC copy for sparse A (sets the header's csc_ok when it fits)
+  if (!a.sparse) {  // CSC copy for sparse A (sets the header's csc_ok when it fits)
     int64_t *cptr = (int64_t *)a.cptr;
     const unsigned cg = (unsigned)((a.n + 7) / 8);
     k_csc_count<<<cg, 256, 0, st>>>(a.At, a.m, a.n, cptr);
@@ -604,7 +608,8 @@ int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
   }
   const dim3 grid((unsigned)P.slots), block((unsigned)P.nt);
   if (op) k_op<AMVM_NT><<<grid, block, P.smem, st>>>(a);
-  else k_solve<AMVM_NT><<<grid, block, P.smem, st>>>(a);
+  else if (a.sparse) k_solve<AMVM_NT, true><<<grid, block, P.smem, st>>>(a);
+  else k_solve<AMVM_NT, false><<<grid, block, P.smem, st>>>(a);
   return cuda_rc(cudaGetLastError());
 }
 
@@ -667,6 +672,48 @@ int amvm_solve(const amvm_problem *prob, const amvm_params *prm, const amvm_solu
   if (rc) return rc;
   if (!ws || ws_bytes < P.ws_bytes) return AMVM_ERR_WORKSPACE;
   KArgs a = base_args(prob, prm, P, ws);
+  a.s_idx = start->idx; a.s_r = start->residual; a.s_obj = start->objective; a.s_cnt = start->updates;
+  a.rng = rng;
+  a.res = *res;
+  return launch(P, false, a, (cudaStream_t)stream);
+}
+
+static int sparse_plan(const amvm_sparse_problem *sp, const amvm_params *prm, bool op, Plan *P,
+                       amvm_problem *dense_view) {
+  if (!sp || !prm || sp->m < 1 || sp->n < 1 || sp->nnz < 0 || sp->max_col_nnz < 0) return AMVM_ERR_INVALID;
+  memset(dense_view, 0, sizeof(*dense_view));
+  dense_view->m = sp->m; dense_view->n = sp->n; dense_view->nlev = sp->nlev; dense_view->count = sp->count;
+  dense_view->B = sp->B; dense_view->levels = sp->levels;
+  // the |s| top list must outlast the rows a column pair can touch
+  int64_t ktop = 2 * sp->max_col_nnz + 1;
+  if (ktop < 32) ktop = 32;
+  if (ktop > sp->m) ktop = sp->m;
+  if (ktop > 4096) return AMVM_ERR_UNSUPPORTED;  // rank-sorted on one CTA
+  return make_plan(dense_view, prm, op, P, 1, (int)ktop);
+}
+
+size_t amvm_sparse_workspace_bytes(const amvm_sparse_problem *sp, const amvm_params *prm) {
+  Plan P;
+  amvm_problem dv;
+  if (sparse_plan(sp, prm, false, &P, &dv)) return 0;
+  return P.ws_bytes;
+}
+
+int amvm_solve_sparse(const amvm_sparse_problem *sp, const amvm_params *prm, const amvm_solution *start,
+                      amvm_pcg64 *rng, amvm_result *res, void *ws, size_t ws_bytes, void *stream) {
+  if (!sp || !prm || !sol_ok(start) || !rng || !res || !sol_ok(&res->best) || !res->initial_objective ||
+      !res->iterations || !res->operator_uses)
+    return AMVM_ERR_INVALID;
+  if (!sp->cptr || !sp->crow || !sp->cval || !sp->rptr || !sp->rcol || !sp->rval || !sp->B || !sp->levels)
+    return AMVM_ERR_INVALID;
+  Plan P;
+  amvm_problem dv;
+  int rc = sparse_plan(sp, prm, false, &P, &dv);
+  if (rc) return rc;
+  if (!ws || ws_bytes < P.ws_bytes) return AMVM_ERR_WORKSPACE;
+  KArgs a = base_args(&dv, prm, P, ws);
+  a.cptr = sp->cptr; a.crow = sp->crow; a.cval = sp->cval;
+  a.rptr = sp->rptr; a.rcol = sp->rcol; a.rval = sp->rval;
   a.s_idx = start->idx; a.s_r = start->residual; a.s_obj = start->objective; a.s_cnt = start->updates;
   a.rng = rng;
   a.res = *res;

@@ -383,6 +383,65 @@ __device__ double gemv_row(GA &&a, GX &&x, int64_t K, int kind) {
 }
 
 // kernel kind of output row i of an m-row dgemv_t (4x4 groups, then 4x2, 4x1)
+// gemv_row for a sparse row (its nonzeros: columns ascending `cols`, values
+// `vals`): the same blocks, lanes and combination order with the zero
+// terms left out -- adding fma(0, x, l) or 0*x leaves every partial sum
+// unchanged, so the result equals the dense one (up to the sign of a zero).
+template <class GX>
+__device__ double gemv_row_sparse(const int32_t *cols, const double *vals, int64_t nnz, GX &&x, int64_t K,
+                                  int kind) {
+  const int64_t m1 = K & -4;
+  double y = 0.0;
+  int64_t e = 0;
+  for (int64_t p = 0; p < m1; p += 2048) {
+    const int64_t pe = p + (m1 - p < 2048 ? m1 - p : 2048);
+    double t;
+    if (kind == 4) {
+      double l[4] = {0.0, 0.0, 0.0, 0.0};
+      for (; e < nnz && __ldg(cols + e) < pe; ++e) {
+        const int64_t c = __ldg(cols + e);
+        l[c & 3] = dfma(__ldg(vals + e), x(c), l[c & 3]);
+      }
+      t = dadd(dadd(l[0], l[2]), dadd(l[1], l[3]));
+    } else if (kind == 2) {
+      double l[2] = {0.0, 0.0};
+      for (; e < nnz && __ldg(cols + e) < pe; ++e) {
+        const int64_t c = __ldg(cols + e);
+        l[c & 1] = dadd(l[c & 1], dmul(__ldg(vals + e), x(c)));
+      }
+      t = dadd(l[0], l[1]);
+    } else {
+      double u[4] = {0.0, 0.0, 0.0, 0.0};  // u0, u1, v0, v1
+      for (; e < nnz && __ldg(cols + e) < pe; ++e) {
+        const int64_t c = __ldg(cols + e);
+        u[c & 3] = dadd(u[c & 3], dmul(__ldg(vals + e), x(c)));
+      }
+      t = dadd(dadd(u[0], u[2]), dadd(u[1], u[3]));
+    }
+    y = dadd(y, t);
+  }
+  // the K & 3 leftover columns, in the dense formula with absent entries 0
+  auto a = [&](int64_t c) -> double {
+    while (e < nnz && __ldg(cols + e) < c) ++e;
+    return (e < nnz && __ldg(cols + e) == c) ? __ldg(vals + e) : 0.0;
+  };
+  switch (K & 3) {
+    case 1: y = dfma(a(m1), x(m1), y); break;
+    case 2: {
+      const double a0 = a(m1), a1 = a(m1 + 1);
+      y = dadd(y, dfma(a0, x(m1), dmul(a1, x(m1 + 1))));
+      break;
+    }
+    case 3: {
+      const double a0 = a(m1), a1 = a(m1 + 1), a2 = a(m1 + 2);
+      y = dadd(y, dfma(a2, x(m1 + 2), dfma(a0, x(m1), dmul(a1, x(m1 + 1)))));
+      break;
+    }
+    default: break;
+  }
+  return y;
+}
+
 __device__ __forceinline__ int gemv_kind(int64_t i, int64_t m) {
   const int64_t g4 = m & ~(int64_t)3;
   if (i < g4) return 4;

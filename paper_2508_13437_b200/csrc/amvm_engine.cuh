@@ -128,6 +128,15 @@ struct KArgs {
   unsigned char *icache;
   size_t icache_bytes;
   int32_t *ivalid;
+  // sparse engine (amvm_solve_sparse): A only as the caller's CSC (cptr,
+  // crow, cval above, rows ascending per column) and CSR (rows below,
+  // columns ascending per row); no dense At / Ar anywhere.  ktop = size of
+  // the |s| top list that bounds untouched rows (>= 2 * max column nnz + 1).
+  int sparse;
+  int32_t ktop;
+  const int64_t *rptr;
+  const int32_t *rcol;
+  const double *rval;
 };
 
 enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR,
@@ -173,6 +182,12 @@ __host__ __device__ inline CscLayout csc_layout(int64_t m, int64_t n) {
   return L;
 }
 
+// Bytes of the dense part of the workspace (row-major Ar + the CSC copy of
+// A) that precedes the slots: none for the sparse engine.
+__host__ __device__ inline size_t ws_dense_bytes(int64_t m, int64_t n, int sparse) {
+  return sparse ? 0 : ws_ar_bytes(m, n) + csc_layout(m, n).total;
+}
+
 struct InstLayout {
   size_t r, idx, total;
 };
@@ -187,7 +202,7 @@ __host__ __device__ inline InstLayout inst_layout(int64_t m, int64_t n) {
 // Per-slot workspace carve-up (shared by host sizing and device use).
 struct SlotLayout {
   size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf, que,
-      hset, rem, sav, pick, coin, ibuf, srt, total;
+      hset, rem, sav, pick, coin, ibuf, srt, rowtmp, top, total;
   int64_t nleaf, kk, hsz;
 };
 
@@ -202,7 +217,8 @@ __host__ __device__ inline uint64_t gen_mask(uint64_t v) {
   return v;
 }
 
-__host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t k_eps, int64_t r, int64_t cap) {
+__host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t k_eps, int64_t r, int64_t cap,
+                                                   int64_t ktop = 0) {
   SlotLayout L;
   int64_t mn = m > n ? m : n;
   L.nleaf = mn / 64 + 4;
@@ -238,6 +254,9 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
     while (n2 < n) n2 <<= 1;
     L.srt = o; o = al256(o + 16 * n2);  // bucket sort: (level, b0, j) per position
   }
+  // sparse engine: one dense row scratch (kept zero between uses), |s| top list
+  L.rowtmp = o; o = al256(o + (ktop > 0 ? 8 * n : 0));
+  L.top = o; o = al256(o + 4 * ktop);
   L.total = o;
   return L;
 }
@@ -252,6 +271,12 @@ struct Ctx {
   const int32_t *crow;
   const double *cval;
   int csc;
+  int sparse, ktop;           // sparse engine (see KArgs)
+  const int64_t *rptr;
+  const int32_t *rcol;
+  const double *rval;
+  double *rowtmp;             // n doubles, zero between uses
+  int32_t *top;               // ktop rows by (|s| desc, index asc)
   double *cr, *ur;
   int32_t *cidx, *uidx;
   double *dbuf, *pbuf, *cbk;
@@ -338,13 +363,18 @@ struct Shared {
   int32_t *iv;                     // ... and its valid flag
   int nfilter_rows, srt_rows_sorted;  // select_rows result (rows[] count, ordered by |s| desc)
   int task_live, task_skip;
+  int ntop;                       // sparse engine: rows in the |s| top list
+  int spl[NT / 32 * 4];           // sparse one_opt window: chosen level per column (-1: none)
+  double spt[NT / 32 * 4];        // ... and its objective
   Pcg rng;
   Ctx c;
 };
 
 __device__ __forceinline__ uint64_t abs_key(double x) { return (uint64_t)__double_as_longlong(fabs(x)); }
 
-template <int NT>
+// SP: the sparse engine (A as CSC + CSR only), a separate instantiation so
+// the dense hot loops keep their registers.
+template <int NT, bool SP = false>
 struct Engine {
   static constexpr int NW = NT / 32;
   Shared<NT> *sh;
@@ -398,11 +428,18 @@ struct Engine {
 #endif
 #endif
     __syncthreads();  // publish cidx
-    if (m == 1) {
+    if (m == 1 && !SP) {
       if (warp == 0) {
         double y = warp_ddot_skx([&](int64_t j) { return At[j]; },
                                  [&](int64_t j) { return lv[cidx[j]]; }, n, lane);
         if (lane == 0) cr[0] = dsub(y, b[0]);
+      }
+    } else if (SP) {
+      for (int64_t i = tid; i < m; i += NT) {
+        const int64_t e0 = __ldg(sh->c.rptr + i), e1 = __ldg(sh->c.rptr + i + 1);
+        double y = gemv_row_sparse(sh->c.rcol + e0, sh->c.rval + e0, e1 - e0,
+                                   [&](int64_t j) { return lv[cidx[j]]; }, n, gemv_kind(i, m));
+        cr[i] = dsub(y, b[i]);
       }
     } else {
       for (int64_t i = tid; i < m; i += NT) {
@@ -429,12 +466,22 @@ struct Engine {
     const int old = cidx[j];
     if (nl == old) return false;
     const double d = dsub(lv[nl], lv[old]);
-    const double *col = At + j * m;
     double mx = 0.0;
-    for (int64_t i = tid; i < m; i += NT) {
-      double y = dadd(cr[i], dmul(d, __ldg(col + i)));
-      cr[i] = y;
-      mx = fmax(mx, fabs(y));
+    if (SP) {  // touched rows only (s + d*0 = s), then the max over all rows
+      const int64_t b0 = __ldg(sh->c.cptr + j), b1 = __ldg(sh->c.cptr + j + 1);
+      for (int64_t e = b0 + tid; e < b1; e += NT) {
+        const int64_t r = __ldg(sh->c.crow + e);
+        cr[r] = dadd(cr[r], dmul(d, __ldg(sh->c.cval + e)));
+      }
+      __syncthreads();
+      for (int64_t i = tid; i < m; i += NT) mx = fmax(mx, fabs(cr[i]));
+    } else {
+      const double *col = At + j * m;
+      for (int64_t i = tid; i < m; i += NT) {
+        double y = dadd(cr[i], dmul(d, __ldg(col + i)));
+        cr[i] = y;
+        mx = fmax(mx, fabs(y));
+      }
     }
     mx = warp_max(mx);
     if (lane == 0) sh->redS[warp] = mx;
@@ -538,8 +585,99 @@ struct Engine {
   // improvement); scanning resumes after it.  Window/batch buffers alternate
   // by parity, so a buffer is rewritten only after every thread has passed
   // the barrier that follows its last read.
+  // one_opt on the sparse engine: every candidate scored exactly from its
+  // column's nonzeros plus the largest |s| among untouched rows (the first
+  // row of the |s| top list outside the column), so no screens: a window of
+  // NW*kSpCW columns is scored by the warps in parallel, the lowest improving
+  // column is applied (the reference's sequential first improvement) and
+  // scanning resumes after it.
+  static constexpr int kSpCW = 4;
+  __device__ void one_opt_sparse() {
+    AMVM_LOCALS
+    constexpr int WS = NW * kSpCW;
+    for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
+      bool changed = false;
+      int64_t p = 0;
+      sp_select_top();
+      while (p < n) {
+        const double t = cobj;
+#pragma unroll 1
+        for (int c = 0; c < kSpCW; ++c) {
+          const int64_t j = p + warp * kSpCW + c;
+          int lvl = -1;
+          double bt = t;
+          if (j < n) {
+            const int k = cidx[j];
+            const bool hm = k > 0, hp = k + 1 < nlev;
+            const double lk = lv[k];
+            const double dm = hm ? dsub(lv[k - 1], lk) : 0.0;
+            const double dp = hp ? dsub(lv[k + 1], lk) : 0.0;
+            const int64_t b0 = __ldg(sh->c.cptr + j), b1 = __ldg(sh->c.cptr + j + 1);
+            double mm = 0.0, mp = 0.0;
+            for (int64_t e = b0 + lane; e < b1; e += 32) {
+              const double rv = cr[__ldg(sh->c.crow + e)], a = __ldg(sh->c.cval + e);
+              mm = fmax(mm, fabs(dadd(rv, dmul(dm, a))));
+              mp = fmax(mp, fabs(dadd(rv, dmul(dp, a))));
+            }
+            mm = warp_max(mm);
+            mp = warp_max(mp);
+            const double u = sp_untouched_max(j, -1);
+            const double tm = fmax(mm, u), tp = fmax(mp, u);
+            if (hm && tm < bt) { bt = tm; lvl = k - 1; }
+            if (hp && tp < bt) { bt = tp; lvl = k + 1; }
+          }
+          if (lane == 0) {
+            sh->spl[warp * kSpCW + c] = lvl;
+            sh->spt[warp * kSpCW + c] = bt;
+          }
+        }
+        __syncthreads();
+        const int wc = (int)(n - p < WS ? n - p : WS);
+        int applied = -1;
+        for (int w = 0; w < wc; ++w)
+          if (sh->spl[w] >= 0) { applied = w; break; }
+        if (tid == 0) {
+          int64_t cnt = 0;
+          const int last = applied >= 0 ? applied : wc - 1;
+          for (int w = 0; w <= last; ++w) {
+            const int k = cidx[p + w];
+            cnt += (k > 0) + (k + 1 < nlev);
+          }
+          sh->c.mv_ref += cnt;
+          sh->c.mv_raw += cnt;
+        }
+        if (applied >= 0) {
+          const int64_t j = p + applied;
+          const int lvl = sh->spl[applied];
+          const double bt = sh->spt[applied];
+          const double d = dsub(lv[lvl], lv[cidx[j]]);
+          const int64_t b0 = __ldg(sh->c.cptr + j), b1 = __ldg(sh->c.cptr + j + 1);
+          __syncthreads();  // everyone has read the window's results and cidx[j]
+          for (int64_t e = b0 + tid; e < b1; e += NT) {
+            const int64_t r = __ldg(sh->c.crow + e);
+            cr[r] = dadd(cr[r], dmul(d, __ldg(sh->c.cval + e)));
+          }
+          if (tid == 0) cidx[j] = lvl;
+          __syncthreads();
+          bump_known(bt);
+          sp_select_top();  // the residual changed
+          changed = true;
+          p = j + 1;
+        } else {
+          __syncthreads();
+          p += wc;
+        }
+      }
+      if (!changed) break;
+    }
+  }
+
   __device__ void one_opt() {
     AMVM_LOCALS
+    if constexpr (SP) {
+      one_opt_sparse();
+      return;
+    }
     constexpr int WS = NW * kCW;
     __syncthreads();
     select_screen();
@@ -725,6 +863,180 @@ struct Engine {
   // the SET matters (the filter is an AND over rows); it is then ordered by
   // key so the tightest rows reject first.  Rows with s = 0 are dropped
   // (localsearch.py:151).  Returns the number of filter rows.
+  // Radix select of the kth largest |cr| key (8 passes of 8-bit digits):
+  // T = that key, need = how many rows with key == T belong to the top kth.
+  __device__ void radix_kth(int64_t kth, uint64_t &T, int64_t &need) {
+    AMVM_LOCALS
+    uint64_t prefix = 0;
+    int64_t remaining = kth;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int e = tid; e < 256; e += NT) sh->hist[e] = 0;
+      __syncthreads();
+      const uint64_t hm = shift == 56 ? 0ull : (~0ull << (shift + 8));
+      // warp-aggregated histogram: |s| values of one instance share their
+      // high digits, so plain per-thread atomics would serialise on a bin
+      for (int64_t i0 = (int64_t)warp * 32; i0 < m; i0 += NT) {
+        const int64_t i = i0 + lane;
+        const uint64_t key = i < m ? abs_key(cr[i]) : 0ull;
+        const bool in = i < m && (key & hm) == prefix;
+        const unsigned act = __ballot_sync(AMVM_FULL, in);
+        if (in) {
+          const unsigned bin = (unsigned)(key >> shift) & 255u;
+          const unsigned peers = __match_any_sync(act, bin);
+          if (lane == __ffs(peers) - 1) atomicAdd(&sh->hist[bin], (unsigned)__popc(peers));
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // the digit d where the count of keys with a larger digit first
+        // reaches `remaining`, scanning from digit 255 down: lane l holds
+        // digits 255-8l .. 248-8l; shuffle-scan of the lane totals
+        unsigned h[8], tot = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          h[e] = sh->hist[255 - 8 * lane - e];
+          tot += h[e];
+        }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(AMVM_FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int64_t before = (int64_t)(incl - tot);  // keys in the lanes above (larger digits)
+        const bool here = before < remaining && before + (int64_t)tot >= remaining;
+        const unsigned who = __ballot_sync(AMVM_FULL, here);
+        if (lane == __ffs(who) - 1) {
+          int64_t cum = before;
+          int e = 0;
+          for (; e < 8; ++e) {
+            if (cum + (int64_t)h[e] >= remaining) break;
+            cum += h[e];
+          }
+          sh->bc_i[0] = 255 - 8 * lane - e;
+          sh->bc_i[1] = (int)cum;
+        }
+      }
+      __syncthreads();
+      prefix |= (uint64_t)sh->bc_i[0] << shift;
+      remaining -= sh->bc_i[1];
+    }
+    T = prefix;
+    need = remaining;
+  }
+
+  // ---------------------------------------------- sparse engine helpers
+  // A[r, col] from the CSR row r (columns ascending): binary search, 0 if absent
+  __device__ double sp_row_at(int64_t r, int64_t col) {
+    const int64_t b0 = __ldg(sh->c.rptr + r), b1 = __ldg(sh->c.rptr + r + 1);
+    int64_t lo = b0, hi = b1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(sh->c.rcol + mid) < col) lo = mid + 1;
+      else hi = mid;
+    }
+    return (lo < b1 && __ldg(sh->c.rcol + lo) == col) ? __ldg(sh->c.rval + lo) : 0.0;
+  }
+  // position of row r in the CSC column col (rows ascending), -1 if absent
+  __device__ int64_t sp_col_find(int64_t col, int64_t r) {
+    const int64_t b0 = __ldg(sh->c.cptr + col), b1 = __ldg(sh->c.cptr + col + 1);
+    int64_t lo = b0, hi = b1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(sh->c.crow + mid) < r) lo = mid + 1;
+      else hi = mid;
+    }
+    return (lo < b1 && __ldg(sh->c.crow + lo) == r) ? lo : -1;
+  }
+  __device__ double sp_col_at(int64_t col, int64_t r) {
+    const int64_t e = sp_col_find(col, r);
+    return e >= 0 ? __ldg(sh->c.cval + e) : 0.0;
+  }
+  // rowtmp[c] = A[r, c] over row r's nonzeros, or back to 0 (block-wide;
+  // the caller synchronises)
+  __device__ void sp_row_scatter(int64_t r, bool clear) {
+    AMVM_LOCALS
+    double *rt = sh->c.rowtmp;
+    const int64_t b0 = __ldg(sh->c.rptr + r), b1 = __ldg(sh->c.rptr + r + 1);
+    for (int64_t e = b0 + tid; e < b1; e += NT) rt[__ldg(sh->c.rcol + e)] = clear ? 0.0 : __ldg(sh->c.rval + e);
+  }
+  // the ktop rows of largest |cr| ordered by (|s| desc, index asc) into top[]
+  // (all m rows when ktop >= m): bounds every row outside a column (or a
+  // column pair) by the first top row the column does not touch
+  __device__ void sp_select_top() {
+    AMVM_LOCALS
+    const int64_t K = sh->c.ktop < m ? sh->c.ktop : m;
+    int32_t *top = sh->c.top;
+    __syncthreads();
+    if (tid == 0) sh->counter = 0;
+    __syncthreads();
+    uint64_t T = 0;
+    int64_t need = 0;
+    if (K < m) radix_kth(K, T, need);
+    for (int64_t i = tid; i < m; i += NT) {
+      const uint64_t key = abs_key(cr[i]);
+      if (K >= m || key > T) top[atomicAdd(&sh->counter, 1)] = (int32_t)i;
+    }
+    __syncthreads();
+    int cnt = sh->counter;
+    __syncthreads();
+    if (K < m && need > 0) {  // rows with key == T, lowest indices first
+      int64_t base = 0;
+      for (int64_t c0 = 0; c0 < m && base < need; c0 += NT) {
+        const int64_t i = c0 + tid;
+        const bool f = i < m && abs_key(cr[i]) == T;
+        const unsigned bal = __ballot_sync(AMVM_FULL, f);
+        if (lane == 0) sh->wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int k = 0; k < NW; ++k) {
+          if (k < warp) before += sh->wcnt[k];
+          tot += sh->wcnt[k];
+        }
+        const int64_t pos = base + before + __popc(bal & ((1u << lane) - 1u));
+        if (f && pos < need) top[cnt + pos] = (int32_t)i;
+        base += tot;
+        __syncthreads();
+      }
+      cnt += (int)need;
+    }
+    // rank sort by (key desc, index asc) through ibuf
+    for (int q = tid; q < cnt; q += NT) ibuf[q] = top[q];
+    __syncthreads();
+    for (int q = tid; q < cnt; q += NT) {
+      const int32_t rq = ibuf[q];
+      const uint64_t kq = abs_key(cr[rq]);
+      int rank = 0;
+      for (int o = 0; o < cnt; ++o) {
+        const int32_t ro = ibuf[o];
+        const uint64_t ko = abs_key(cr[ro]);
+        rank += (ko > kq) || (ko == kq && ro < rq);
+      }
+      top[rank] = rq;
+    }
+    if (tid == 0) sh->ntop = cnt;
+    __syncthreads();
+  }
+
+  // max |s| over the rows a column (or two) does not touch: the first top
+  // row outside both (warp-wide; ktop > nnz(i) + nnz(j) guarantees one)
+  __device__ double sp_untouched_max(int64_t ci, int64_t cj) {
+    AMVM_LOCALS
+    const int32_t *top = sh->c.top;
+    const int cnt = sh->ntop;
+    for (int b0 = 0; b0 < cnt; b0 += 32) {
+      const int q = b0 + lane;
+      bool free_row = false;
+      if (q < cnt) {
+        const int64_t r = top[q];
+        free_row = sp_col_find(ci, r) < 0 && (cj < 0 || sp_col_find(cj, r) < 0);
+      }
+      const unsigned bal = __ballot_sync(AMVM_FULL, free_row);
+      if (bal) return fabs(cr[top[b0 + __ffs(bal) - 1]]);
+    }
+    return 0.0;  // every row touched (m <= nnz): nothing outside
+  }
+
   __device__ int select_rows() {
     AMVM_LOCALS
     __syncthreads();
@@ -732,64 +1044,7 @@ struct Engine {
     __syncthreads();
     uint64_t T = 0;
     int64_t need = 0;
-    if (kk < m) {
-      uint64_t prefix = 0;
-      int64_t remaining = kk;
-      for (int shift = 56; shift >= 0; shift -= 8) {
-        for (int e = tid; e < 256; e += NT) sh->hist[e] = 0;
-        __syncthreads();
-        const uint64_t hm = shift == 56 ? 0ull : (~0ull << (shift + 8));
-        // warp-aggregated histogram: |s| values of one instance share their
-        // high digits, so plain per-thread atomics would serialise on a bin
-        for (int64_t i0 = (int64_t)warp * 32; i0 < m; i0 += NT) {
-          const int64_t i = i0 + lane;
-          const uint64_t key = i < m ? abs_key(cr[i]) : 0ull;
-          const bool in = i < m && (key & hm) == prefix;
-          const unsigned act = __ballot_sync(AMVM_FULL, in);
-          if (in) {
-            const unsigned bin = (unsigned)(key >> shift) & 255u;
-            const unsigned peers = __match_any_sync(act, bin);
-            if (lane == __ffs(peers) - 1) atomicAdd(&sh->hist[bin], (unsigned)__popc(peers));
-          }
-        }
-        __syncthreads();
-        if (warp == 0) {
-          // the digit d where the count of keys with a larger digit first
-          // reaches `remaining`, scanning from digit 255 down: lane l holds
-          // digits 255-8l .. 248-8l; shuffle-scan of the lane totals
-          unsigned h[8], tot = 0;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            h[e] = sh->hist[255 - 8 * lane - e];
-            tot += h[e];
-          }
-          unsigned incl = tot;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(AMVM_FULL, incl, o);
-            if (lane >= o) incl += y;
-          }
-          const int64_t before = (int64_t)(incl - tot);  // keys in the lanes above (larger digits)
-          const bool here = before < remaining && before + (int64_t)tot >= remaining;
-          const unsigned who = __ballot_sync(AMVM_FULL, here);
-          if (lane == __ffs(who) - 1) {
-            int64_t cum = before;
-            int e = 0;
-            for (; e < 8; ++e) {
-              if (cum + (int64_t)h[e] >= remaining) break;
-              cum += h[e];
-            }
-            sh->bc_i[0] = 255 - 8 * lane - e;
-            sh->bc_i[1] = (int)cum;
-          }
-        }
-        __syncthreads();
-        prefix |= (uint64_t)sh->bc_i[0] << shift;
-        remaining -= sh->bc_i[1];
-      }
-      T = prefix;
-      need = remaining;
-    }
+    if (kk < m) radix_kth(kk, T, need);
     // keys strictly above T (all rows when kk >= m), unordered
     for (int64_t i = tid; i < m; i += NT) {
       uint64_t key = abs_key(cr[i]);
@@ -904,9 +1159,11 @@ struct Engine {
 
   __device__ bool fc_rest(int64_t i, int32_t j, double delta, int nr, int g) {
     AMVM_LOCALS
+    constexpr bool sp = SP;
     for (int q = g; q < nr; ++q) {
       const int64_t rq = rows[q];
-      const double da = dsub(__ldg(Ar + rq * n + j), __ldg(Ar + rq * n + i));
+      const double da = sp ? dsub(sp_row_at(rq, j), sp_row_at(rq, i))
+                           : dsub(__ldg(Ar + rq * n + j), __ldg(Ar + rq * n + i));
       const double bq = ddiv(reps[q], delta);
       if (!(rsgn[q] ? (da < bq) : (da > -bq))) return false;
     }
@@ -923,7 +1180,8 @@ struct Engine {
       const int q = q0 + lane;
       if (q < nr) {
         const int64_t rq = rows[q];
-        const double da = dsub(__ldg(Ar + rq * n + j), __ldg(Ar + rq * n + i));
+        const double da = SP ? dsub(sp_row_at(rq, j), sp_row_at(rq, i))
+                                       : dsub(__ldg(Ar + rq * n + j), __ldg(Ar + rq * n + i));
         const double bq = ddiv(reps[q], delta);
         ok = rsgn[q] ? (da < bq) : (da > -bq);
       }
@@ -956,8 +1214,15 @@ struct Engine {
     int base = 0;  // sh->qnext only grows: pass survivors land at [base, qnext)
     // kRowPasses passes, and more while the queue stays long (sparse rows
     // keep most pairs alive; batched passes beat per-pair fc_rest there)
-    for (; q < nr && qn > 0 && (q < g + np || qn > kDrainLong); ++q) {
-      const double *row = Ar + (int64_t)rows[q] * n;
+    constexpr bool sp = SP;
+    // (sparse engine: every remaining row as a pass -- a pass costs the row's
+    // nonzeros plus the queue, cheaper than per-pair binary searches)
+    for (; q < nr && qn > 0 && (q < g + np || qn > kDrainLong || sp); ++q) {
+      if (sp) {  // the row, densely, in the (zero) row scratch for this pass
+        sp_row_scatter(rows[q], false);
+        __syncthreads();
+      }
+      const double *row = sp ? sh->c.rowtmp : Ar + (int64_t)rows[q] * n;
       const double eq = reps[q];
       const bool pos = rsgn[q] != 0;
       if (tab2) {
@@ -978,9 +1243,9 @@ struct Engine {
         }
         double aj[U], ai[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          aj[u] = __ldg(row + c[u].j);
-          ai[u] = __ldg(row + c[u].i);
+        for (int u = 0; u < U; ++u) {  // (the sparse row scratch is written in-kernel: no .nc loads)
+          aj[u] = sp ? row[c[u].j] : __ldg(row + c[u].j);
+          ai[u] = sp ? row[c[u].i] : __ldg(row + c[u].i);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -997,6 +1262,7 @@ struct Engine {
       }
       __syncthreads();
       const int tot = sh->qnext;
+      if (sp) sp_row_scatter(rows[q], true);  // back to zero (all reads done)
       __syncthreads();  // everyone has read it (and the table) before the next pass
       qn = tot - base;
       base = tot;
@@ -1297,6 +1563,13 @@ struct Engine {
     __syncthreads();
     // sort every level bucket by the tightest row's folded value b0 (eps_0 = 0:
     // that row defines t), so each i's row-0 survivors in a bucket are a prefix
+    // (sparse engine: row 0 densely in the row scratch for the fill loops)
+    constexpr bool sp = SP;
+    if (sp) {
+      sp_row_scatter(rows[0], false);
+      __syncthreads();
+    }
+    auto row0 = [&](int32_t j) { return sp ? sh->c.rowtmp[j] : __ldg(Ar + (int64_t)rows[0] * n + j); };
     {
       int64_t n2 = 1;
       while (n2 < n) n2 <<= 1;
@@ -1308,7 +1581,7 @@ struct Engine {
         for (int64_t e = tid; e < n2; e += NT) {
           if (e < n) {
             const int32_t j = perm[e];
-            const double a = __ldg(Ar + (int64_t)rows[0] * n + j);
+            const double a = row0(j);
             sk[e] = ((uint32_t)cidx[j] << 16) | (uint32_t)j;
             sb[e] = rsgn[0] ? a : -a;
           } else {
@@ -1342,7 +1615,7 @@ struct Engine {
         for (int64_t e = tid; e < n2; e += NT) {
           if (e < n) {
             const int32_t j = perm[e];
-            const double a = __ldg(Ar + (int64_t)rows[0] * n + j);
+            const double a = row0(j);
             sl[e] = cidx[j];
             sj[e] = j;
             sb[e] = rsgn[0] ? a : -a;
@@ -1375,10 +1648,30 @@ struct Engine {
     }
     FC_PROF(1);
     // staged rows in level-sorted order, sign folded: ag[q*n + pos]
-    for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
-      const int64_t q = e / n, ps = e - q * n;
-      const double a = __ldg(Ar + (int64_t)rows[q] * n + perm[ps]);
-      ag[e] = rsgn[q] ? a : -a;
+    if (sp) {  // row by row through the dense row scratch (row 0 is still in it)
+      for (int q = 0; q < g; ++q) {
+        if (q > 0) {
+          sp_row_scatter(rows[q], false);
+          __syncthreads();
+        }
+        for (int64_t ps = tid; ps < n; ps += NT) {
+          const double a = sh->c.rowtmp[perm[ps]];
+          ag[(int64_t)q * n + ps] = rsgn[q] ? a : -a;
+        }
+        __syncthreads();
+        sp_row_scatter(rows[q], true);
+        __syncthreads();
+      }
+      if (g == 0) {
+        sp_row_scatter(rows[0], true);
+        __syncthreads();
+      }
+    } else {
+      for (int64_t e = tid; e < (int64_t)g * n; e += NT) {
+        const int64_t q = e / n, ps = e - q * n;
+        const double a = __ldg(Ar + (int64_t)rows[q] * n + perm[ps]);
+        ag[e] = rsgn[q] ? a : -a;
+      }
     }
     const int ll = (int)(nlev * nlev);
     if (tab) {
@@ -1505,10 +1798,14 @@ struct Engine {
     const double t0 = cobj;
     // sparse A: rows[] holds the filter rows by (|s| desc, index asc)
     const int nrows = sh->c.csc && sh->srt_rows_sorted ? sh->nfilter_rows : 0;
+    constexpr bool sp = SP;
+    if (sp) sp_select_top();
     for (int c = warp; c < cnt; c += NW) {
       const Cand e = cbuf[c];
       double mx = 0.0;
-      if (!(nrows > 0 && swap_tprime_sparse(e.i, e.j, e.d, nrows, mx))) {
+      if (sp) {
+        mx = swap_tprime_sp(e.i, e.j, e.d);
+      } else if (!(nrows > 0 && swap_tprime_sparse(e.i, e.j, e.d, nrows, mx))) {
         const double *ci = At + (int64_t)e.i * m;
         const double *cj = At + (int64_t)e.j * m;
         mx = 0.0;
@@ -1545,6 +1842,43 @@ struct Engine {
     }
     __syncthreads();
     return found;
+  }
+
+  // Sparse engine: t' over the union of the two columns' rows (the other
+  // column's entry by binary search in its CSC rows, 0 if absent) and the
+  // largest |s| outside both (the |s| top list); exactly the dense value.
+  __device__ double swap_tprime_sp(int i, int j, double d) {
+    AMVM_LOCALS
+    const int64_t *cp = sh->c.cptr;
+    const int32_t *crw = sh->c.crow;
+    const double *cv = sh->c.cval;
+    double mx = sp_untouched_max(i, j);
+    for (int64_t e = __ldg(cp + i) + lane; e < __ldg(cp + i + 1); e += 32) {  // rows of column i
+      const int64_t r = __ldg(crw + e);
+      mx = fmax(mx, fabs(dadd(cr[r], dmul(d, dsub(sp_col_at(j, r), __ldg(cv + e))))));
+    }
+    for (int64_t e = __ldg(cp + j) + lane; e < __ldg(cp + j + 1); e += 32) {  // rows only column j touches
+      const int64_t r = __ldg(crw + e);
+      if (sp_col_find(i, r) < 0) mx = fmax(mx, fabs(dadd(cr[r], dmul(d, dsub(__ldg(cv + e), 0.0)))));
+    }
+    return warp_max(mx);
+  }
+
+  // s += d (A[:, j] - A[:, i]) on the sparse engine: each touched row once
+  // (block-wide, no barrier inside; the caller synchronises)
+  __device__ void swap_update_sp(int i, int j, double d) {
+    AMVM_LOCALS
+    const int64_t *cp = sh->c.cptr;
+    const int32_t *crw = sh->c.crow;
+    const double *cv = sh->c.cval;
+    for (int64_t e = __ldg(cp + i) + tid; e < __ldg(cp + i + 1); e += NT) {
+      const int64_t r = __ldg(crw + e);
+      cr[r] = dadd(cr[r], dmul(d, dsub(sp_col_at(j, r), __ldg(cv + e))));
+    }
+    for (int64_t e = __ldg(cp + j) + tid; e < __ldg(cp + j + 1); e += NT) {
+      const int64_t r = __ldg(crw + e);
+      if (sp_col_find(i, r) < 0) cr[r] = dadd(cr[r], dmul(d, dsub(__ldg(cv + e), 0.0)));
+    }
   }
 
   // t' = max_r |s_r + d (a_rj - a_ri)| for sparse A (warp-wide), exactly the
@@ -1586,9 +1920,13 @@ struct Engine {
   // apply_swap, core.py:228-245, with the objective predicted by best_swap.
   __device__ void apply_swap_known(int i, int j, double d, double t) {
     AMVM_LOCALS
-    const double *ci = At + (int64_t)i * m;
-    const double *cj = At + (int64_t)j * m;
-    for (int64_t r = tid; r < m; r += NT) cr[r] = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
+    if constexpr (SP) {
+      swap_update_sp(i, j, d);
+    } else {
+      const double *ci = At + (int64_t)i * m;
+      const double *cj = At + (int64_t)j * m;
+      for (int64_t r = tid; r < m; r += NT) cr[r] = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
+    }
     if (tid == 0) {
       const int32_t t0 = cidx[i];
       cidx[i] = cidx[j];
@@ -1604,13 +1942,19 @@ struct Engine {
     AMVM_LOCALS
     const int ki = cidx[i], kj = cidx[j];
     const double d = dsub(lv[ki], lv[kj]);
-    const double *ci = At + (int64_t)i * m;
-    const double *cj = At + (int64_t)j * m;
     double mx = 0.0;
-    for (int64_t r = tid; r < m; r += NT) {
-      const double y = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
-      cr[r] = y;
-      mx = fmax(mx, fabs(y));
+    if constexpr (SP) {
+      swap_update_sp(i, j, d);
+      __syncthreads();
+      for (int64_t r = tid; r < m; r += NT) mx = fmax(mx, fabs(cr[r]));
+    } else {
+      const double *ci = At + (int64_t)i * m;
+      const double *cj = At + (int64_t)j * m;
+      for (int64_t r = tid; r < m; r += NT) {
+        const double y = dadd(cr[r], dmul(d, dsub(__ldg(cj + r), __ldg(ci + r))));
+        cr[r] = y;
+        mx = fmax(mx, fabs(y));
+      }
     }
     const double t = block_max_own(mx);
     if (tid == 0) {
@@ -2228,14 +2572,21 @@ struct Engine {
       c.cptr = a.cptr;
       c.crow = a.crow;
       c.cval = a.cval;
-      c.csc = ((const WsHeader *)a.ws)->csc_ok;
+      c.csc = a.sparse ? 1 : ((const WsHeader *)a.ws)->csc_ok;
+      c.sparse = a.sparse;
+      c.ktop = a.ktop;
+      c.rptr = a.rptr;
+      c.rcol = a.rcol;
+      c.rval = a.rval;
       c.prm = a.prm;
       c.cap = a.cap;
       c.tab = a.tab;
-      const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap);
+      const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap, a.sparse ? a.ktop : 0);
       c.kk = L.kk;
-      unsigned char *base = a.ws + sizeof(WsHeader) + ws_ar_bytes(a.m, a.n) + csc_layout(a.m, a.n).total +
+      unsigned char *base = a.ws + sizeof(WsHeader) + ws_dense_bytes(a.m, a.n, a.sparse) +
                             (size_t)slot * a.slot_bytes;
+      c.rowtmp = (double *)(base + L.rowtmp);
+      c.top = (int32_t *)(base + L.top);
       c.status = (int32_t *)a.ws;
       c.ur = (double *)(base + L.ur);
       c.uidx = (int32_t *)(base + L.uidx);
@@ -2271,6 +2622,10 @@ struct Engine {
       c.nleaf_n = pw_leaves(a.n, c.lf_lo + c.nleaf_m, c.lf_len + c.nleaf_m, (int)(2 * L.nleaf - c.nleaf_m));
     }
     __syncthreads();
+    if constexpr (SP) {  // the row scratch starts (and stays) zero; the workspace is not cleared by the host
+      for (int64_t j = tid; j < a.n; j += NT) sh->c.rowtmp[j] = 0.0;
+      __syncthreads();
+    }
   }
 
   __device__ void load_levels(const KArgs &a, int64_t inst) {

@@ -171,6 +171,132 @@ class SliceBatch:
         self._lb.check_status()
 
 
+class SparseSliceBatch:
+    """Tomography slices sharing a SPARSE projector, solved by the sparse
+    engine (``amvm_solve_sparse``): A stays CSC + CSR on the device (the
+    full 256^2 x 180 slice: ~340 MB instead of 2 x 24 GB dense copies).
+    Same results as :class:`SliceBatch` on the same inputs (bit for bit).
+
+    ``csr`` = (indptr int64[m+1], indices int64[nnz], values f64[nnz]) device
+    tensors with ascending columns per row (``projection_csr_device``); B is
+    slices x m, idx0 slices x n (host or device).  The start residual
+    A x0 - b is computed on the device in numpy's dense dgemv order."""
+
+    def __init__(self, csr, m: int, n: int, B, levels, idx0, device=None):
+        from . import _native as N
+
+        torch = N.torch_cuda()
+        self.torch, self.lib = torch, N.load_library()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        indptr, indices, values = (t.to(dev) for t in csr)
+        levels = np.asarray(levels, dtype=np.float64)
+        if levels.ndim != 1 or np.any(np.diff(levels) <= 0) or not np.all(np.isfinite(levels)):
+            raise ValueError("levels must be strictly increasing and finite")
+        B = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B, dtype=torch.float64).to(dev)
+        idx0 = torch.as_tensor(np.asarray(idx0) if not isinstance(idx0, torch.Tensor) else idx0).to(dev)
+        B = B.reshape(-1, m).contiguous()
+        idx0 = idx0.reshape(B.shape[0], n).to(torch.int32).contiguous()
+        if int(idx0.min()) < 0 or int(idx0.max()) >= levels.size:
+            raise ValueError("idx0 outside the level set")
+        self.m, self.n, self.count, self.nlev = m, n, B.shape[0], levels.size
+        self.nnz = int(values.numel())
+        # CSR with int32 columns; CSC (rows ascending per column) by a stable sort on the column
+        self.rptr = indptr.contiguous()
+        self.rcol = indices.to(torch.int32).contiguous()
+        self.rval = values.contiguous()
+        rows = torch.repeat_interleave(torch.arange(m, device=dev), indptr[1:] - indptr[:-1])
+        order = torch.sort(indices * m + rows, stable=True).indices
+        self.crow = rows[order].to(torch.int32).contiguous()
+        self.cval = values[order].contiguous()
+        counts = torch.bincount(indices, minlength=n)
+        self.cptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        self.cptr[1:] = torch.cumsum(counts, 0)
+        self.max_col_nnz = int(counts.max().item()) if n else 0
+        self.B = B
+        self.L = torch.from_numpy(np.tile(levels, (self.count, 1))).to(dev)
+        self.idx0 = idx0
+        lvd = torch.from_numpy(levels).to(dev)
+        X = lvd[idx0.long()].t().contiguous()                  # n x S level values of the start
+        y = projections_device((self.rptr, indices, self.rval), m, n, X)  # A @ x in numpy's dgemv order
+        self.r0 = (y - B).contiguous()
+        self.obj0 = self.r0.abs().amax(dim=1).contiguous()
+        self.cnt0 = torch.zeros(self.count, dtype=torch.int32, device=dev)
+
+    def problem(self):
+        from . import _native as N
+
+        return N.SparseProblem(self.m, self.n, self.nlev, self.count, self.nnz, self.max_col_nnz,
+                               self.cptr.data_ptr(), self.crow.data_ptr(), self.cval.data_ptr(),
+                               self.rptr.data_ptr(), self.rcol.data_ptr(), self.rval.data_ptr(),
+                               self.B.data_ptr(), self.L.data_ptr())
+
+    def workspace_bytes(self, cfg=None) -> int:
+        from . import _native as N
+        from .controller import SolverConfig, make_params
+
+        cfg = cfg or SolverConfig()
+        prm = make_params(cfg, self.n, time_budget=cfg.time_limit)
+        prob = self.problem()
+        return int(self.lib.amvm_sparse_workspace_bytes(N.C.byref(prob), N.C.byref(prm)))
+
+    def solve(self, cfg=None, seeds=None, trace: bool = False) -> dict:
+        """amvm_solve_sparse over the slices; returns device tensors (no sync),
+        the same dict as ``ptq.LayerBatch.solve``."""
+        from . import _native as N
+        from .controller import SolverConfig, make_params
+
+        torch = self.torch
+        cfg = cfg or SolverConfig()
+        dev = self.device
+        seeds = np.arange(self.count) if seeds is None else np.asarray(seeds)
+        # pinned + non_blocking: kept on self until the copy has run
+        self._rng_host = torch.from_numpy(N.seed_states(seeds).view(np.uint8)).pin_memory()
+        self.rng = self._rng_host.to(dev, non_blocking=True)
+        T = max(int(cfg.max_iters), 1)
+        c, m, n = self.count, self.m, self.n
+        o = {
+            "best_idx": torch.empty((c, n), dtype=torch.int32, device=dev),
+            "best_residual": torch.empty((c, m), dtype=torch.float64, device=dev),
+            "best_objective": torch.empty(c, dtype=torch.float64, device=dev),
+            "best_updates": torch.empty(c, dtype=torch.int32, device=dev),
+            "initial_objective": torch.empty(c, dtype=torch.float64, device=dev),
+            "iterations": torch.empty(c, dtype=torch.int32, device=dev),
+            "operator_uses": torch.empty((c, 4), dtype=torch.int64, device=dev),
+            "moves_scored": torch.empty((c, 2), dtype=torch.int64, device=dev),
+            "phase_cycles": torch.empty((c, 16), dtype=torch.int64, device=dev),
+        }
+        tr = [None] * 4
+        if trace:
+            for k, dt in (("trace_current_t", torch.float64), ("trace_best_t", torch.float64),
+                          ("trace_pair", torch.uint8), ("trace_accepted", torch.uint8)):
+                o[k] = torch.empty((c, T), dtype=dt, device=dev)
+            tr = [o[k].data_ptr() for k in ("trace_current_t", "trace_best_t", "trace_pair", "trace_accepted")]
+        res = N.ResultPtrs(
+            N.SolutionPtrs(o["best_idx"].data_ptr(), o["best_residual"].data_ptr(),
+                           o["best_objective"].data_ptr(), o["best_updates"].data_ptr()),
+            o["initial_objective"].data_ptr(), o["iterations"].data_ptr(), o["operator_uses"].data_ptr(),
+            *tr, o["moves_scored"].data_ptr(), o["phase_cycles"].data_ptr())
+        prm = make_params(cfg, n, time_budget=cfg.time_limit)
+        prob = self.problem()
+        nbytes = self.lib.amvm_sparse_workspace_bytes(N.C.byref(prob), N.C.byref(prm))
+        if nbytes == 0:
+            raise ValueError("problem shape or parameters rejected by libamvm")
+        ws = N.workspace(dev, nbytes)
+        start = N.SolutionPtrs(self.idx0.data_ptr(), self.r0.data_ptr(), self.obj0.data_ptr(),
+                               self.cnt0.data_ptr())
+        N.check(self.lib.amvm_solve_sparse(N.C.byref(prob), N.C.byref(prm), N.C.byref(start), N.ptr(self.rng),
+                                           N.C.byref(res), N.ptr(ws), N.C.c_size_t(ws.numel()),
+                                           N.stream_handle()), "amvm_solve_sparse")
+        self._ws = ws
+        return o
+
+    def check_status(self) -> None:
+        from . import _native as N
+
+        N.check(self.lib.amvm_status(N.ptr(self._ws), N.stream_handle()), "amvm_solve_sparse")
+
+
 def projection_csr_device(side: int, n_angles: int, device=None):
     """The projector built on the GPU (``amvm_projector_indptr`` /
     ``amvm_projector_fill``, csrc/amvm_tomo.cuh) as device CSR tensors
