@@ -51,6 +51,7 @@ print(json.dumps({"engine": "dense" if dense else "sparse", "config": f"{side}^2
                   "slice_iters_per_s": S * iters / (ms / 1e3),
                   "moves_per_s": float(o["moves_scored"][:, 0].sum()) / (ms / 1e3),
                   "peak_mem_GB": round(torch.cuda.max_memory_allocated() / 1e9, 2),
+                  "workspace_GB": round((sb.workspace_bytes(cfg) if not dense else 0) / 1e9, 2),
                   "setup_s": round(t1 - t0, 2),
                   "best_mean": float(o["best_objective"].mean()), "init_mean": float(o["initial_objective"].mean()),
                   "phase_share": {k: round(float(v / pc[:8].sum()), 3) for k, v in zip(names, pc[:8])},
