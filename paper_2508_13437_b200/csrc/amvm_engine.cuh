@@ -46,6 +46,10 @@ constexpr int kTJ = AMVM_TJ;  // find_candidates j-tile (level-sorted positions)
 #define AMVM_ROW_PASSES 24
 #endif
 constexpr int kDrainLong = 1024;  // queue length that keeps the batched passes going
+#ifndef AMVM_DRAIN_SHORT
+#define AMVM_DRAIN_SHORT 64
+#endif
+constexpr int kDrainShort = AMVM_DRAIN_SHORT;  // at or below: no row passes, warp-per-pair checks
 constexpr int kRowPasses = AMVM_ROW_PASSES;  // queue passes (one filter row each) before fc_rest
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
@@ -1217,7 +1221,9 @@ struct Engine {
     constexpr bool sp = SP;
     // (sparse engine: every remaining row as a pass -- a pass costs the row's
     // nonzeros plus the queue, cheaper than per-pair binary searches)
-    for (; q < nr && qn > 0 && (q < g + np || qn > kDrainLong || sp); ++q) {
+    // A short queue skips the passes (each pays a bound table and three
+    // barriers) and goes straight to the warp-per-pair check below.
+    for (; q < nr && qn > (sp ? 0 : kDrainShort) && (q < g + np || qn > kDrainLong || sp); ++q) {
       if (sp) {  // the row, densely, in the (zero) row scratch for this pass
         sp_row_scatter(rows[q], false);
         __syncthreads();
