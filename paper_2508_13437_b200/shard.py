@@ -47,15 +47,13 @@ def gather_rows(ids: np.ndarray, fields: dict, total: int, group=None) -> tuple[
     maxr = max(max(cnts), 1)
 
     def exchange(a: np.ndarray) -> np.ndarray:
+        # each field travels in its own dtype (int8 codes: 1 byte per variable)
         a = np.asarray(a)
         tail = a.shape[1:]
         width = int(np.prod(tail)) if tail else 1
-        if a.dtype.kind == "f":
-            dt, npdt = torch.float64, np.float64
-        elif a.dtype == np.uint8 and a.dtype.kind == "u":
-            dt, npdt = torch.uint8, np.uint8  # codes travel as bytes (int4 grids fit)
-        else:
-            dt, npdt = torch.int64, np.int64
+        npdt = a.dtype if a.dtype in (np.int8, np.uint8, np.int16, np.int32, np.int64, np.float32,
+                                      np.float64) else (np.float64 if a.dtype.kind == "f" else np.int64)
+        dt = torch.from_numpy(np.zeros(1, dtype=npdt)).dtype
         buf = torch.zeros((maxr, width), dtype=dt, device=dev)
         if k:
             buf[:k] = torch.from_numpy(np.ascontiguousarray(a.reshape(k, width), dtype=npdt)).to(dev)
