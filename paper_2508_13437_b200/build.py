@@ -47,7 +47,10 @@ def _obj(unit: str) -> str:
 
 
 def _stale() -> bool:
-    return _newer(LIB, [d for u in UNITS for d in _deps(u)])
+    # per object against its sources, then the library against the objects
+    # (a library linked after an edit must not hide a stale object)
+    return (any(_newer(_obj(u), _deps(u)) for u in UNITS)
+            or _newer(LIB, [d for u in UNITS for d in _deps(u)] + [_obj(u) for u in UNITS]))
 
 
 def nvcc() -> str:

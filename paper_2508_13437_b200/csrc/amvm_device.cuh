@@ -221,10 +221,11 @@ __device__ double pw_leaf(F &&get, int64_t lo, int64_t n) {
 }
 
 // Leaves of the pairwise tree of length n, in left-to-right order.  Returns
-// the count (<= cap); leaf k covers [lo[k], lo[k]+len[k]).
-__device__ inline int pw_leaves(int64_t n, int64_t *lo, int64_t *len, int cap) {
+// the count (<= cap); leaf k covers [lo[k], lo[k]+len[k]).  st_lo / st_n: a
+// 48-deep scratch stack supplied by the caller (shared memory in the engine,
+// so the kernel keeps no local-memory stack frame for it).
+__device__ inline int pw_leaves(int64_t n, int64_t *lo, int64_t *len, int cap, int64_t *st_lo, int64_t *st_n) {
   // explicit stack of (lo, n); push right then left so leaves pop in order
-  int64_t st_lo[48], st_n[48];
   int sp = 0, cnt = 0;
   st_lo[sp] = 0;
   st_n[sp++] = n;
@@ -250,11 +251,10 @@ __device__ inline int pw_leaves(int64_t n, int64_t *lo, int64_t *len, int cap) {
 }
 
 // Combine leaf sums in the exact tree order (recursive shape, iterative walk).
-__device__ inline double pw_combine(int64_t n, const double *leaf_sum) {
+// st_n / st_state / st_val: 48-deep caller scratch (see pw_leaves).
+__device__ inline double pw_combine(int64_t n, const double *leaf_sum, int64_t *st_n, int *st_state,
+                                    double *st_val) {
   // post-order evaluation with an explicit stack
-  int64_t st_n[48];
-  int st_state[48];
-  double st_val[48];
   int sp = 0, leaf = 0;
   st_n[0] = n;
   st_state[0] = 0;

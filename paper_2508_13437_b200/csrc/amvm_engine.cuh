@@ -49,12 +49,20 @@ constexpr int kDrainLong = 1024;  // queue length that keeps the batched passes 
 #ifndef AMVM_DRAIN_SHORT
 #define AMVM_DRAIN_SHORT 64
 #endif
+#ifndef AMVM_FC_PAIRS
+#define AMVM_FC_PAIRS 4
+#endif
+// find_candidates enumerates lane-per-pair (instead of lane-per-i with the
+// row-0 prefix) when the mean non-empty level bucket holds fewer than this
+// many variables (0: never): the i-groups would leave most lanes idle
+constexpr int kFcPairs = AMVM_FC_PAIRS;
 constexpr int kDrainShort = AMVM_DRAIN_SHORT;  // at or below: no row passes, warp-per-pair checks
 constexpr int kRowPasses = AMVM_ROW_PASSES;  // queue passes (one filter row each) before fc_rest
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
+constexpr int kTKMax = 128;    // narrow impact tile (n < NT): rows at most
 // impact stream shapes (columns per thread, rows per slice, ring stages):
 // wide instances 4 x 2 x 2 (four independent exp chains per thread),
 // n < 4*NT: 1 x 8 x 3.  Both rings fit the phase scratch.
@@ -74,7 +82,7 @@ __host__ __device__ inline size_t fc_tb_off(int64_t nlev) { return ((size_t)8 * 
 __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
   size_t fc = fc_tb_off(nlev) + 8 * kG * kTJ + 4 * 2 * kTJ;
   if (tab) fc += 8 * kG * nlev * nlev;
-  size_t imp = 8 * kTC * (kTK + 1) + 16 * kTK;
+  size_t imp = 8 * kTC * (kTK + 1) + 16 * kTKMax;
   const size_t r4 = 8 * (size_t)kIS4 * kIC4 * kTC * kIR4, r1 = 8 * (size_t)kIS1 * kIC1 * kTC * kIR1;
   const size_t ring = r4 > r1 ? r4 : r1;
   if (ring > imp) imp = ring;
@@ -368,8 +376,13 @@ struct Shared {
   int nfilter_rows, srt_rows_sorted;  // select_rows result (rows[] count, ordered by |s| desc)
   int task_live, task_skip;
   int ntop;                       // sparse engine: rows in the |s| top list
+  int fc_pairs;                   // find_candidates: lane-per-pair enumeration (small level buckets)
+  uint64_t swap_best;             // best_swap: smallest complete t' so far (bit pattern)
   int spl[NT / 32 * 4];           // sparse one_opt window: chosen level per column (-1: none)
   double spt[NT / 32 * 4];        // ... and its objective
+  int64_t pw_a[48], pw_b[48];     // pairwise-sum tree walk stacks (thread 0 only)
+  int pw_s[48];
+  double pw_res;
   Pcg rng;
   Ctx c;
 };
@@ -418,9 +431,9 @@ struct Engine {
     AMVM_LOCALS
     for (int k = tid; k < nleaf; k += NT) lf_sum[k] = pw_leaf(get, lo[k], ln[k]);
     __syncthreads();
-    double s = pw_combine(len, lf_sum);
+    if (tid == 0) sh->pw_res = pw_combine(len, lf_sum, sh->pw_a, sh->pw_s, (double *)sh->pw_b);
     __syncthreads();
-    return s;
+    return sh->pw_res;  // rewritten only after the next call's first barrier
   }
 
   // Solution.refresh (core.py:173-177): numpy A @ x - b in the OpenBLAS order.
@@ -867,22 +880,27 @@ struct Engine {
   // the SET matters (the filter is an AND over rows); it is then ordered by
   // key so the tightest rows reject first.  Rows with s = 0 are dropped
   // (localsearch.py:151).  Returns the number of filter rows.
-  // Radix select of the kth largest |cr| key (8 passes of 8-bit digits):
-  // T = that key, need = how many rows with key == T belong to the top kth.
-  __device__ void radix_kth(int64_t kth, uint64_t &T, int64_t &need) {
+  // The kth largest |cr| key (kth >= 1): T = its bit pattern, need = how
+  // many keys equal to T belong to the top kth.  MSD radix select, 8-bit
+  // digits.  With a scratch `ck` (ccap keys), once the keys sharing the
+  // chosen prefix fit in it they are compacted there and the remaining
+  // passes histogram only them instead of rescanning all m rows.
+  __device__ void radix_kth(int64_t kth, uint64_t &T, int64_t &need, uint64_t *ck = nullptr, int ccap = 0) {
     AMVM_LOCALS
     uint64_t prefix = 0;
     int64_t remaining = kth;
+    int nc = -1;  // keys in ck (-1: not compacted, scan cr)
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int e = tid; e < 256; e += NT) sh->hist[e] = 0;
       __syncthreads();
       const uint64_t hm = shift == 56 ? 0ull : (~0ull << (shift + 8));
       // warp-aggregated histogram: |s| values of one instance share their
       // high digits, so plain per-thread atomics would serialise on a bin
-      for (int64_t i0 = (int64_t)warp * 32; i0 < m; i0 += NT) {
+      const int64_t len = nc >= 0 ? nc : m;
+      for (int64_t i0 = (int64_t)warp * 32; i0 < len; i0 += NT) {
         const int64_t i = i0 + lane;
-        const uint64_t key = i < m ? abs_key(cr[i]) : 0ull;
-        const bool in = i < m && (key & hm) == prefix;
+        const uint64_t key = i < len ? (nc >= 0 ? ck[i] : abs_key(cr[i])) : 0ull;
+        const bool in = i < len && (key & hm) == prefix;
         const unsigned act = __ballot_sync(AMVM_FULL, in);
         if (in) {
           const unsigned bin = (unsigned)(key >> shift) & 255u;
@@ -919,11 +937,29 @@ struct Engine {
           }
           sh->bc_i[0] = 255 - 8 * lane - e;
           sh->bc_i[1] = (int)cum;
+          sh->bc_i[3] = (int)h[e];  // keys sharing the new prefix
         }
+        if (lane == 0) sh->bc_i[2] = 0;
       }
       __syncthreads();
       prefix |= (uint64_t)sh->bc_i[0] << shift;
       remaining -= sh->bc_i[1];
+      if (ck && nc < 0 && shift > 0 && sh->bc_i[3] <= ccap) {  // block-uniform
+        const uint64_t hm2 = ~0ull << shift;
+        for (int64_t i0 = (int64_t)warp * 32; i0 < m; i0 += NT) {
+          const int64_t i = i0 + lane;
+          const uint64_t key = i < m ? abs_key(cr[i]) : 0ull;
+          const bool in = i < m && (key & hm2) == prefix;
+          const unsigned bal = __ballot_sync(AMVM_FULL, in);
+          if (!bal) continue;
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&sh->bc_i[2], __popc(bal));
+          base = __shfl_sync(AMVM_FULL, base, 0);
+          if (in) ck[base + __popc(bal & ((1u << lane) - 1u))] = key;
+        }
+        __syncthreads();
+        nc = sh->bc_i[3];
+      }
     }
     T = prefix;
     need = remaining;
@@ -1048,7 +1084,8 @@ struct Engine {
     __syncthreads();
     uint64_t T = 0;
     int64_t need = 0;
-    if (kk < m) radix_kth(kk, T, need);
+    // (the find_candidates scratch is free until the buckets are built)
+    if (kk < m) radix_kth(kk, T, need, (uint64_t *)scr, (int)(scratch_bytes(nlev, tab) / 8));
     // keys strictly above T (all rows when kk >= m), unordered
     for (int64_t i = tid; i < m; i += NT) {
       uint64_t key = abs_key(cr[i]);
@@ -1513,6 +1550,104 @@ struct Engine {
 #endif
   }
 
+  // fc_pass with one lane per (i, j) pair: for each i (one per warp, claimed
+  // in turn) the lanes sweep the tile's positions below i's level, test every
+  // staged row (row 0 first, the rest only when a lane survives it) and emit
+  // exactly what fc_pass emits -- the same survivor set in another order
+  // (every consumer of the list is order-free or sorts it).  For small level
+  // buckets (C1: 16 variables per level, C2: one), where fc_pass's i-groups
+  // leave most lanes idle.  Staged rows are laid out row-major per tile here
+  // ([q][e]: consecutive lanes, consecutive words).
+  template <int MODE>
+  __device__ void fc_pass_pairs(int nr, int g, double fD, int64_t fI) {
+    AMVM_LOCALS
+    int32_t *lst = (int32_t *)scr;
+    const int32_t *nxt = lst + (nlev + 1);
+    double *tq = (double *)(scr + fc_tb_off(nlev));  // [kG][kTJ]
+    int32_t *tl = (int32_t *)(tq + kG * kTJ);
+    int32_t *tj = tl + kTJ;
+    const double *bt = (const double *)(tj + kTJ);
+    const int32_t *perm = ibuf;
+    const int qcap = (int)fc_qcap(cap);
+    constexpr bool filt = MODE != FC_ALL;
+    constexpr bool counting = MODE == FC_COUNT;
+    // positions of the lowest non-empty level have nothing below them
+    const int64_t i0 = nxt[nlev] < nlev ? (int64_t)lst[nxt[nlev] + 1] : n;
+    for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
+      const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
+      const int w = (int)(p1 - p0);
+      for (int e = tid; e < w; e += NT) {
+        const int32_t j = perm[p0 + e];
+        tj[e] = j;
+        tl[e] = cidx[j];
+      }
+      for (int e = tid; e < g * w; e += NT) {
+        const int q = e / w, x = e - q * w;
+        tq[q * kTJ + x] = ag[(int64_t)q * n + p0 + x];
+      }
+      if (tid == 0) sh->gnext = 0;
+      __syncthreads();
+      const int64_t ib = i0 > p0 + 1 ? i0 : p0 + 1;  // i at or before p0: nothing below in the tile
+      for (;;) {
+        int64_t wi = 0;
+        if (lane == 0) wi = atomicAdd(&sh->gnext, 1);
+        const int64_t ip = ib + __shfl_sync(AMVM_FULL, wi, 0);
+        if (ip >= n) break;
+        const int32_t i = perm[ip];
+        const int ki = cidx[i];
+        const int64_t eend = ((int64_t)lst[ki] < p1 ? (int64_t)lst[ki] : p1) - p0;
+        if (eend <= 0) continue;
+        if (filt && (int64_t)i > fI && !(dsub(lv[ki], lv[nxt[nlev]]) > fD)) continue;  // even the largest delta is cut
+        const double xi = lv[ki];
+        double bi[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) bi[q] = q < g ? ag[(int64_t)q * n + ip] : 0.0;
+        for (int e0 = 0; e0 < eend; e0 += 32) {
+          const int e = e0 + lane;
+          const bool ok = e < eend;
+          const int ec = ok ? e : 0;
+          const int kj = tl[ec];
+          const double delta = dsub(xi, lv[kj]);
+          bool alive = ok;
+          if (filt) alive = alive && (delta > fD || (delta == fD && (int64_t)i <= fI));
+          if (g > 0)
+            alive = alive && dsub(tq[ec], bi[0]) < (tab ? bt[(int64_t)ki * nlev + kj] : ddiv(reps[0], delta));
+          if (!__any_sync(AMVM_FULL, alive)) continue;
+#pragma unroll
+          for (int q = 1; q < kG; ++q) {
+            if (q < g && alive) {
+              const double bq = tab ? bt[((int64_t)q * nlev + ki) * nlev + kj] : ddiv(reps[q], delta);
+              alive = dsub(tq[q * kTJ + ec], bi[q]) < bq;
+            }
+          }
+          const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+          if (!bal) continue;
+          if (nr <= g && counting) {
+            if (lane == 0) atomicAdd(&sh->counter, __popc(bal));
+            continue;
+          }
+          int bse = 0;
+          if (lane == 0) bse = atomicAdd(nr <= g ? &sh->counter : &sh->qcount, __popc(bal));
+          bse = __shfl_sync(AMVM_FULL, bse, 0);
+          if (alive) {
+            const int pos = bse + __popc(bal & ((1u << lane) - 1u));
+            const int32_t j = tj[e];
+            if (nr <= g) {
+              if (pos < cap) cbuf[pos] = Cand{i, j, delta};
+            } else if (pos < qcap) {
+              que[pos] = QEnt{i, j, (uint16_t)ki, (uint16_t)kj, 0u};
+            } else if (fc_rest(i, j, delta, nr, g)) {
+              fc_append(i, j, delta, counting);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (nr > g) fc_drain(nr, g, counting);
+    __syncthreads();
+  }
+
   __device__ int find_candidates(bool always_sort) {
     AMVM_LOCALS
 #ifdef AMVM_FC_PROFILE  // diagnostic: sub-phase cycles in pc[8..13]
@@ -1536,15 +1671,24 @@ struct Engine {
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) atomicAdd(&lfl[cidx[j]], 1);
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {  // exclusive prefix over the level counts (warp shuffle-scan, 32 levels a step)
       int32_t acc = 0;
-      for (int64_t k = 0; k < nlev; ++k) {
-        const int32_t c = lfl[k];
-        lst[k] = acc;
-        lfl[k] = acc;
-        acc += c;
+      for (int64_t k0 = 0; k0 < nlev; k0 += 32) {
+        const int64_t k = k0 + lane;
+        const int32_t c = k < nlev ? lfl[k] : 0;
+        int32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(AMVM_FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (k < nlev) {
+          lst[k] = acc + incl - c;
+          lfl[k] = acc + incl - c;
+        }
+        acc += __shfl_sync(AMVM_FULL, incl, 31);
       }
-      lst[nlev] = acc;
+      if (lane == 0) lst[nlev] = acc;
     }
     __syncthreads();
     for (int64_t j = tid; j < n; j += NT) perm[atomicAdd(&lfl[cidx[j]], 1)] = (int32_t)j;
@@ -1555,6 +1699,7 @@ struct Engine {
     // variables over 1024 levels)
     if (warp == 0) {
       int nxt = (int)nlev;
+      int64_t nne = 0;
       for (int64_t top = nlev - 1; top >= 0; top -= 32) {
         const int64_t k = top - lane;
         const bool ne = k >= 0 && lst[k + 1] > lst[k];
@@ -1563,10 +1708,15 @@ struct Engine {
         const unsigned above = bal & ((1u << lane) - 1u);
         if (k >= 0) lfl[k] = above ? (int)(top - (31 - __clz(above))) : nxt;
         if (bal) nxt = (int)(top - (31 - __clz(bal)));  // the lowest non-empty level in this chunk
+        nne += __popc(bal);
       }
-      if (lane == 0) lfl[nlev] = nxt;
+      if (lane == 0) {
+        lfl[nlev] = nxt;
+        sh->fc_pairs = n < (int64_t)kFcPairs * nne;
+      }
     }
     __syncthreads();
+    const bool pairs = sh->fc_pairs != 0;
     // sort every level bucket by the tightest row's folded value b0 (eps_0 = 0:
     // that row defines t), so each i's row-0 survivors in a bucket are a prefix
     // (sparse engine: row 0 densely in the row scratch for the fill loops)
@@ -1576,7 +1726,7 @@ struct Engine {
       __syncthreads();
     }
     auto row0 = [&](int32_t j) { return sp ? sh->c.rowtmp[j] : __ldg(Ar + (int64_t)rows[0] * n + j); };
-    {
+    if (!pairs) {  // (the lane-per-pair enumeration needs no order inside a bucket)
       int64_t n2 = 1;
       while (n2 < n) n2 <<= 1;
       if (n2 <= 65536 && nlev <= 32768 && fc_tb_off(nlev) + (size_t)12 * n2 <= scratch_bytes(nlev, tab)) {
@@ -1693,7 +1843,8 @@ struct Engine {
     }
     __syncthreads();
     FC_PROF(2);
-    fc_pass<FC_ALL>(nr, g, 0.0, 0);
+    if (sh->fc_pairs) fc_pass_pairs<FC_ALL>(nr, g, 0.0, 0);
+    else fc_pass<FC_ALL>(nr, g, 0.0, 0);
     FC_PROF(3);
     int cnt = sh->counter;
     __syncthreads();
@@ -1717,7 +1868,8 @@ struct Engine {
   __device__ int fc_count(int nr, int g, double fD, int64_t fI) {
     if (tid == 0) { sh->counter = 0; sh->qcount = 0; }
     __syncthreads();
-    fc_pass<FC_COUNT>(nr, g, fD, fI);
+    if (sh->fc_pairs) fc_pass_pairs<FC_COUNT>(nr, g, fD, fI);
+    else fc_pass<FC_COUNT>(nr, g, fD, fI);
     const int c = sh->counter;
     __syncthreads();
     return c;
@@ -1772,7 +1924,8 @@ struct Engine {
     }
     if (tid == 0) { sh->counter = 0; sh->qcount = 0; }
     __syncthreads();
-    fc_pass<FC_CUT>(nr, g, dc, ilo);
+    if (sh->fc_pairs) fc_pass_pairs<FC_CUT>(nr, g, dc, ilo);
+    else fc_pass<FC_CUT>(nr, g, dc, ilo);
     int cnt = sh->counter;
     __syncthreads();
     if (cnt > cap) {  // impossible: < maxc + n survivors up to the cut
@@ -1806,6 +1959,11 @@ struct Engine {
     const int nrows = sh->c.csc && sh->srt_rows_sorted ? sh->nfilter_rows : 0;
     constexpr bool sp = SP;
     if (sp) sp_select_top();
+    // CTA-wide best complete t' so far (bit pattern: t' >= 0 orders as an
+    // integer): a scan whose running max exceeds it cannot win, whatever the
+    // order the warps finish in, so the winner is the same as a full scan's
+    if (tid == 0) sh->swap_best = ~0ull;
+    __syncthreads();
     for (int c = warp; c < cnt; c += NW) {
       const Cand e = cbuf[c];
       double mx = 0.0;
@@ -1816,15 +1974,23 @@ struct Engine {
         const double *cj = At + (int64_t)e.j * m;
         mx = 0.0;
         int it = 0;
+        bool cut = false;
         for (int64_t r = lane; r < m; r += 32) {
           const double y = dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r))));
           mx = fmax(mx, fabs(y));
-          if ((++it & 15) == 0 && __any_sync(AMVM_FULL, mx >= t0)) break;
+          if ((++it & 7) == 0) {
+            const uint64_t sb = *(volatile uint64_t *)&sh->swap_best;
+            if (__any_sync(AMVM_FULL, mx >= t0 || abs_key(mx) > sb)) { cut = true; break; }
+          }
         }
         mx = warp_max(mx);
+        if (cut) continue;  // not improving, or beaten by a complete scan
       }
-      if (mx < t0 && (wi < 0 || mx < wt || (mx == wt && (e.i < wi || (e.i == wi && e.j < wj))))) {
-        wt = mx; wi = e.i; wj = e.j; wd = e.d;
+      if (mx < t0) {
+        if (lane == 0) atomicMin((unsigned long long *)&sh->swap_best, (unsigned long long)abs_key(mx));
+        if (wi < 0 || mx < wt || (mx == wt && (e.i < wi || (e.i == wi && e.j < wj)))) {
+          wt = mx; wi = e.i; wj = e.j; wd = e.d;
+        }
       }
     }
     if (tid == 0) sh->c.mv_ref += cnt;
@@ -2096,28 +2262,31 @@ struct Engine {
       impact_stream<kIC1, kIR1, kIS1>(na, t, tot);
       return;
     }
-    double *tile = (double *)scr;                      // kTC x (kTK+1)
-    double *rowv = tile + kTC * (kTK + 1);             // kTK x {|s_k|, (-alpha)(t - |s_k|)}
-    for (int64_t cb = 0; cb < n; cb += kTC) {
-      const int cols = (int)(n - cb < kTC ? n - cb : kTC);
-      double acc = 0.0;
-      for (int64_t kb = 0; kb < m; kb += kTK) {
-        const int rws = (int)(m - kb < kTK ? m - kb : kTK);
-        if (tid < kTK) {
-          const double sv = tid < rws ? fabs(cr[kb + tid]) : 0.0;
-          rowv[2 * tid] = sv;
-          rowv[2 * tid + 1] = dmul(na, dsub(t, sv));
-        }
-        double av[kPer];
+    // n < NT: one tile = the n columns x tk rows (tk = kTC*kTK/n, so no
+    // thread computes a term for a column that does not exist: C2 has 127)
+    const int tk = (int)((kTC * kTK) / n < kTKMax ? (kTC * kTK) / n : kTKMax);
+    double *tile = (double *)scr;                      // n x (tk+1)
+    double *rowv = tile + kTC * (kTK + 1);             // tk x {|s_k|, (-alpha)(t - |s_k|)}
+    const int cols = (int)n;
+    double acc = 0.0;
+    for (int64_t kb = 0; kb < m; kb += tk) {
+      const int rws = (int)(m - kb < tk ? m - kb : tk);
+      for (int k = tid; k < tk; k += NT) {
+        const double sv = k < rws ? fabs(cr[kb + k]) : 0.0;
+        rowv[2 * k] = sv;
+        rowv[2 * k + 1] = dmul(na, dsub(t, sv));
+      }
+      double av[kPer];
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int e = tid + q * NT, c = e / kTK, k = e - c * kTK;
-          av[q] = (c < cols && k < rws) ? fabs(__ldg(At + (cb + c) * m + kb + k)) : 0.0;
-        }
-        __syncthreads();
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * NT, c = e / tk, k = e - c * tk;
+        av[q] = (c < cols && k < rws) ? fabs(__ldg(At + c * m + kb + k)) : 0.0;
+      }
+      __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int e = tid + q * NT, c = e / kTK, k = e - c * kTK;
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * NT, c = e / tk, k = e - c * tk;
+        if (c < cols) {
           const double a = av[q];
           const double as = a > 0.0 ? a : 1.0;
           double y;
@@ -2126,17 +2295,14 @@ struct Engine {
           y = dfma(y, dfma(-as, y, 1.0), y);
           const double x = dmul(rowv[2 * k + 1], y);
           const double term = dmul(rowv[2 * k], exp_nonpos(x));
-          tile[c * (kTK + 1) + k] = a > 0.0 ? term : 0.0;
+          tile[c * (tk + 1) + k] = a > 0.0 ? term : 0.0;
         }
-        __syncthreads();
-        if (tid < cols)
-#pragma unroll
-          for (int k = 0; k < kTK; ++k)
-            if (k < rws) acc = dadd(acc, tile[tid * (kTK + 1) + k]);
       }
-      if (tid < cols) dbuf[cb + tid] = ddiv(acc, tot);
       __syncthreads();
+      if (tid < cols)
+        for (int k = 0; k < rws; ++k) acc = dadd(acc, tile[tid * (tk + 1) + k]);
     }
+    if (tid < cols) dbuf[tid] = ddiv(acc, tot);
     __syncthreads();
   }
 
@@ -2624,8 +2790,9 @@ struct Engine {
       o += scratch_bytes(a.nlev, a.tab);
       c.cr = a.cr_smem ? (double *)(amvm_dyn_smem + o) : (double *)(base + L.crg);
       // leaf trees of numpy's pairwise sum for lengths m and n
-      c.nleaf_m = pw_leaves(a.m, c.lf_lo, c.lf_len, (int)L.nleaf);
-      c.nleaf_n = pw_leaves(a.n, c.lf_lo + c.nleaf_m, c.lf_len + c.nleaf_m, (int)(2 * L.nleaf - c.nleaf_m));
+      c.nleaf_m = pw_leaves(a.m, c.lf_lo, c.lf_len, (int)L.nleaf, sh->pw_a, sh->pw_b);
+      c.nleaf_n = pw_leaves(a.n, c.lf_lo + c.nleaf_m, c.lf_len + c.nleaf_m, (int)(2 * L.nleaf - c.nleaf_m),
+                            sh->pw_a, sh->pw_b);
     }
     __syncthreads();
     if constexpr (SP) {  // the row scratch starts (and stays) zero; the workspace is not cleared by the host

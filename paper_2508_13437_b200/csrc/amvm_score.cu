@@ -20,10 +20,25 @@ int launch_adj_rt(const amvm_problem *prob, const int32_t *idx, const double *re
   if (cudaFuncSetAttribute(k_score_adj<CB, RT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return AMVM_ERR_CUDA;
-  k_score_adj<CB, RT, NC><<<G, NC + 32, smem, st>>>(prob->m, prob->n, prob->nlev, prob->count, prob->At,
-                                                    prob->levels, idx, residual, out_t, blk_t, blk_i, done, best,
-                                                    best_t);
-  return cuda_rc(cudaGetLastError());
+  // back-to-back scorer launches overlap one grid's tail with the next one's
+  // column stream (programmatic dependent launch; AMVM_SCORE_PDL=0 disables)
+  static const bool pdl = [] {
+    const char *e = getenv("AMVM_SCORE_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3(NC + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cuda_rc(cudaLaunchKernelEx(&cfg, k_score_adj<CB, RT, NC>, prob->m, prob->n, prob->nlev, prob->count,
+                                    prob->At, prob->levels, idx, residual, out_t, blk_t, blk_i, done, best,
+                                    best_t));
 }
 
 template <int CB, int NC>

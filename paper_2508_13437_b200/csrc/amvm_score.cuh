@@ -370,6 +370,11 @@ __global__ void __launch_bounds__(NC + 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: the next scorer launch on this stream may
+  // start its CTAs (and stream its columns) while this grid drains; it waits
+  // (griddepcontrol.wait below) before its first global store or ticket.
+  // Both are no-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   ADJ_TL(0);
   if (warp == NWc) {  // ---------------- producer warp: one lane issues every copy
     // each instance's residual goes into the queue ahead of its columns (a
@@ -501,6 +506,9 @@ __global__ void __launch_bounds__(NC + 32, 1)
         atomicMax(&cm[2 * (lc0 + (vid >> 1)) + (vid & 1)], (unsigned long long)__double_as_longlong(x[0]));
     }
     ADJ_TL(3);
+    // the previous grid on the stream (same outputs / workspace) has finished
+    // and its stores are visible before this one writes
+    if (c == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     adj_consumer_sync_n<NC>();  // every column's maxima complete
     if (!want_best) {  // scores only: no grid-wide reduction
       for (int q = tid; q < 2 * ncol; q += NC) {
