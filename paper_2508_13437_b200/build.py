@@ -4,6 +4,7 @@ from __future__ import annotations
 
 import os
 import subprocess
+import time
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -73,11 +74,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), file=sys.stderr)
-            procs.append((obj, subprocess.Popen(cmd)))
-    for obj, p in procs:
+            procs.append((obj, subprocess.Popen(cmd), time.time()))
+    for obj, p, t0 in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, f"nvcc {obj}")
         os.replace(obj + ".tmp", obj)
+        os.utime(obj, (t0, t0))  # stamped with the compile start: a source edited meanwhile stays newer
     tmp = LIB + ".tmp"
     subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
                     *[_obj(u) for u in UNITS]], check=True)

@@ -63,6 +63,9 @@ constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
 constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
 constexpr int kTKMax = 128;    // narrow impact tile (n < NT): rows at most
+#ifndef AMVM_IMPACT_PREFETCH
+#define AMVM_IMPACT_PREFETCH 0     // narrow impact tile: next tile's loads in flight while scoring
+#endif
 // impact stream shapes (columns per thread, rows per slice, ring stages):
 // wide instances 4 x 2 x 2 (four independent exp chains per thread),
 // n < 4*NT: 1 x 8 x 3.  Both rings fit the phase scratch.
@@ -377,7 +380,10 @@ struct Shared {
   int task_live, task_skip;
   int ntop;                       // sparse engine: rows in the |s| top list
   int fc_pairs;                   // find_candidates: lane-per-pair enumeration (small level buckets)
+  int fc_maxb;                    // find_candidates: largest level bucket
   uint64_t swap_best;             // best_swap: smallest complete t' so far (bit pattern)
+  int vrow[32];                   // best_swap: rows that recently proved a swap non-improving
+  int vins;                       // ... insertion counter (ring of 32)
   int spl[NT / 32 * 4];           // sparse one_opt window: chosen level per column (-1: none)
   double spt[NT / 32 * 4];        // ... and its objective
   int64_t pw_a[48], pw_b[48];     // pairwise-sum tree walk stacks (thread 0 only)
@@ -938,12 +944,21 @@ struct Engine {
           sh->bc_i[0] = 255 - 8 * lane - e;
           sh->bc_i[1] = (int)cum;
           sh->bc_i[3] = (int)h[e];  // keys sharing the new prefix
+          sh->bc_i[5] = (int64_t)h[e] == remaining - cum;  // ... and all of them are in the top kth
         }
         if (lane == 0) sh->bc_i[2] = 0;
       }
       __syncthreads();
       prefix |= (uint64_t)sh->bc_i[0] << shift;
       remaining -= sh->bc_i[1];
+      if (sh->bc_i[5] && prefix > 0) {
+        // every key with this prefix is needed: "key > prefix - 1" selects
+        // exactly the top kth (no ties to resolve), so the digits below are moot
+        T = prefix - 1;
+        need = 0;
+        __syncthreads();  // bc_i is rewritten by the next call
+        return;
+      }
       if (ck && nc < 0 && shift > 0 && sh->bc_i[3] <= ccap) {  // block-uniform
         const uint64_t hm2 = ~0ull << shift;
         for (int64_t i0 = (int64_t)warp * 32; i0 < m; i0 += NT) {
@@ -1362,19 +1377,21 @@ struct Engine {
       }
       if (tid == 0) sh->gnext = 0;
       __syncthreads();
-      int ki = 0;
+      // buckets are handed out from the highest level down: a group's work
+      // grows with the number of levels below it, so the longest groups
+      // start first and the warps finish together (longest-first order)
+      int ki = (int)nlev - 1;
       int64_t gbase = 0;  // first group id of bucket ki (groups are claimed in increasing order)
       for (;;) {
         int64_t grp = 0;
         if (lane == 0) grp = atomicAdd(&sh->gnext, 1);
         grp = __shfl_sync(AMVM_FULL, grp, 0);
         if (grp >= ngrp) break;
-        while (ki < nlev && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
+        while (ki >= 0 && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
           gbase += (lst[ki + 1] - lst[ki] + 31) >> 5;
-          ++ki;
+          --ki;
         }
-        if (ki >= nlev) break;
-        if (ki == 0) continue;  // no level below the lowest
+        if (ki <= 0) break;  // the lowest level has nothing below it (and every later group is there)
         if ((int64_t)lst[ki] <= p0) continue;  // no lower-level position in this tile
         const int64_t ip = lst[ki] + (grp - gbase) * 32 + lane;
         const bool have = ip < lst[ki + 1];
@@ -1591,8 +1608,8 @@ struct Engine {
       for (;;) {
         int64_t wi = 0;
         if (lane == 0) wi = atomicAdd(&sh->gnext, 1);
-        const int64_t ip = ib + __shfl_sync(AMVM_FULL, wi, 0);
-        if (ip >= n) break;
+        const int64_t ip = n - 1 - __shfl_sync(AMVM_FULL, wi, 0);  // highest level (most pairs) first
+        if (ip < ib) break;
         const int32_t i = perm[ip];
         const int ki = cidx[i];
         const int64_t eend = ((int64_t)lst[ki] < p1 ? (int64_t)lst[ki] : p1) - p0;
@@ -1700,9 +1717,11 @@ struct Engine {
     if (warp == 0) {
       int nxt = (int)nlev;
       int64_t nne = 0;
+      int maxb = 0;
       for (int64_t top = nlev - 1; top >= 0; top -= 32) {
         const int64_t k = top - lane;
         const bool ne = k >= 0 && lst[k + 1] > lst[k];
+        if (ne) maxb = max(maxb, lst[k + 1] - lst[k]);
         const unsigned bal = __ballot_sync(AMVM_FULL, ne);  // bit l: level top - l non-empty
         // next non-empty above k: the nearest set bit below lane l (higher level), else nxt
         const unsigned above = bal & ((1u << lane) - 1u);
@@ -1710,9 +1729,11 @@ struct Engine {
         if (bal) nxt = (int)(top - (31 - __clz(bal)));  // the lowest non-empty level in this chunk
         nne += __popc(bal);
       }
+      maxb = __reduce_max_sync(AMVM_FULL, maxb);
       if (lane == 0) {
         lfl[nlev] = nxt;
         sh->fc_pairs = n < (int64_t)kFcPairs * nne;
+        sh->fc_maxb = maxb;
       }
     }
     __syncthreads();
@@ -1726,7 +1747,38 @@ struct Engine {
       __syncthreads();
     }
     auto row0 = [&](int32_t j) { return sp ? sh->c.rowtmp[j] : __ldg(Ar + (int64_t)rows[0] * n + j); };
-    if (!pairs) {  // (the lane-per-pair enumeration needs no order inside a bucket)
+    if (!pairs && sh->fc_maxb <= 32) {
+      // every bucket fits a warp: one warp per bucket, a register bitonic sort
+      // by (b0, j) -- the same order the block sort below produces
+      for (int64_t k = warp; k < nlev; k += NW) {
+        const int b0 = lst[k], sz = lst[k + 1] - b0;
+        if (sz < 2) continue;
+        const bool ok = lane < sz;
+        int32_t j = ok ? perm[b0 + lane] : 0x7fffffff;
+        double bv = 0.0;
+        if (ok) {
+          const double a = row0(j);
+          bv = rsgn[0] ? a : -a;
+        }
+#pragma unroll
+        for (int kk2 = 2; kk2 <= 32; kk2 <<= 1) {
+#pragma unroll
+          for (int jj = kk2 >> 1; jj > 0; jj >>= 1) {
+            const double ob = __shfl_xor_sync(AMVM_FULL, bv, jj);
+            const int32_t oj = __shfl_xor_sync(AMVM_FULL, j, jj);
+            // invalid lanes (j = INT_MAX) sort last
+            const bool oinv = oj == 0x7fffffff, minv = j == 0x7fffffff;
+            const bool other_less = !oinv && (minv || ob < bv || (ob == bv && oj < j));
+            const bool lower = (lane & jj) == 0, up = (lane & kk2) == 0;
+            // keep the smaller in the lower lane of an ascending pair
+            const bool take = (lower == up) ? other_less : (!other_less && oj != j);
+            if (take) { bv = ob; j = oj; }
+          }
+        }
+        if (ok) perm[b0 + lane] = j;
+      }
+      __syncthreads();
+    } else if (!pairs) {  // (the lane-per-pair enumeration needs no order inside a bucket)
       int64_t n2 = 1;
       while (n2 < n) n2 <<= 1;
       if (n2 <= 65536 && nlev <= 32768 && fc_tb_off(nlev) + (size_t)12 * n2 <= scratch_bytes(nlev, tab)) {
@@ -1972,15 +2024,27 @@ struct Engine {
       } else if (!(nrows > 0 && swap_tprime_sparse(e.i, e.j, e.d, nrows, mx))) {
         const double *ci = At + (int64_t)e.i * m;
         const double *cj = At + (int64_t)e.j * m;
+        {  // screen: the rows that cut earlier candidates (one per lane; exact proofs)
+          const int r = *(volatile int *)&sh->vrow[lane];
+          const double y = fabs(dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r)))));
+          const uint64_t sb = *(volatile uint64_t *)&sh->swap_best;
+          if (__any_sync(AMVM_FULL, y >= t0 || abs_key(y) > sb)) continue;
+        }
         mx = 0.0;
+        int64_t mr = lane;  // the row attaining this lane's max
         int it = 0;
         bool cut = false;
         for (int64_t r = lane; r < m; r += 32) {
-          const double y = dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r))));
-          mx = fmax(mx, fabs(y));
+          const double y = fabs(dadd(cr[r], dmul(e.d, dsub(__ldg(cj + r), __ldg(ci + r)))));
+          if (y > mx) { mx = y; mr = r; }
           if ((++it & 7) == 0) {
             const uint64_t sb = *(volatile uint64_t *)&sh->swap_best;
-            if (__any_sync(AMVM_FULL, mx >= t0 || abs_key(mx) > sb)) { cut = true; break; }
+            const unsigned hit = __ballot_sync(AMVM_FULL, mx >= t0 || abs_key(mx) > sb);
+            if (hit) {  // remember the row that proved it for the screen
+              if (lane == __ffs(hit) - 1) sh->vrow[atomicAdd(&sh->vins, 1) & 31] = (int)mr;
+              cut = true;
+              break;
+            }
           }
         }
         mx = warp_max(mx);
@@ -2269,6 +2333,19 @@ struct Engine {
     double *rowv = tile + kTC * (kTK + 1);             // tk x {|s_k|, (-alpha)(t - |s_k|)}
     const int cols = (int)n;
     double acc = 0.0;
+    // the next tile's A entries are loaded while this one is scored
+    double av[kPer];
+    auto load = [&](int64_t kb0, double *dst) {
+      const int rws0 = (int)(m - kb0 < tk ? m - kb0 : tk);
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * NT, c = e / tk, k = e - c * tk;
+        dst[q] = (kb0 < m && c < cols && k < rws0) ? fabs(__ldg(At + c * m + kb0 + k)) : 0.0;
+      }
+    };
+#if AMVM_IMPACT_PREFETCH
+    load(0, av);
+#endif
     for (int64_t kb = 0; kb < m; kb += tk) {
       const int rws = (int)(m - kb < tk ? m - kb : tk);
       for (int k = tid; k < tk; k += NT) {
@@ -2276,13 +2353,14 @@ struct Engine {
         rowv[2 * k] = sv;
         rowv[2 * k + 1] = dmul(na, dsub(t, sv));
       }
-      double av[kPer];
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const int e = tid + q * NT, c = e / tk, k = e - c * tk;
-        av[q] = (c < cols && k < rws) ? fabs(__ldg(At + c * m + kb + k)) : 0.0;
-      }
+#if !AMVM_IMPACT_PREFETCH
+      load(kb, av);
+#endif
       __syncthreads();
+#if AMVM_IMPACT_PREFETCH
+      double avn[kPer];
+      load(kb + tk, avn);
+#endif
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         const int e = tid + q * NT, c = e / tk, k = e - c * tk;
@@ -2301,6 +2379,10 @@ struct Engine {
       __syncthreads();
       if (tid < cols)
         for (int k = 0; k < rws; ++k) acc = dadd(acc, tile[tid * (tk + 1) + k]);
+#if AMVM_IMPACT_PREFETCH
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) av[q] = avn[q];
+#endif
     }
     if (tid < cols) dbuf[tid] = ddiv(acc, tot);
     __syncthreads();
@@ -2794,6 +2876,8 @@ struct Engine {
       c.nleaf_n = pw_leaves(a.n, c.lf_lo + c.nleaf_m, c.lf_len + c.nleaf_m, (int)(2 * L.nleaf - c.nleaf_m),
                             sh->pw_a, sh->pw_b);
     }
+    if (tid < 32) sh->vrow[tid] = 0;  // any row index < m is a valid screen row
+    if (tid == 0) sh->vins = 0;
     __syncthreads();
     if constexpr (SP) {  // the row scratch starts (and stays) zero; the workspace is not cleared by the host
       for (int64_t j = tid; j < a.n; j += NT) sh->c.rowtmp[j] = 0.0;

@@ -14,8 +14,12 @@ import tempfile
 def line_map(lib, kern):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
-    cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-    out = subprocess.run(["nvdisasm", "-gi", os.path.join(d, cub)], capture_output=True, text=True).stdout
+    out = ""
+    for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):  # one per translation unit
+        o = subprocess.run(["nvdisasm", "-gi", os.path.join(d, cub)], capture_output=True, text=True).stdout
+        if f".text.{kern}:" in o:
+            out = o
+            break
     m, cur, inside, block = {}, None, False, []
     for line in out.splitlines():
         if line.startswith(".text."):
