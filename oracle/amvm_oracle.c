@@ -314,8 +314,19 @@ static int64_t choice_p(pcg_t *g, const double *p, int64_t k, double *cdf) {
 typedef struct {
   int64_t m, n, nlev;
   const double *A; /* row-major m x n (reference layout, core.py:84) */
+  const double *At; /* optional column-major copy (n x m) or NULL: column
+                       scans read it instead of striding A (same values,
+                       same arithmetic order: speed only, for full-size
+                       goldens) */
   const double *b, *lv;
 } oprob;
+
+/* column j of A as (pointer, stride): element i at c[i * st] */
+static const double *acol(const oprob *P, int64_t j, int64_t *st) {
+  if (P->At) { *st = 1; return P->At + j * P->m; }
+  *st = P->n;
+  return P->A + j;
+}
 
 typedef struct {
   int32_t *idx;
@@ -357,7 +368,9 @@ static void apply_shift(const oprob *P, const amvm_params *prm, osol *S, int64_t
   int32_t old = S->idx[j];
   if (nl == old) return;
   double d = P->lv[nl] - P->lv[old];
-  for (int64_t i = 0; i < P->m; i++) S->r[i] = S->r[i] + d * P->A[i * P->n + j];
+  int64_t st;
+  const double *cj = acol(P, j, &st);
+  for (int64_t i = 0; i < P->m; i++) S->r[i] = S->r[i] + d * cj[i * st];
   S->idx[j] = nl;
   bump(P, prm, S);
 }
@@ -366,10 +379,9 @@ static void apply_shift(const oprob *P, const amvm_params *prm, osol *S, int64_t
 static void apply_swap(const oprob *P, const amvm_params *prm, osol *S, int64_t i, int64_t j) {
   double xi = P->lv[S->idx[i]], xj = P->lv[S->idx[j]];
   double dl = xi - xj;
-  for (int64_t k = 0; k < P->m; k++) {
-    const double *row = P->A + k * P->n;
-    S->r[k] = S->r[k] + dl * (row[j] - row[i]);
-  }
+  int64_t st;
+  const double *ci = acol(P, i, &st), *cj = acol(P, j, &st);
+  for (int64_t k = 0; k < P->m; k++) S->r[k] = S->r[k] + dl * (cj[k * st] - ci[k * st]);
   int32_t t = S->idx[i];
   S->idx[i] = S->idx[j];
   S->idx[j] = t;
@@ -406,8 +418,10 @@ static void one_opt(const oprob *P, const amvm_params *prm, osol *S, ocount *C) 
         if (c < 0 || c >= P->nlev) continue;
         double d = lv[c] - lv[k];
         double t = 0.0;
+        int64_t st;
+        const double *cj = acol(P, j, &st);
         for (int64_t i = 0; i < P->m; i++) {
-          double v = fabs(S->r[i] + d * P->A[i * P->n + j]);
+          double v = fabs(S->r[i] + d * cj[i * st]);
           if (v > t) t = v;
         }
         if (C) { C->moves_ref++; C->moves_raw++; }
@@ -505,9 +519,10 @@ static int best_swap(const oprob *P, const amvm_params *prm, const osol *S, int3
   double best = 0;
   for (int64_t q = 0; q < cnt; q++) {
     double tn = 0.0;
+    int64_t st;
+    const double *ci = acol(P, c[q].i, &st), *cj = acol(P, c[q].j, &st);
     for (int64_t k = 0; k < P->m; k++) {
-      const double *row = P->A + k * P->n;
-      double v = fabs(S->r[k] + c[q].delta * (row[c[q].j] - row[c[q].i]));
+      double v = fabs(S->r[k] + c[q].delta * (cj[k * st] - ci[k * st]));
       if (v > tn) tn = v;
     }
     if (C) { C->moves_ref++; C->moves_raw++; }
@@ -757,10 +772,11 @@ typedef struct {
   const double *A;      /* m x n row-major */
   const double *B;      /* count x m */
   const double *levels; /* count x nlev */
+  const double *At;     /* optional n x m column-major copy of A, or NULL */
 } orc_problem;
 
 static void mk_prob(const orc_problem *p, int64_t k, oprob *P) {
-  P->m = p->m; P->n = p->n; P->nlev = p->nlev; P->A = p->A;
+  P->m = p->m; P->n = p->n; P->nlev = p->nlev; P->A = p->A; P->At = p->At;
   P->b = p->B + k * p->m;
   P->lv = p->levels + k * p->nlev;
 }

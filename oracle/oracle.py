@@ -53,7 +53,8 @@ class Result(C.Structure):
 
 class Problem(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("nlev", C.c_int64), ("count", C.c_int64),
-                ("A", C.c_void_p), ("B", C.c_void_p), ("levels", C.c_void_p)]
+                ("A", C.c_void_p), ("B", C.c_void_p), ("levels", C.c_void_p),
+                ("At", C.c_void_p)]  # optional column-major copy (speed only), NULL
 
 
 def build() -> str:
@@ -121,13 +122,18 @@ def pcg_to_state(g: PCG) -> dict:
 class _Batch:
     """Owns the numpy buffers behind one oracle call."""
 
-    def __init__(self, A, B, L):
+    def __init__(self, A, B, L, colmajor: bool = False):
         self.A = np.ascontiguousarray(A, dtype=np.float64)
         self.B = np.ascontiguousarray(np.atleast_2d(B), dtype=np.float64)
         self.L = np.ascontiguousarray(np.atleast_2d(L), dtype=np.float64)
         m, n = self.A.shape
+        # colmajor: also hand over A^T so column scans are contiguous (same
+        # values in the same order; for full-size goldens, where the
+        # reference's strided A[:, j] would take hours)
+        self.At = np.ascontiguousarray(self.A.T) if colmajor else None
         self.prob = Problem(m, n, self.L.shape[1], self.B.shape[0], self.A.ctypes.data,
-                            self.B.ctypes.data, self.L.ctypes.data)
+                            self.B.ctypes.data, self.L.ctypes.data,
+                            self.At.ctypes.data if colmajor else None)
 
 
 def _sol(idx, r, obj, cnt):
@@ -138,13 +144,14 @@ def _sol(idx, r, obj, cnt):
     return (idx, r, obj, cnt), Sol(idx.ctypes.data, r.ctypes.data, obj.ctypes.data, cnt.ctypes.data)
 
 
-def solve(A, B, levels, idx0, r0, obj0, cnt0, prm: Params, states, threads: int = 1) -> dict:
+def solve(A, B, levels, idx0, r0, obj0, cnt0, prm: Params, states, threads: int = 1,
+          colmajor: bool = False) -> dict:
     """Oracle counterpart of amvm_solve on HOST arrays.
 
     ``B``/``levels``/``idx0``/``r0`` may be 1-d (one instance) or stacked;
     ``states`` is one PCG (or numpy state dict) per instance.
     """
-    bt = _Batch(A, B, levels)
+    bt = _Batch(A, B, levels, colmajor)
     count, m, n = bt.prob.count, bt.prob.m, bt.prob.n
     keep, start = _sol(idx0, r0, obj0, cnt0)
     if not isinstance(states, (list, tuple)):

@@ -2336,11 +2336,22 @@ struct Engine {
     // the next tile's A entries are loaded while this one is scored
     double av[kPer];
     auto load = [&](int64_t kb0, double *dst) {
+      // unconditional loads from clamped (always valid) addresses, masked
+      // after: all kPer loads are in flight together instead of one
+      // predicated load-use pair at a time
       const int rws0 = (int)(m - kb0 < tk ? m - kb0 : tk);
+      const int64_t kbc = kb0 < m ? kb0 : 0;
+      double raw[kPer];
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         const int e = tid + q * NT, c = e / tk, k = e - c * tk;
-        dst[q] = (kb0 < m && c < cols && k < rws0) ? fabs(__ldg(At + c * m + kb0 + k)) : 0.0;
+        const int cc = c < cols ? c : cols - 1, kc = k < rws0 ? k : 0;
+        raw[q] = __ldg(At + cc * m + kbc + kc);
+      }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * NT, c = e / tk, k = e - c * tk;
+        dst[q] = (kb0 < m && c < cols && k < rws0) ? fabs(raw[q]) : 0.0;
       }
     };
 #if AMVM_IMPACT_PREFETCH

@@ -1,7 +1,7 @@
 """Full-size C3 slice golden (256^2 phantom, 180 angles: m = 46080, n = 65536,
 3 grey levels) for the sparse engine, made with the CPU oracle port (the
 unmodified Python reference cannot run this size: its find_candidates builds
-a 34 GB n x n matrix).  Dev container only (needs ~26 GB):
+a 34 GB n x n matrix).  Dev container only (needs ~50 GB: A and its column-major copy):
 
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden_c3full.py
 
@@ -50,7 +50,7 @@ def main() -> None:
     print(f"built in {time.time() - t0:.1f} s; m={m} n={n} nnz={int((A != 0).sum())} obj0={obj0}", flush=True)
     prm = O.make_params(n, max_iters=ITERS)
     t1 = time.time()
-    out = O.solve(A, b, LV, idx0, r0, obj0, 0, prm, O.pcg_from_seed(0))
+    out = O.solve(A, b, LV, idx0, r0, obj0, 0, prm, O.pcg_from_seed(0), colmajor=True)
     print(f"oracle {ITERS} iterations in {time.time() - t1:.1f} s: best {out['best_objective'][0]}", flush=True)
     rec = {"side": SIDE, "angles": ANGLES, "m": m, "n": n, "eta": eta, "b": b, "idx0": idx0.astype(np.int8),
            "obj0": obj0, "r0_sha": mg.sha(r0), "A_sha": mg.sha(A), "iterations": int(out["iterations"][0]),
