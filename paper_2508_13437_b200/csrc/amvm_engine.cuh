@@ -2625,38 +2625,68 @@ struct Engine {
     for (int64_t q = 0; q < r; ++q) {
       const double total = block_pairwise(gd, n, lf_lo + nleaf_m, lf_len + nleaf_m, nleaf_n);
       if (!(total > 0.0)) {
-        // mass exhausted: rng.choice(setdiff1d(arange(n), picked), r - q, False)
+        // mass exhausted: rng.choice(setdiff1d(arange(n), picked), r - q, False);
+        // the set difference (ascending) by the whole block: mark the picks,
+        // then an order-preserving compaction, NT positions per step
+        int32_t *rest = (int32_t *)pbuf;  // n int32 fit in n doubles
+        for (int64_t k = tid; k < n; k += NT) ibuf[k] = 0;
+        __syncthreads();
+        for (int64_t k = tid; k < q; k += NT) ibuf[pick[k]] = 1;
+        __syncthreads();
+        int64_t base = 0;
+        for (int64_t c0 = 0; c0 < n; c0 += NT) {
+          const int64_t k = c0 + tid;
+          const bool f = k < n && !ibuf[k];
+          const unsigned bal = __ballot_sync(AMVM_FULL, f);
+          if (lane == 0) sh->wcnt[warp] = __popc(bal);
+          __syncthreads();
+          int before = 0, tot = 0;
+          for (int w = 0; w < NW; ++w) {
+            if (w < warp) before += sh->wcnt[w];
+            tot += sh->wcnt[w];
+          }
+          if (f) rest[base + before + __popc(bal & ((1u << lane) - 1u))] = (int32_t)k;
+          base += tot;
+          __syncthreads();
+        }
         if (tid == 0) {
-          for (int64_t k = 0; k < n; ++k) ibuf[k] = 0;
-          for (int64_t k = 0; k < q; ++k) ibuf[pick[k]] = 1;
-          int32_t *rest = (int32_t *)pbuf;  // n int32 fit in n doubles
-          int64_t nrest = 0;
-          for (int64_t k = 0; k < n; ++k)
-            if (!ibuf[k]) rest[nrest++] = (int32_t)k;
-          choice_noreplace(sh->rng, nrest, r - q, pick + q);
+          choice_noreplace(sh->rng, base, r - q, pick + q);
           for (int64_t k = q; k < r; ++k) pick[k] = rest[pick[k]];
         }
         break;
       }
-      for (int64_t k = tid; k < n; k += NT) pbuf[k] = ddiv(dbuf[k], total);
+      // p = d / total, also into the (idle) phase scratch when it fits, so
+      // the sequential cumsum below reads shared memory
+      double *const ps = (size_t)n * 8 <= scratch_bytes(nlev, tab) ? (double *)scr : pbuf;
+      for (int64_t k = tid; k < n; k += NT) {
+        const double v = ddiv(dbuf[k], total);
+        pbuf[k] = v;
+        ps[k] = v;
+      }
       __syncthreads();
       if (warp == 0) {
         // Generator.choice(n, p): cdf = cumsum(p); cdf /= cdf[-1];
         // searchsorted(cdf, random(), 'right').  The cumsum is numpy's
-        // sequential chain; warp 0 runs it with coalesced loads and
-        // shuffle-broadcast adds (every lane holds the identical running
-        // sum), keeping the value before each 32-element chunk so the search
-        // rescans one chunk instead of storing the whole cdf.
+        // sequential chain: lane 0 runs it as a bare DADD chain (the loads
+        // are independent of it and run ahead), keeping the value before
+        // each 32-element chunk so the search rescans one chunk instead of
+        // storing the whole cdf.
         const int64_t nch = (n + 31) / 32;
         double acc = 0.0;
-        for (int64_t c = 0; c < nch; ++c) {
-          const int64_t k = c * 32 + lane;
-          const double pv = k < n ? pbuf[k] : 0.0;
-          if (lane == 0) cbk[c] = acc;
-          const int cnt = (int)(n - c * 32 < 32 ? n - c * 32 : 32);
-          for (int l = 0; l < cnt; ++l) acc = dadd(acc, __shfl_sync(AMVM_FULL, pv, l));
+        if (lane == 0) {
+          for (int64_t c = 0; c < nch; ++c) {
+            cbk[c] = acc;
+            const double *pc = ps + c * 32;
+            if (n - c * 32 >= 32) {
+#pragma unroll
+              for (int l = 0; l < 32; ++l) acc = dadd(acc, pc[l]);
+            } else {
+              for (int l = 0; l < (int)(n - c * 32); ++l) acc = dadd(acc, pc[l]);
+            }
+          }
         }
-        const double last = acc;  // cdf[n-1]
+        __syncwarp();
+        const double last = __shfl_sync(AMVM_FULL, acc, 0);  // cdf[n-1]
         double u = 0.0;
         if (lane == 0) u = pcg_random(sh->rng);
         u = __shfl_sync(AMVM_FULL, u, 0);
