@@ -361,18 +361,39 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
                   ws.numel(), N.stream_handle()) for p_ in probs]
         for k in range(2 * copies):
             N.check(lib.amvm_score_moves(*calls[k % copies]), "amvm_score_moves")
-        per = []
+        torch.cuda.synchronize()
+        # the launches captured once in a CUDA graph and replayed, so the
+        # events time the GPU and not the host's per-call issue rate (the
+        # ctypes call + launch take about as long as the ~14 us kernel)
+        g_ = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(st)
+        with torch.cuda.stream(cs):
+            g_.capture_begin()
+            for k in range(launches):
+                N.check(lib.amvm_score_moves(*calls[k % copies][:-1], N.stream_handle()), "amvm_score_moves")
+            g_.capture_end()
+        st.wait_stream(cs)
+        g_.replay()
+        torch.cuda.synchronize()
+        per, host = [], []
         for _ in range(5):
             flush.zero_()
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g_.replay()
+            b_.record(st)
+            torch.cuda.synchronize()
+            per.append(a.elapsed_time(b_) / launches)
+            flush.zero_()  # the same launches issued one by one from the host
             a.record(st)
             for k in range(launches):
                 N.check(lib.amvm_score_moves(*calls[k % copies]), "amvm_score_moves")
             b_.record(st)
             torch.cuda.synchronize()
-            per.append(a.elapsed_time(b_) / launches)
-        del Ats
-        return float(np.median(per)), launches
+            host.append(a.elapsed_time(b_) / launches)
+        del Ats, g_
+        return float(np.median(per)), launches, float(np.median(host))
 
     def leg(count, mode, flush_each):
         lv = torch.linspace(-1, 1, nlev, dtype=torch.float64).repeat(count, 1).to(dev)
@@ -401,8 +422,13 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
 
     pk = peaks()
     ms1, ms1_min, live1 = leg(1, "adjacent", True)
-    msc, launches = cycled()
-    msb_c, _ = cycled(with_best=True)
+    msc, launches, msc_host = cycled()
+    msb_c, _, _ = cycled(with_best=True)
+    os.environ["AMVM_SCORE_PDL"] = "0"  # the same launches without programmatic dependent launch
+    try:
+        msc_nopdl, _, _ = cycled()
+    finally:
+        del os.environ["AMVM_SCORE_PDL"]
     alg = 8 * m * n + 8 * m + 4 * n + 16 * n
     gbs = alg / (msc / 1e3) / 1e9
     gbs1 = alg / (ms1 / 1e3) / 1e9
@@ -415,7 +441,13 @@ def scorer_roofline(X, dev, flush, reps: int = 20, batch: int = 512) -> dict:
                      "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic,
                      "kernel": "k_score_adj (north-star scorer (c): adjacent set |V_s| = 2, every score of one "
                                f"C5 instance m=2048 x n=4096; {launches} back-to-back launches cycling over 4 copies "
-                               "of A (256 MiB > L2), average per launch, median of 5 runs)",
+                               "of A (256 MiB > L2), replayed from a CUDA graph, average per launch, median of 5 "
+                               "runs; consecutive launches overlap one grid's tail with the next grid's column "
+                               "stream (programmatic dependent launch, griddepcontrol))",
+                     "host_issued_ms_per_launch": round(msc_host, 5),
+                     "without_pdl": {"ms_per_launch": round(msc_nopdl, 5),
+                                     "GBps": round(alg / (msc_nopdl / 1e3) / 1e9, 1),
+                                     "frac": round(alg / (msc_nopdl / 1e3) / 1e9 / pk["hbm_gbs"], 4)},
                      "with_fused_best_move": {"ms_per_launch": round(msb_c, 5),
                                               "GBps": round(alg / (msb_c / 1e3) / 1e9, 1),
                                               "frac": round(alg / (msb_c / 1e3) / 1e9 / pk["hbm_gbs"], 4)},

@@ -17,15 +17,21 @@ template <int CB, int RT, int NC>
 int launch_adj_rt(const amvm_problem *prob, const int32_t *idx, const double *residual, double *out_t, int64_t *best,
                   double *best_t, double *blk_t, int64_t *blk_i, unsigned *done, int G, cudaStream_t st) {
   const size_t smem = adj_smem_bytes(prob->m, CB, (prob->n + G - 1) / G, prob->nlev);
-  if (cudaFuncSetAttribute(k_score_adj<CB, RT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return AMVM_ERR_CUDA;
+  // the attribute is raised once per instantiation and device (a driver call
+  // per launch would dominate back-to-back launches of a ~14 us kernel)
+  static int dev_ok[64];  // largest smem set so far, per device (0: none)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return AMVM_ERR_CUDA;
+  if ((int)smem > dev_ok[dev]) {
+    if (cudaFuncSetAttribute(k_score_adj<CB, RT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return AMVM_ERR_CUDA;
+    dev_ok[dev] = (int)smem;
+  }
   // back-to-back scorer launches overlap one grid's tail with the next one's
   // column stream (programmatic dependent launch; AMVM_SCORE_PDL=0 disables)
-  static const bool pdl = [] {
-    const char *e = getenv("AMVM_SCORE_PDL");
-    return !(e && atoi(e) == 0);
-  }();
+  const char *pe = getenv("AMVM_SCORE_PDL");
+  const bool pdl = !(pe && atoi(pe) == 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)G);
   cfg.blockDim = dim3(NC + 32);
