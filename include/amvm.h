@@ -77,7 +77,9 @@ typedef struct {
   int32_t one_opt_max_sweeps;   /* ONE_OPT_MAX_SWEEPS localsearch.py:20        */
   int32_t ls_max_rounds;        /* LOCAL_SEARCH_MAX_ROUNDS localsearch.py:21   */
   int32_t n_segment;            /* N_SEGMENT controller.py:30                  */
-  int32_t threads;       /* CTA size: 0 = auto (this build: 256 only)         */
+  int32_t threads;       /* CTA size: 0 = auto (512 threads, one CTA per SM,  *
+                          * when count <= SM count, else 256 x 2 per SM); 256  *
+                          * or 512 force one (component calls: 256 only)       */
 } amvm_params;
 
 /* numpy PCG64 bit generator state == Generator.bit_generator.state.        */

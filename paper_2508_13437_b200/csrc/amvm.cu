@@ -17,7 +17,7 @@ using namespace amvm;
 // Persistent solve: one CTA per resident slot, instances pulled from a
 // counter so uneven iteration counts balance across SMs.
 template <int NT, bool SP>
-__global__ void __launch_bounds__(NT, AMVM_MIN_BLOCKS) k_solve(KArgs a) {
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : AMVM_MIN_BLOCKS) k_solve(KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   Engine<NT, SP> E;
   E.bind(a, smem, blockIdx.x);
@@ -454,14 +454,14 @@ int64_t pow2ceil(int64_t v) {
 
 template <int NT>
 size_t smem_bytes(int64_t m, int64_t nlev, int cr_smem, int tab) {
-  size_t s = sizeof(Shared<NT>) + 8 * ((nlev + 1) & ~1) + scratch_bytes(nlev, tab);
+  size_t s = sizeof(Shared<NT>) + 8 * ((nlev + 1) & ~1) + scratch_bytes<NT>(nlev, tab);
   if (cr_smem) s += 8 * m;
   return s;
 }
 
 template <int NT>
 int occupancy(size_t smem, bool op, int *blocks, bool sp) {
-  auto fn = op ? k_op<NT> : (sp ? k_solve<NT, true> : k_solve<NT, false>);
+  auto fn = op ? k_op<AMVM_NT> : (sp ? k_solve<NT, true> : k_solve<NT, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return AMVM_ERR_CUDA;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, NT, smem);
@@ -469,14 +469,17 @@ int occupancy(size_t smem, bool op, int *blocks, bool sp) {
   return AMVM_OK;
 }
 
+// Two CTA sizes: 256 threads, 2 CTAs per SM (batches: more instances than
+// SMs), and 512 threads, one CTA per SM with all its registers (at most as
+// many instances as SMs: each instance's phases get twice the warps).
+constexpr int kNtWide = 512;
+
 size_t smem_for(int nt, int64_t m, int64_t nlev, int cr_smem, int tab) {
-  (void)nt;
-  return smem_bytes<AMVM_NT>(m, nlev, cr_smem, tab);
+  return nt == kNtWide ? smem_bytes<kNtWide>(m, nlev, cr_smem, tab) : smem_bytes<AMVM_NT>(m, nlev, cr_smem, tab);
 }
 
 int occupancy_for(int nt, size_t smem, bool op, int *blocks, bool sp = false) {
-  (void)nt;
-  return occupancy<AMVM_NT>(smem, op, blocks, sp);
+  return nt == kNtWide ? occupancy<kNtWide>(smem, op, blocks, sp) : occupancy<AMVM_NT>(smem, op, blocks, sp);
 }
 
 constexpr size_t kSmemMax = 220 * 1024;
@@ -494,9 +497,16 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, i
   if (prm->r < 1 || prm->r > p->n || prm->k_eps < 1 || prm->max_iters < 0 || prm->refresh_period < 1 ||
       prm->n_segment < 1)
     return AMVM_ERR_INVALID;
+  int sms = 0;
+  if (!op) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return AMVM_ERR_NO_DEVICE;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return AMVM_ERR_CUDA;
+  }
   int nt = prm->threads;
-  if (nt == 0) nt = AMVM_NT;
-  if (nt != AMVM_NT) return AMVM_ERR_UNSUPPORTED;  // this build instantiates one CTA size
+  if (nt == 0) nt = (!op && p->count <= sms) ? kNtWide : AMVM_NT;  // auto: a whole SM per instance when they fit
+  if (nt != AMVM_NT && nt != kNtWide) return AMVM_ERR_UNSUPPORTED;
+  if (op && nt != AMVM_NT) return AMVM_ERR_UNSUPPORTED;  // component calls: 256 threads
   P->nt = nt;
   P->tab = p->nlev <= kTabMaxLev;
 #ifndef AMVM_CR_SMEM_MAX
@@ -524,15 +534,27 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, i
     P->tab = 0;
     P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
   }
+  if (P->smem > kSmemMax && nt == kNtWide && prm->threads == 0) {  // the wide CTA does not fit: 256 threads
+    P->nt = nt = AMVM_NT;
+    P->tab = p->nlev <= kTabMaxLev;
+    P->cr_smem = p->m * 8 <= AMVM_CR_SMEM_MAX;
+    P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
+    if (P->smem > kSmemMax && P->cr_smem) {
+      P->cr_smem = 0;
+      P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
+    }
+    if (P->smem > kSmemMax && P->tab) {
+      P->tab = 0;
+      P->smem = smem_for(nt, p->m, p->nlev, P->cr_smem, P->tab);
+    }
+  }
   if (P->smem > kSmemMax) return AMVM_ERR_UNSUPPORTED;  // nlev too large for the smem level table
   const SlotLayout L = slot_layout(p->m, p->n, prm->k_eps, prm->r, cap, sparse ? ktop : 0);
   P->slot_bytes = al256(L.total);
   if (op) {
     P->slots = 1;
   } else {
-    int dev = 0, sms = 0, blocks = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return AMVM_ERR_NO_DEVICE;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return AMVM_ERR_CUDA;
+    int blocks = 0;
     int rc = occupancy_for(nt, P->smem, false, &blocks, sparse != 0);
     if (rc) return rc;
     if (blocks < 1) return AMVM_ERR_UNSUPPORTED;
@@ -608,6 +630,8 @@ int launch(const Plan &P, bool op, const KArgs &a, cudaStream_t st) {
   }
   const dim3 grid((unsigned)P.slots), block((unsigned)P.nt);
   if (op) k_op<AMVM_NT><<<grid, block, P.smem, st>>>(a);
+  else if (P.nt == kNtWide && a.sparse) k_solve<kNtWide, true><<<grid, block, P.smem, st>>>(a);
+  else if (P.nt == kNtWide) k_solve<kNtWide, false><<<grid, block, P.smem, st>>>(a);
   else if (a.sparse) k_solve<AMVM_NT, true><<<grid, block, P.smem, st>>>(a);
   else k_solve<AMVM_NT, false><<<grid, block, P.smem, st>>>(a);
   return cuda_rc(cudaGetLastError());

@@ -32,16 +32,17 @@ namespace amvm {
 #define AMVM_MIN_BLOCKS 2
 #endif
 constexpr int kS = 32;         // one_opt screening rows (exact rejection test), one per lane
-constexpr int kCW = 16;        // one_opt window: columns per warp (window = NW * kCW)
+// one_opt window: columns per warp; the window (NW * kCW columns) is a
+// 128-bit mask, so 16 columns per warp at 256 threads, 8 at 512
+template <int NT>
+constexpr int kCWv = 4096 / NT < 16 ? 4096 / NT : 16;
 constexpr int kB = 8;          // one_opt second screen: flagged columns per batch
 #ifndef AMVM_KG
 #define AMVM_KG 8
 #endif
 constexpr int kG = AMVM_KG;    // filter rows staged in smem per find_candidates
-#ifndef AMVM_TJ
-#define AMVM_TJ (2 * AMVM_NT)
-#endif
-constexpr int kTJ = AMVM_TJ;  // find_candidates j-tile (level-sorted positions)
+template <int NT>
+constexpr int kTJv = 2 * NT;  // find_candidates j-tile (level-sorted positions)
 #ifndef AMVM_ROW_PASSES
 #define AMVM_ROW_PASSES 24
 #endif
@@ -60,7 +61,7 @@ constexpr int kDrainShort = AMVM_DRAIN_SHORT;  // at or below: no row passes, wa
 constexpr int kRowPasses = AMVM_ROW_PASSES;  // queue passes (one filter row each) before fc_rest
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
 constexpr int kTabMaxLev = 16; // bound table in smem when nlev <= this
-constexpr int kTC = AMVM_NT;    // impact tile: columns (= CTA size: one column per thread)
+// impact tile: columns = CTA size (one column per thread)
 constexpr int kTK = 16;        // impact tile: rows
 constexpr int kTKMax = 128;    // narrow impact tile (n < NT): rows at most
 #ifndef AMVM_IMPACT_PREFETCH
@@ -82,7 +83,9 @@ constexpr int kIC1 = 1, kIR1 = 8, kIS1 = 3;
 // sort, which reuses everything after them), then the staged tiles.
 __host__ __device__ inline size_t fc_tb_off(int64_t nlev) { return ((size_t)8 * (nlev + 2) + 15) & ~(size_t)15; }
 
+template <int NT>
 __host__ __device__ inline size_t scratch_bytes(int64_t nlev, int tab) {
+  constexpr int kTJ = kTJv<NT>, kTC = NT;
   size_t fc = fc_tb_off(nlev) + 8 * kG * kTJ + 4 * 2 * kTJ;
   if (tab) fc += 8 * kG * nlev * nlev;
   size_t imp = 8 * kTC * (kTK + 1) + 16 * kTKMax;
@@ -367,7 +370,7 @@ struct Shared {
   int gnext;
   int qnext;
   int srow[kS];
-  int wk[2][NT / 32 * kCW];     // one_opt window: level index per column
+  int wk[2][NT / 32 * kCWv<NT>];  // one_opt window: level index per column
   unsigned sflag[2][NT / 32];   // one_opt window: first-screen survivors per warp
   int wsum[2][NT / 32];         // one_opt window: valid candidates per warp
   unsigned rejw[2][2][NT / 32]; // one_opt batch: second-screen rejections per warp
@@ -400,6 +403,7 @@ __device__ __forceinline__ uint64_t abs_key(double x) { return (uint64_t)__doubl
 template <int NT, bool SP = false>
 struct Engine {
   static constexpr int NW = NT / 32;
+  static constexpr int kCW = kCWv<NT>, kTJ = kTJv<NT>, kTC = NT;
   Shared<NT> *sh;
   int tid, lane, warp;
   // replicated block-uniform scalars: every thread evolves identical copies
@@ -1100,7 +1104,7 @@ struct Engine {
     uint64_t T = 0;
     int64_t need = 0;
     // (the find_candidates scratch is free until the buckets are built)
-    if (kk < m) radix_kth(kk, T, need, (uint64_t *)scr, (int)(scratch_bytes(nlev, tab) / 8));
+    if (kk < m) radix_kth(kk, T, need, (uint64_t *)scr, (int)(scratch_bytes<NT>(nlev, tab) / 8));
     // keys strictly above T (all rows when kk >= m), unordered
     for (int64_t i = tid; i < m; i += NT) {
       uint64_t key = abs_key(cr[i]);
@@ -1781,7 +1785,7 @@ struct Engine {
     } else if (!pairs) {  // (the lane-per-pair enumeration needs no order inside a bucket)
       int64_t n2 = 1;
       while (n2 < n) n2 <<= 1;
-      if (n2 <= 65536 && nlev <= 32768 && fc_tb_off(nlev) + (size_t)12 * n2 <= scratch_bytes(nlev, tab)) {
+      if (n2 <= 65536 && nlev <= 32768 && fc_tb_off(nlev) + (size_t)12 * n2 <= scratch_bytes<NT>(nlev, tab)) {
         // in shared memory (after the bucket bounds): key (level << 16 | j)
         // + b0, one compare-exchange pair per thread per step
         double *sb = (double *)(scr + fc_tb_off(nlev));
@@ -2657,7 +2661,7 @@ struct Engine {
       }
       // p = d / total, also into the (idle) phase scratch when it fits, so
       // the sequential cumsum below reads shared memory
-      double *const ps = (size_t)n * 8 <= scratch_bytes(nlev, tab) ? (double *)scr : pbuf;
+      double *const ps = (size_t)n * 8 <= scratch_bytes<NT>(nlev, tab) ? (double *)scr : pbuf;
       for (int64_t k = tid; k < n; k += NT) {
         const double v = ddiv(dbuf[k], total);
         pbuf[k] = v;
@@ -2910,7 +2914,7 @@ struct Engine {
       c.off_lv = (uint32_t)o;
       o += 8 * ((a.nlev + 1) & ~1);
       c.off_scr = (uint32_t)o;
-      o += scratch_bytes(a.nlev, a.tab);
+      o += scratch_bytes<NT>(a.nlev, a.tab);
       c.cr = a.cr_smem ? (double *)(amvm_dyn_smem + o) : (double *)(base + L.crg);
       // leaf trees of numpy's pairwise sum for lengths m and n
       c.nleaf_m = pw_leaves(a.m, c.lf_lo, c.lf_len, (int)L.nleaf, sh->pw_a, sh->pw_b);

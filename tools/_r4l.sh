@@ -1,5 +1,5 @@
 #!/bin/bash
-# worst-remove sampling: lane-0 DADD chain from smem, block-parallel setdiff
+# dual CTA size (512 x 1 for count <= SMs)
 OUT=${OUT:-r4l}; mkdir -p gpurun_out/$OUT
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/$OUT/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/$OUT/pytest.log
 tail -2 gpurun_out/$OUT/pytest.log
