@@ -57,8 +57,6 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttr", action="store_true", help="skip the wall-time-to-reference-l_inf leg")
     ap.add_argument("--no-legs", action="store_true", help="skip the C4-layer and C3-slices legs")
-    ap.add_argument("--c3-full", action="store_true",
-                    help="add the full-size (256^2 x 180) C3 leg: 148 slices x 2 iterations, sparse engine (~200 s)")
     return ap.parse_args()
 
 
@@ -612,9 +610,7 @@ def run_amvm(args, rank, world):
         line["roofline"] = sc.pop("roofline")
         line["scorer"] = sc
         if not args.no_legs:
-            line["workloads"] = {"c4_layer": c4_leg(dev), "c3_slices": c3_leg(dev)}
-            if args.c3_full:  # ~200 s of device time: opt-in
-                line["workloads"]["c3_full"] = c3_full_leg(dev)
+            line["workloads"] = {"c4_layer": c4_leg(dev), "c3_slices": c3_leg(dev), "c3_full": c3_full_leg(dev)}
     print(json.dumps(line), flush=True)
     if not par["bitwise"]:
         print(f"PARITY FAILURE: {par['mismatches']}", file=sys.stderr)
@@ -692,9 +688,9 @@ def c3_leg(dev, side: int = 128, n_angles: int = 64, slices: int = 148, iters: i
     """BASELINE configs[2] family: discrete tomography slices (3 grey levels,
     squares/disk/checker phantoms, eta = 5% of the max row sum, 100 SIRT
     iterations) sharing one parallel-beam projector, at 128^2 x 64 angles
-    (m=8192, n=16384; the full 256^2 x 180 slice needs the dense engine's
-    48 GB), `slices` slices x `iters` iterations in one
-    batched solve.  Slice 0 (seed 0, squares) is the reference's own C3m
+    (m=8192, n=16384), `slices` slices x `iters` iterations in one batched
+    solve on the sparse engine (A as CSC + CSR; the dense engine's time is
+    reported beside it).  Slice 0 (seed 0, squares) is the reference's own C3m
     instance: bitwise parity with its golden.  CPU: the port on the 64^2 x 45
     reference instance (C3s golden), 1 core."""
     import torch
@@ -715,23 +711,33 @@ def c3_leg(dev, side: int = 128, n_angles: int = 64, slices: int = 148, iters: i
     t0 = time.perf_counter()
     fe = tomo.build_tomo_device(side, (0.0, 1.0, 2.0), n_angles, eta, seeds=tuple(range(slices)),
                                 phantom_kinds=kinds, sirt_iters=100, device=dev)
-    sb = tomo.SliceBatch(A, fe["B"].cpu().numpy(), fe["levels"], fe["idx0"].cpu().numpy(), device=dev)
+    de = tomo.SliceBatch(A, fe["B"].cpu().numpy(), fe["levels"], fe["idx0"].cpu().numpy(), device=dev)
     del A
+    sb = tomo.SparseSliceBatch(fe["csr"], m, n, fe["B"], fe["levels"], fe["idx0"], device=dev)
     torch.cuda.synchronize()
     fe_s = time.perf_counter() - t0
     cfg = SolverConfig(max_iters=iters)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    o = sb.solve(cfg, seeds=np.arange(slices))
-    b.record()
-    torch.cuda.synchronize()
-    sb.check_status()
-    ms = a.elapsed_time(b)
+
+    def timed(batch):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = batch.solve(cfg, seeds=np.arange(slices))
+        b.record()
+        torch.cuda.synchronize()
+        batch.check_status()
+        return out, a.elapsed_time(b)
+
+    o, ms = timed(sb)
+    od, ms_dense = timed(de)
+    del de
+    same = all(np.array_equal(o[k].cpu().numpy(), od[k].cpu().numpy())
+               for k in ("iterations", "best_objective", "best_idx", "moves_scored"))
     mv = o["moves_scored"].sum(dim=0).cpu().numpy()
     rec = load("solve_c3m")[0]
     par = {"slice": 0, "bitwise": bool(
         int(o["iterations"][0]) == int(rec["iterations"]) and float(o["best_objective"][0]) == rec["best_objective"]
-        and np.array_equal(o["best_idx"][0].cpu().numpy(), rec["best_idx"]))}
+        and np.array_equal(o["best_idx"][0].cpu().numpy(), rec["best_idx"])) and same,
+        "sparse_equals_dense_all_slices": bool(same)}
     from oracle import oracle as O
     r3 = load("solve_c3s")[0]
     A3 = stored_A(r3)
@@ -743,6 +749,8 @@ def c3_leg(dev, side: int = 128, n_angles: int = 64, slices: int = 148, iters: i
             "config": f"C3 family: {slices} tomography slices {side}^2 x {n_angles} angles (m={m}, n={n}, "
                       f"3 grey levels) sharing one projector, {iters} ALNS iterations each, one GPU",
             "device_ms": round(ms, 2), "moves_scored_per_s": float(mv[0]) / (ms / 1e3),
+            "engine": "sparse (amvm_solve_sparse, column-indexed candidate filter)",
+            "dense_engine": {"device_ms": round(ms_dense, 2), "value": slices * iters / (ms_dense / 1e3)},
             "front_end_s": round(fe_s, 2), "parity": par,
             "seeds": "slice k: phantom kinds[k % 3], noise seed k, ALNS seed k (slice 0 = the reference's C3m run)",
             "cpu_baseline": {"value": 1.0 / cdt, "unit": "slice-iterations/s", "cores": 1, "kind": "port",

@@ -150,6 +150,8 @@ typedef struct {
   const int64_t *rptr; const int32_t *rcol; const double *rval;  /* CSR, m + 1 / nnz / nnz */
   const double *B;      /* count x m targets b                                    */
   const double *levels; /* count x nlev                                           */
+  int64_t max_row_nnz;  /* largest row nonzero count; > 0 enables the column-     *
+                         * indexed candidate filter (0: the general filter)       */
 } amvm_sparse_problem;
 
 AMVM_API size_t amvm_sparse_workspace_bytes(const amvm_sparse_problem *prob, const amvm_params *prm);

@@ -47,7 +47,8 @@ class SparseProblem(C.Structure):
                 ("nnz", C.c_int64), ("max_col_nnz", C.c_int64),
                 ("cptr", C.c_void_p), ("crow", C.c_void_p), ("cval", C.c_void_p),
                 ("rptr", C.c_void_p), ("rcol", C.c_void_p), ("rval", C.c_void_p),
-                ("B", C.c_void_p), ("levels", C.c_void_p)]
+                ("B", C.c_void_p), ("levels", C.c_void_p),
+                ("max_row_nnz", C.c_int64)]  # > 0: the column-indexed candidate filter
 
 
 class Params(C.Structure):

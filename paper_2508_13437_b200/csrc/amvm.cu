@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "amvm_engine.cuh"
@@ -442,6 +443,7 @@ struct Plan {
   size_t ist_bytes;  // per parked instance (chunked solve), 0 otherwise
   size_t icache_bytes;  // per instance impact-score cache (solve), 0 for ops
   int sparse, ktop;     // sparse engine (amvm_solve_sparse)
+  int64_t fecap;        // sparse engine: column-indexed filter list capacity (0: off)
   int chunk_iters;
   size_t ws_bytes;
 };
@@ -488,10 +490,14 @@ constexpr size_t kSmemMax = 220 * 1024;
 #endif
 constexpr int kChunkIters = AMVM_CHUNK_ITERS;  // chunked solve: ALNS iterations per task
 
-int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, int sparse = 0, int ktop = 0) {
+int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, int sparse = 0, int ktop = 0,
+              int64_t max_row_nnz = 0) {
   if (!p || !prm) return AMVM_ERR_INVALID;
   P->sparse = sparse;
   P->ktop = ktop;
+  // the filter rows' nonzeros, indexed by column (k_eps rows at most)
+  P->fecap = (sparse && max_row_nnz > 0) ? std::min<int64_t>(prm->k_eps, p->m) * max_row_nnz : 0;
+  if (P->fecap > ((int64_t)1 << 24)) P->fecap = 0;  // too many to index per slot: the general filter
   if (p->m < 1 || p->n < 1 || p->nlev < 1 || p->count < 1) return AMVM_ERR_INVALID;
   if (p->n > 0x7fffffff || p->m > 0x7fffffff) return AMVM_ERR_UNSUPPORTED;
   if (prm->r < 1 || prm->r > p->n || prm->k_eps < 1 || prm->max_iters < 0 || prm->refresh_period < 1 ||
@@ -522,6 +528,14 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, i
   const int64_t all_pairs = n * (n - 1) / 2;
   int64_t cap = maxc > 0 ? std::max<int64_t>(std::max<int64_t>(2 * maxc, maxc + n), 1024) : std::max<int64_t>(all_pairs, 1024);
   if (p->count <= 16) cap = std::max<int64_t>(cap, std::min<int64_t>(all_pairs, (int64_t)1 << 22));
+  // sparse rows (tomography) let tens of thousands of pairs through the
+  // filter: room for them, so a call sorts its survivors once instead of
+  // taking the counting-pass overflow path (~20 enumerations)
+  if (sparse) cap = std::max<int64_t>(cap, std::min<int64_t>(all_pairs, (int64_t)1 << 17));
+  if (sparse && getenv("AMVM_SPARSE_CAP")) {  // test knob: a small buffer drives the overflow path
+    const int64_t want = std::max<int64_t>(atoll(getenv("AMVM_SPARSE_CAP")), maxc + n);
+    cap = std::max<int64_t>(want, 1024);
+  }
   cap = pow2ceil(cap);
   if (cap > ((int64_t)1 << 30)) return AMVM_ERR_UNSUPPORTED;
   P->cap = (int)cap;
@@ -549,7 +563,7 @@ int make_plan(const amvm_problem *p, const amvm_params *prm, bool op, Plan *P, i
     }
   }
   if (P->smem > kSmemMax) return AMVM_ERR_UNSUPPORTED;  // nlev too large for the smem level table
-  const SlotLayout L = slot_layout(p->m, p->n, prm->k_eps, prm->r, cap, sparse ? ktop : 0);
+  const SlotLayout L = slot_layout(p->m, p->n, prm->k_eps, prm->r, cap, sparse ? ktop : 0, P->fecap);
   P->slot_bytes = al256(L.total);
   if (op) {
     P->slots = 1;
@@ -585,6 +599,7 @@ KArgs base_args(const amvm_problem *p, const amvm_params *prm, const Plan &P, vo
   a.ist_bytes = P.ist_bytes;
   a.sparse = P.sparse;
   a.ktop = P.ktop;
+  a.fecap = P.fecap;
   if (!P.sparse) {  // the dense part: row-major Ar and the CSC copy (sparse: the caller's CSC / CSR)
     a.Ar = (const double *)(a.ws + sizeof(WsHeader));
     unsigned char *cb = a.ws + sizeof(WsHeader) + ws_ar_bytes(p->m, p->n);
@@ -713,7 +728,8 @@ static int sparse_plan(const amvm_sparse_problem *sp, const amvm_params *prm, bo
   if (ktop < 32) ktop = 32;
   if (ktop > sp->m) ktop = sp->m;
   if (ktop > 4096) return AMVM_ERR_UNSUPPORTED;  // rank-sorted on one CTA
-  return make_plan(dense_view, prm, op, P, 1, (int)ktop);
+  if (sp->max_row_nnz < 0) return AMVM_ERR_INVALID;
+  return make_plan(dense_view, prm, op, P, 1, (int)ktop, sp->max_row_nnz);
 }
 
 size_t amvm_sparse_workspace_bytes(const amvm_sparse_problem *sp, const amvm_params *prm) {

@@ -155,6 +155,7 @@ struct KArgs {
   const int64_t *rptr;
   const int32_t *rcol;
   const double *rval;
+  int64_t fecap;  // column-indexed filter lists: entry capacity (0: off)
 };
 
 enum { OP_ONE_OPT = 1, OP_LOCAL_SEARCH, OP_FIND_CAND, OP_BEST_SWAP, OP_IMPACT, OP_DESTROY, OP_REPAIR,
@@ -218,9 +219,16 @@ __host__ __device__ inline InstLayout inst_layout(int64_t m, int64_t n) {
 }
 
 // Per-slot workspace carve-up (shared by host sizing and device use).
+// Column-indexed filter list entry (sparse engine): filter row q touches the
+// column with folded value b; next = the column's next entry (-1: end).
+struct FEnt {
+  int32_t q, next;
+  double b;
+};
+
 struct SlotLayout {
   size_t ur, crg, uidx, cidx, dbuf, pbuf, cbk, lf_lo, lf_len, lf_sum, rows, reps, rsgn, ag, cbuf, que,
-      hset, rem, sav, pick, coin, ibuf, srt, rowtmp, top, total;
+      hset, rem, sav, pick, coin, ibuf, srt, rowtmp, top, fhead, fent, total;
   int64_t nleaf, kk, hsz;
 };
 
@@ -236,7 +244,7 @@ __host__ __device__ inline uint64_t gen_mask(uint64_t v) {
 }
 
 __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t k_eps, int64_t r, int64_t cap,
-                                                   int64_t ktop = 0) {
+                                                   int64_t ktop = 0, int64_t fecap = 0) {
   SlotLayout L;
   int64_t mn = m > n ? m : n;
   L.nleaf = mn / 64 + 4;
@@ -275,6 +283,9 @@ __host__ __device__ inline SlotLayout slot_layout(int64_t m, int64_t n, int64_t 
   // sparse engine: one dense row scratch (kept zero between uses), |s| top list
   L.rowtmp = o; o = al256(o + (ktop > 0 ? 8 * n : 0));
   L.top = o; o = al256(o + 4 * ktop);
+  // column-indexed filter: per-column list heads (kept -1 between uses), entries
+  L.fhead = o; o = al256(o + (fecap > 0 ? 4 * n : 0));
+  L.fent = o; o = al256(o + sizeof(FEnt) * fecap);
   L.total = o;
   return L;
 }
@@ -295,6 +306,9 @@ struct Ctx {
   const double *rval;
   double *rowtmp;             // n doubles, zero between uses
   int32_t *top;               // ktop rows by (|s| desc, index asc)
+  int32_t *fhead;             // column-indexed filter: list head per column (-1 between uses)
+  FEnt *fent;                 // ... entries
+  int64_t fecap;              // ... capacity (0: off)
   double *cr, *ur;
   int32_t *cidx, *uidx;
   double *dbuf, *pbuf, *cbk;
@@ -1669,6 +1683,239 @@ struct Engine {
     __syncthreads();
   }
 
+  // Sparse engine, column-indexed filter (SP, lists configured): the same
+  // survivor set as the staged-row enumeration, for sparse filter rows.
+  //   * row 0 is the argmax row (eps_0 = 0, bound +0): a pair survives it iff
+  //     b0_j < b0_i (folded values; exact: a difference of two doubles is < 0
+  //     iff the first is smaller), so every survivor has b0_i > 0 or b0_j < 0:
+  //     the pairs are enumerated from row 0's nonzeros (b0_i > 0: i fixed, all
+  //     j; b0_i <= 0 then needs b0_j < b0_i <= 0: j fixed with b0_j < 0, all i
+  //     with b0_j < b0_i <= 0) -- a disjoint cover of the row-0 survivors;
+  //   * a row q >= 1 whose bound is positive at the largest level difference
+  //     passes every pair it touches in neither column (da = 0 < bound), so
+  //     each pair is tested only on the rows in its two columns' lists (the
+  //     filter rows' nonzeros indexed by column), with the reference's
+  //     arithmetic (dsub of the folded values, ddiv(eps, delta)).
+  // fc_sparse_build: checks the preconditions and builds the lists (false:
+  // the general filter runs); fc_sparse_enum<MODE> is one enumeration (FC_ALL
+  // collects, FC_COUNT counts and FC_CUT collects the survivors up to (fD, fI)
+  // in the reference order, FC_HIST counts the survivors with delta == fD per
+  // i into ibuf and those with delta > fD); fc_sparse_reset restores the
+  // resting state (heads -1, row scratch zero).
+  enum { FC_HIST = 3 };
+  __device__ bool fc_sparse_build(int nr) {
+    AMVM_LOCALS
+    const int32_t *rw = sh->c.rcol;
+    const double *rv = sh->c.rval;
+    const int64_t *rp = sh->c.rptr;
+    int32_t *fh = sh->c.fhead;
+    FEnt *fe = sh->c.fent;
+    double *rt = sh->c.rowtmp;
+    if (tid == 0) {
+      const double dmax = dsub(lv[nlev - 1], lv[0]);
+      bool ok = nr >= 1 && reps[0] == 0.0 && dmax > 0.0;
+      int64_t ent = 0;
+      for (int q = 1; q < nr && ok; ++q) {
+        ok = ddiv(reps[q], dmax) > 0.0;
+        ent += __ldg(rp + rows[q] + 1) - __ldg(rp + rows[q]);
+      }
+      sh->bc_i[6] = ok && ent <= sh->c.fecap;
+      sh->bc_i[7] = 0;
+    }
+    __syncthreads();
+    if (!sh->bc_i[6]) return false;
+    // lists: the nonzeros of filter rows 1.. by column (unordered: AND is order-free)
+    for (int q = 1 + warp; q < nr; q += NW) {
+      const int64_t r = rows[q], e0 = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+      const bool pos = rsgn[q] != 0;
+      for (int64_t e = e0 + lane; e < e1; e += 32) {
+        const int32_t c = __ldg(rw + e);
+        const double a = __ldg(rv + e);
+        const int slot = atomicAdd(&sh->bc_i[7], 1);
+        fe[slot].q = q;
+        fe[slot].b = pos ? a : -a;
+        fe[slot].next = atomicExch(&fh[c], slot);
+      }
+    }
+    // row 0, folded, densely in the (zero) row scratch
+    const int64_t r0 = rows[0], z0 = __ldg(rp + r0), z1 = __ldg(rp + r0 + 1);
+    const bool pos0 = rsgn[0] != 0;
+    for (int64_t e = z0 + tid; e < z1; e += NT) {
+      const double a = __ldg(rv + e);
+      rt[__ldg(rw + e)] = pos0 ? a : -a;
+    }
+    __syncthreads();
+    return true;
+  }
+
+  __device__ void fc_sparse_reset(int nr) {
+    AMVM_LOCALS
+    const int32_t *rw = sh->c.rcol;
+    const int64_t *rp = sh->c.rptr;
+    __syncthreads();
+    for (int q = 1 + warp; q < nr; q += NW) {
+      const int64_t r = rows[q], e0 = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+      for (int64_t e = e0 + lane; e < e1; e += 32) sh->c.fhead[__ldg(rw + e)] = -1;
+    }
+    const int64_t r0 = rows[0], z0 = __ldg(rp + r0), z1 = __ldg(rp + r0 + 1);
+    for (int64_t e = z0 + tid; e < z1; e += NT) sh->c.rowtmp[__ldg(rw + e)] = 0.0;
+    __syncthreads();
+  }
+
+  template <int MODE>
+  __device__ int fc_sparse_enum(double fD, int64_t fI) {
+    AMVM_LOCALS
+    const int32_t *rw = sh->c.rcol;
+    const int64_t *rp = sh->c.rptr;
+    const int32_t *fh = sh->c.fhead;
+    const FEnt *fe = sh->c.fent;
+    const double *rt = sh->c.rowtmp;
+    if (tid == 0) sh->counter = 0;
+    __syncthreads();
+    const int64_t r0 = rows[0], z0 = __ldg(rp + r0), z1 = __ldg(rp + r0 + 1);
+    const int64_t s0 = z1 - z0, nch = (n + 31) / 32;
+    for (int64_t it = warp; it < s0 * nch; it += NW) {
+      const int64_t k = it / nch;
+      const int32_t c = __ldg(rw + z0 + k);
+      const double bc = rt[c];
+      const int64_t x = (it - k * nch) * 32 + lane;
+      // bc > 0: (i, j) = (c, x) with b0_x < bc;  bc < 0: (i, j) = (x, c) with bc < b0_x <= 0
+      bool alive = false;
+      int32_t i = 0, j = 0;
+      if (x < n && bc != 0.0) {
+        const double bx = rt[x];
+        if (bc > 0.0) {
+          i = c; j = (int32_t)x;
+          alive = bx < bc && cidx[j] < cidx[i];
+        } else {
+          i = (int32_t)x; j = c;
+          alive = bc < bx && bx <= 0.0 && cidx[i] > cidx[j];
+        }
+      }
+      double delta = 0.0;
+      if (alive) {
+        delta = dsub(lv[cidx[i]], lv[cidx[j]]);
+        if (MODE == FC_COUNT || MODE == FC_CUT) alive = delta > fD || (delta == fD && (int64_t)i <= fI);
+        if (MODE == FC_HIST) alive = delta >= fD;
+      }
+      if (alive) {
+        // rows touching i (b_q(j) from j's list, 0 if absent)
+        for (int32_t e = fh[i]; e >= 0 && alive; e = fe[e].next) {
+          const int q = fe[e].q;
+          double bj = 0.0;
+          for (int32_t f = fh[j]; f >= 0; f = fe[f].next)
+            if (fe[f].q == q) { bj = fe[f].b; break; }
+          alive = dsub(bj, fe[e].b) < ddiv(reps[q], delta);
+        }
+        // rows touching j only (b_q(i) = 0)
+        for (int32_t f = fh[j]; f >= 0 && alive; f = fe[f].next) {
+          const int q = fe[f].q;
+          bool in_i = false;
+          for (int32_t e = fh[i]; e >= 0; e = fe[e].next)
+            if (fe[e].q == q) { in_i = true; break; }
+          if (!in_i) alive = dsub(fe[f].b, 0.0) < ddiv(reps[q], delta);
+        }
+      }
+      if (MODE == FC_HIST) {
+        if (alive && delta == fD) atomicAdd(&ibuf[i], 1);
+        alive = alive && delta > fD;
+      }
+      const unsigned bal = __ballot_sync(AMVM_FULL, alive);
+      if (bal) {
+        int bse = 0;
+        if (lane == 0) bse = atomicAdd(&sh->counter, __popc(bal));
+        if (MODE == FC_ALL || MODE == FC_CUT) {
+          bse = __shfl_sync(AMVM_FULL, bse, 0);
+          const int pos = bse + __popc(bal & ((1u << lane) - 1u));
+          if (alive && pos < cap) cbuf[pos] = Cand{i, j, delta};
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = sh->counter;
+    __syncthreads();
+    return cnt;
+  }
+
+  // The whole sparse filter; -1: preconditions not met (general filter).
+  // More survivors than the buffer: the max_candidates-th survivor of the
+  // reference order (-delta, i, j) is found as in fc_overflow -- binary
+  // search over the level differences by counting passes, then ONE pass
+  // counting that class's survivors per i (a scan finds the cut i) -- and
+  // only the survivors up to it are collected.
+  __device__ int fc_sparse(int nr) {
+    AMVM_LOCALS
+    if (!fc_sparse_build(nr)) return -1;
+    int cnt = fc_sparse_enum<FC_ALL>(0.0, 0);
+    const int maxc = prm->max_candidates;
+    if (cnt > cap && maxc > 0) {
+      double *dcl = dbuf;  // idle during find_candidates
+      if (tid == 0) {  // distinct level differences, descending (all level pairs: a superset is harmless)
+        int nd = 0, bad = 0;
+        for (int ki = 1; ki < nlev && !bad; ++ki)
+          for (int kj = 0; kj < ki && !bad; ++kj) {
+            const double d = dsub(lv[ki], lv[kj]);
+            int at = 0;
+            while (at < nd && dcl[at] > d) ++at;
+            if (at < nd && dcl[at] == d) continue;
+            if (nd == kMaxDeltaClasses || nd >= n) { bad = 1; break; }
+            for (int q = nd; q > at; --q) dcl[q] = dcl[q - 1];
+            dcl[at] = d;
+            ++nd;
+          }
+        sh->bc_i[4] = bad ? -1 : nd;
+      }
+      __syncthreads();
+      const int nd = sh->bc_i[4];
+      __syncthreads();
+      if (nd <= 0) {
+        fc_sparse_reset(nr);
+        return -1;
+      }
+      int lo = 0, hi = nd - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (fc_sparse_enum<FC_COUNT>(dcl[mid], INT64_MAX) >= maxc) hi = mid;
+        else lo = mid + 1;
+      }
+      const double dc = dcl[lo];
+      for (int64_t k = tid; k < n; k += NT) ibuf[k] = 0;
+      __syncthreads();
+      const int above = fc_sparse_enum<FC_HIST>(dc, 0);  // survivors with delta > dc; ibuf: per i at dc
+      // the smallest i* with above + #{delta == dc, i <= i*} >= maxc (warp 0 scans)
+      if (warp == 0) {
+        int64_t acc = above, istar = n - 1;
+        bool found = false;
+        for (int64_t k0 = 0; k0 < n && !found; k0 += 32) {
+          const int64_t k = k0 + lane;
+          const int v = k < n ? ibuf[k] : 0;
+          int incl = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(AMVM_FULL, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const unsigned hit = __ballot_sync(AMVM_FULL, k < n && acc + incl >= maxc);
+          if (hit) {
+            istar = k0 + __ffs(hit) - 1;
+            found = true;
+          }
+          acc += __shfl_sync(AMVM_FULL, incl, 31);
+        }
+        if (lane == 0) sh->bc_d[2] = (double)istar;
+      }
+      __syncthreads();
+      const int64_t istar = (int64_t)sh->bc_d[2];
+      cnt = fc_sparse_enum<FC_CUT>(dc, istar);
+    }
+    fc_sparse_reset(nr);
+    if (cnt > cap) {  // no max_candidates and more survivors than the buffer
+      fail(AMVM_ERR_UNSUPPORTED);
+      cnt = (int)cap;
+    }
+    return cnt;
+  }
+
   __device__ int find_candidates(bool always_sort) {
     AMVM_LOCALS
 #ifdef AMVM_FC_PROFILE  // diagnostic: sub-phase cycles in pc[8..13]
@@ -1679,6 +1926,19 @@ struct Engine {
 #endif
     const int nr = select_rows();
     FC_PROF(0);
+    if constexpr (SP) {
+      if (sh->c.fecap > 0) {
+        int cnt = fc_sparse(nr);
+        if (cnt >= 0) {
+          const int maxc = prm->max_candidates;
+          if ((maxc > 0 && cnt > maxc) || (always_sort && cnt > 1)) {
+            sort_cands(cnt);
+            if (maxc > 0 && cnt > maxc) cnt = maxc;
+          }
+          return cnt;
+        }
+      }
+    }
     const int g = nr < kG ? nr : kG;
     int32_t *lst = (int32_t *)scr;
     int32_t *lfl = lst + (nlev + 1);
@@ -2880,8 +3140,14 @@ struct Engine {
       c.prm = a.prm;
       c.cap = a.cap;
       c.tab = a.tab;
-      const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap, a.sparse ? a.ktop : 0);
+      const SlotLayout L = slot_layout(a.m, a.n, a.prm.k_eps, a.prm.r, a.cap, a.sparse ? a.ktop : 0,
+                                       a.sparse ? a.fecap : 0);
       c.kk = L.kk;
+      c.fecap = a.sparse ? a.fecap : 0;
+      c.fhead = (int32_t *)(a.ws + sizeof(WsHeader) + ws_dense_bytes(a.m, a.n, a.sparse) +
+                            (size_t)slot * a.slot_bytes + L.fhead);
+      c.fent = (FEnt *)(a.ws + sizeof(WsHeader) + ws_dense_bytes(a.m, a.n, a.sparse) +
+                        (size_t)slot * a.slot_bytes + L.fent);
       unsigned char *base = a.ws + sizeof(WsHeader) + ws_dense_bytes(a.m, a.n, a.sparse) +
                             (size_t)slot * a.slot_bytes;
       c.rowtmp = (double *)(base + L.rowtmp);
@@ -2926,6 +3192,8 @@ struct Engine {
     __syncthreads();
     if constexpr (SP) {  // the row scratch starts (and stays) zero; the workspace is not cleared by the host
       for (int64_t j = tid; j < a.n; j += NT) sh->c.rowtmp[j] = 0.0;
+      if (sh->c.fecap > 0)  // (list heads likewise start and stay -1)
+        for (int64_t j = tid; j < a.n; j += NT) sh->c.fhead[j] = -1;
       __syncthreads();
     }
   }

@@ -182,7 +182,7 @@ class SparseSliceBatch:
     slices x m, idx0 slices x n (host or device).  The start residual
     A x0 - b is computed on the device in numpy's dense dgemv order."""
 
-    def __init__(self, csr, m: int, n: int, B, levels, idx0, device=None):
+    def __init__(self, csr, m: int, n: int, B, levels, idx0, device=None, column_filter: bool = True):
         from . import _native as N
 
         torch = N.torch_cuda()
@@ -213,6 +213,9 @@ class SparseSliceBatch:
         self.cptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
         self.cptr[1:] = torch.cumsum(counts, 0)
         self.max_col_nnz = int(counts.max().item()) if n else 0
+        # column_filter: the candidate filter indexes the filter rows' nonzeros
+        # by column (same survivors; False runs the general staged-row filter)
+        self.max_row_nnz = int((indptr[1:] - indptr[:-1]).max().item()) if m and column_filter else 0
         self.B = B
         self.L = torch.from_numpy(np.tile(levels, (self.count, 1))).to(dev)
         self.idx0 = idx0
@@ -229,7 +232,7 @@ class SparseSliceBatch:
         return N.SparseProblem(self.m, self.n, self.nlev, self.count, self.nnz, self.max_col_nnz,
                                self.cptr.data_ptr(), self.crow.data_ptr(), self.cval.data_ptr(),
                                self.rptr.data_ptr(), self.rcol.data_ptr(), self.rval.data_ptr(),
-                               self.B.data_ptr(), self.L.data_ptr())
+                               self.B.data_ptr(), self.L.data_ptr(), self.max_row_nnz)
 
     def workspace_bytes(self, cfg=None) -> int:
         from . import _native as N

@@ -111,3 +111,54 @@ def test_sparse_workspace_is_small(tomo):
     sb = tomo.SparseSliceBatch(csr, m, n, np.zeros((1, m)), (0.0, 1.0, 2.0), np.zeros((1, n), np.int32))
     ws = sb.workspace_bytes(SolverConfig(max_iters=2))
     assert 0 < ws < 2 * 8 * m * n / 8, ws
+
+
+@pytest.mark.parametrize("side,n_angles,slices,iters", [(24, 16, 8, 12), (64, 45, 6, 4)])
+def test_column_indexed_filter_equals_general_filter(tomo, side, n_angles, slices, iters):
+    """The sparse engine's column-indexed candidate filter (filter rows'
+    nonzeros indexed by column, pairs enumerated from the argmax row) keeps
+    exactly the general staged-row filter's survivors: whole trajectories
+    and candidate counts bitwise, with and without max_candidates truncation."""
+    from paper_2508_13437_b200 import SolverConfig
+
+    lv = (0.0, 1.0, 2.0)
+    fe = tomo.build_tomo_device(side, lv, n_angles, 0.2, seeds=tuple(range(slices)),
+                                phantom_kinds=("squares", "disk", "checker"), sirt_iters=20)
+    m, n = fe["m"], fe["n"]
+    for maxc in (5000, 64):
+        cfg = SolverConfig(max_iters=iters, destroy_rate=0.02, max_candidates=maxc)
+        outs = []
+        for col in (True, False):
+            sb = tomo.SparseSliceBatch(fe["csr"], m, n, fe["B"], fe["levels"], fe["idx0"], column_filter=col)
+            assert (sb.max_row_nnz > 0) == col
+            outs.append(sb.solve(cfg, seeds=np.arange(slices), trace=True))
+            sb.check_status()
+        for key in ("iterations", "best_objective", "best_idx", "trace_current_t", "trace_best_t", "trace_pair",
+                    "trace_accepted", "moves_scored", "operator_uses"):
+            np.testing.assert_array_equal(outs[0][key].cpu().numpy(), outs[1][key].cpu().numpy(),
+                                          err_msg=f"{key} (max_candidates={maxc})")
+
+
+@pytest.mark.parametrize("side,n_angles", [(16, 48), (32, 32)])
+def test_column_indexed_filter_overflow_path(tomo, monkeypatch, side, n_angles):
+    """More filter survivors than the candidate buffer (AMVM_SPARSE_CAP
+    shrinks it): the column-indexed filter finds the max_candidates cut by
+    counting passes and a per-i histogram and keeps exactly the general
+    filter's truncated list."""
+    from paper_2508_13437_b200 import SolverConfig
+
+    lv = (0.0, 1.0, 2.0)
+    fe = tomo.build_tomo_device(side, lv, n_angles, 0.2, seeds=tuple(range(20)),
+                                phantom_kinds=("squares", "disk", "checker"), sirt_iters=20)
+    m, n = fe["m"], fe["n"]
+    cfg = SolverConfig(max_iters=6, destroy_rate=0.02, max_candidates=16)
+    monkeypatch.setenv("AMVM_SPARSE_CAP", "1024")
+    outs = []
+    for col in (True, False):
+        sb = tomo.SparseSliceBatch(fe["csr"], m, n, fe["B"], fe["levels"], fe["idx0"], column_filter=col)
+        outs.append(sb.solve(cfg, seeds=np.arange(20), trace=True))
+        sb.check_status()
+    assert int(outs[0]["phase_cycles"][:, 9].sum()) > 0  # candidates were found
+    for key in ("iterations", "best_objective", "best_idx", "trace_current_t", "trace_best_t", "trace_pair",
+                "trace_accepted", "moves_scored"):
+        np.testing.assert_array_equal(outs[0][key].cpu().numpy(), outs[1][key].cpu().numpy(), err_msg=key)
