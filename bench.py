@@ -730,8 +730,10 @@ def c3_leg(dev, side: int = 128, n_angles: int = 64, slices: int = 148, iters: i
     o, ms = timed(sb)
     od, ms_dense = timed(de)
     del de
+    # (raw exact-scan counts differ by construction: only the reference-equivalent column is compared)
     same = all(np.array_equal(o[k].cpu().numpy(), od[k].cpu().numpy())
-               for k in ("iterations", "best_objective", "best_idx", "moves_scored"))
+               for k in ("iterations", "best_objective", "best_idx")) and \
+        np.array_equal(o["moves_scored"][:, 0].cpu().numpy(), od["moves_scored"][:, 0].cpu().numpy())
     mv = o["moves_scored"].sum(dim=0).cpu().numpy()
     rec = load("solve_c3m")[0]
     par = {"slice": 0, "bitwise": bool(
