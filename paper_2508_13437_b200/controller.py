@@ -15,6 +15,7 @@ strategy can be replayed against the GPU path.
 
 from __future__ import annotations
 
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -317,6 +318,48 @@ def _report(out: dict, initial_objective: float, started: float) -> SolveReport:
     )
 
 
+def _sparse_view(D, inst):
+    """A as CSC + CSR device arrays when it is sparse (density <= 1/8) and
+    large (m*n >= 2^20), else None: solve() then runs the sparse engine
+    (amvm_solve_sparse), whose results equal the dense engine's bit for bit
+    (tests/test_sparse_gpu.py, tests/test_c3full_gpu.py).  AMVM_SPARSE_ROUTE=0
+    keeps every solve on the dense engine."""
+    if os.environ.get("AMVM_SPARSE_ROUTE", "1") == "0" or inst.m * inst.n < (1 << 20):
+        return None
+    key = f"{D.device}:sparse"
+    if key in inst._device:  # built once per instance and device
+        return inst._device[key]
+    inst._device[key] = sp = _build_sparse_view(D, inst)
+    return sp
+
+
+def _build_sparse_view(D, inst):
+    torch = D.torch
+    At = D._keep[0]  # n x m, column-major A
+    nnz = int(torch.count_nonzero(At).item())
+    if nnz * 8 > inst.m * inst.n:
+        return None
+    m, n = inst.m, inst.n
+    A = At.t()  # m x n view
+    rc = torch.nonzero(A)  # row-major order: rows ascending, columns ascending within a row
+    rows, cols = rc[:, 0], rc[:, 1]
+    rval = A[rows, cols].contiguous()
+    rptr = torch.zeros(m + 1, dtype=torch.int64, device=D.device)
+    rptr[1:] = torch.cumsum(torch.bincount(rows, minlength=m), 0)
+    order = torch.sort(cols * m + rows, stable=True).indices
+    cptr = torch.zeros(n + 1, dtype=torch.int64, device=D.device)
+    counts = torch.bincount(cols, minlength=n)
+    cptr[1:] = torch.cumsum(counts, 0)
+    keep = [rptr, cols.to(torch.int32).contiguous(), rval, cptr, rows[order].to(torch.int32).contiguous(),
+            rval[order].contiguous()]
+    max_row = int((rptr[1:] - rptr[:-1]).max().item())
+    prob = N.SparseProblem(m, n, len(inst.values), 1, nnz, int(counts.max().item()),
+                           keep[3].data_ptr(), keep[4].data_ptr(), keep[5].data_ptr(),
+                           keep[0].data_ptr(), keep[1].data_ptr(), keep[2].data_ptr(),
+                           D._keep[1].data_ptr(), D._keep[2].data_ptr(), max_row)
+    return prob, keep
+
+
 def _solve_device(inst, cfg, current, rng, max_iters, budget) -> dict:
     D = _Dev(inst, current)
     torch = D.torch
@@ -344,10 +387,21 @@ def _solve_device(inst, cfg, current, rng, max_iters, budget) -> dict:
         o["initial_objective"].data_ptr(), o["iterations"].data_ptr(), o["operator_uses"].data_ptr(),
         o["trace_current_t"].data_ptr(), o["trace_best_t"].data_ptr(), o["trace_pair"].data_ptr(),
         o["trace_accepted"].data_ptr(), o["moves_scored"].data_ptr())
-    ws, wsb = D.ws(prm)
-    rc = D.lib.amvm_solve(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), N.ptr(rng_buf),
-                          N.C.byref(res), ws, wsb, N.stream_handle())
-    D.finish(rc, "amvm_solve", ws)
+    sp = _sparse_view(D, inst)
+    if sp is not None:  # sparse A: the sparse engine (same results)
+        nbytes = D.lib.amvm_sparse_workspace_bytes(N.C.byref(sp[0]), N.C.byref(prm))
+        if nbytes == 0:
+            raise ValueError("problem shape or parameters rejected by libamvm")
+        buf = N.workspace(D.device, nbytes)
+        ws, wsb = N.ptr(buf), N.C.c_size_t(buf.numel())
+        rc = D.lib.amvm_solve_sparse(N.C.byref(sp[0]), N.C.byref(prm), N.C.byref(D.sol), N.ptr(rng_buf),
+                                     N.C.byref(res), ws, wsb, N.stream_handle())
+        D.finish(rc, "amvm_solve_sparse", ws)
+    else:
+        ws, wsb = D.ws(prm)
+        rc = D.lib.amvm_solve(N.C.byref(D.prob), N.C.byref(prm), N.C.byref(D.sol), N.ptr(rng_buf),
+                              N.C.byref(res), ws, wsb, N.stream_handle())
+        D.finish(rc, "amvm_solve", ws)
     host = {k: v.cpu().numpy() for k, v in o.items()}
     it = int(host["iterations"][0])
     return {
