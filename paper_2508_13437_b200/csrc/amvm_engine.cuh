@@ -402,6 +402,7 @@ struct Shared {
   int vrow[32];                   // best_swap: rows that recently proved a swap non-improving
   int vins;                       // ... insertion counter (ring of 32)
   int spl[NT / 32 * 4];           // sparse one_opt window: chosen level per column (-1: none)
+  int spc[NT / 32 * 4];           // ... and the window's columns
   double spt[NT / 32 * 4];        // ... and its objective
   int64_t pw_a[48], pw_b[48];     // pairwise-sum tree walk stacks (thread 0 only)
   int pw_s[48];
@@ -628,26 +629,78 @@ struct Engine {
   // the barrier that follows its last read.
   // one_opt on the sparse engine: every candidate scored exactly from its
   // column's nonzeros plus the largest |s| among untouched rows (the first
-  // row of the |s| top list outside the column), so no screens: a window of
-  // NW*kSpCW columns is scored by the warps in parallel, the lowest improving
-  // column is applied (the reference's sequential first improvement) and
-  // scanning resumes after it.
+  // row of the |s| top list outside the column).  Screen (exact): a column
+  // that does not touch the argmax row r* (|s_r*| = t) keeps |s_r*| = t in
+  // both shifted residuals, so it cannot improve -- only the columns of r*'s
+  // CSR row are scored, NW*kSpCW per window in ascending order, the lowest
+  // improving one is applied (the reference's sequential first improvement)
+  // and scanning resumes after it with the new r*.  The reference-equivalent
+  // move count still covers every column passed.
   static constexpr int kSpCW = 4;
+  // candidate moves of the columns [j0, j1): 2 per column minus the grid ends
+  __device__ int64_t sp_count_moves(int64_t j0, int64_t j1) {
+    AMVM_LOCALS
+    int64_t c = 0;
+    for (int64_t j = j0 + tid; j < j1; j += NT) {
+      const int k = cidx[j];
+      c += (k > 0) + (k + 1 < nlev);
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(AMVM_FULL, c, o);
+    __syncthreads();
+    if (lane == 0) sh->red2i[0][warp] = (int)c;
+    __syncthreads();
+    int64_t tot = 0;
+    for (int w = 0; w < NW; ++w) tot += sh->red2i[0][w];
+    __syncthreads();
+    return tot;
+  }
+
   __device__ void one_opt_sparse() {
     AMVM_LOCALS
     constexpr int WS = NW * kSpCW;
+    const int64_t *rp = sh->c.rptr;
+    const int32_t *rw = sh->c.rcol;
     for (int sw = 0; sw < prm->one_opt_max_sweeps; ++sw) {
       bool changed = false;
       int64_t p = 0;
       sp_select_top();
       while (p < n) {
         const double t = cobj;
+        // the window's columns: the next WS columns >= p of the argmax row (or
+        // of all columns if the top row is not at t)
+        if (tid == 0) {
+          const int32_t rs = sh->c.top[0];
+          int64_t e0 = -1, e1 = -1;
+          if (fabs(cr[rs]) == t) {
+            e1 = __ldg(rp + rs + 1);
+            int64_t lo = __ldg(rp + rs), hi = e1;
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              if (__ldg(rw + mid) < p) lo = mid + 1;
+              else hi = mid;
+            }
+            e0 = lo;
+          }
+          int w = 0;
+          if (e0 >= 0) {
+            for (; w < WS && e0 + w < e1; ++w) sh->spc[w] = __ldg(rw + e0 + w);
+            sh->bc_i[8] = e0 + w < e1;  // more screen-row columns after this window
+          } else {
+            for (; w < WS && p + w < n; ++w) sh->spc[w] = (int)(p + w);
+            sh->bc_i[8] = p + w < n;
+          }
+          sh->bc_i[9] = w;
+        }
+        __syncthreads();
+        const int wc = sh->bc_i[9];
+        const bool more = sh->bc_i[8] != 0;
 #pragma unroll 1
         for (int c = 0; c < kSpCW; ++c) {
-          const int64_t j = p + warp * kSpCW + c;
+          const int slotw = warp * kSpCW + c;
           int lvl = -1;
           double bt = t;
-          if (j < n) {
+          if (slotw < wc) {
+            const int64_t j = sh->spc[slotw];
             const int k = cidx[j];
             const bool hm = k > 0, hp = k + 1 < nlev;
             const double lk = lv[k];
@@ -668,27 +721,25 @@ struct Engine {
             if (hp && tp < bt) { bt = tp; lvl = k + 1; }
           }
           if (lane == 0) {
-            sh->spl[warp * kSpCW + c] = lvl;
-            sh->spt[warp * kSpCW + c] = bt;
+            sh->spl[slotw] = lvl;
+            sh->spt[slotw] = bt;
           }
         }
         __syncthreads();
-        const int wc = (int)(n - p < WS ? n - p : WS);
         int applied = -1;
         for (int w = 0; w < wc; ++w)
           if (sh->spl[w] >= 0) { applied = w; break; }
+        // every column passed up to the applied one (or through the window /
+        // to the end when nothing improves) counts as scored
+        const int64_t end = applied >= 0 ? (int64_t)sh->spc[applied] + 1
+                                         : (more ? (int64_t)sh->spc[wc - 1] + 1 : n);
+        const int64_t cnt = sp_count_moves(p, end);
         if (tid == 0) {
-          int64_t cnt = 0;
-          const int last = applied >= 0 ? applied : wc - 1;
-          for (int w = 0; w <= last; ++w) {
-            const int k = cidx[p + w];
-            cnt += (k > 0) + (k + 1 < nlev);
-          }
           sh->c.mv_ref += cnt;
           sh->c.mv_raw += cnt;
         }
         if (applied >= 0) {
-          const int64_t j = p + applied;
+          const int64_t j = sh->spc[applied];
           const int lvl = sh->spl[applied];
           const double bt = sh->spt[applied];
           const double d = dsub(lv[lvl], lv[cidx[j]]);
@@ -703,11 +754,10 @@ struct Engine {
           bump_known(bt);
           sp_select_top();  // the residual changed
           changed = true;
-          p = j + 1;
         } else {
           __syncthreads();
-          p += wc;
         }
+        p = end;
       }
       if (!changed) break;
     }

@@ -1,5 +1,5 @@
 #!/bin/bash
-# column-indexed sparse filter + overflow path
+# sparse one_opt: argmax-row column screen
 OUT=${OUT:-r5j}; mkdir -p gpurun_out/$OUT
 timeout 900 python -m pytest tests/test_sparse_gpu.py tests/test_c3full_gpu.py -x -q > gpurun_out/$OUT/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/$OUT/pytest.log
 tail -3 gpurun_out/$OUT/pytest.log
