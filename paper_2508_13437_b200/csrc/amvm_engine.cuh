@@ -1824,11 +1824,14 @@ struct Engine {
     __syncthreads();
     const int64_t r0 = rows[0], z0 = __ldg(rp + r0), z1 = __ldg(rp + r0 + 1);
     const int64_t s0 = z1 - z0, nch = (n + 31) / 32;
-    for (int64_t it = warp; it < s0 * nch; it += NW) {
-      const int64_t k = it / nch;
+    // one warp per row-0 nonzero c; skipped whole when c cannot pair (b0_c = 0,
+    // or no level on the needed side of c's)
+    for (int64_t k = warp; k < s0; k += NW)
+    for (int64_t ch = 0; ch < nch; ++ch) {
       const int32_t c = __ldg(rw + z0 + k);
       const double bc = rt[c];
-      const int64_t x = (it - k * nch) * 32 + lane;
+      if (bc == 0.0 || (bc > 0.0 ? cidx[c] == 0 : cidx[c] == nlev - 1)) break;
+      const int64_t x = ch * 32 + lane;
       // bc > 0: (i, j) = (c, x) with b0_x < bc;  bc < 0: (i, j) = (x, c) with bc < b0_x <= 0
       bool alive = false;
       int32_t i = 0, j = 0;
@@ -2969,38 +2972,41 @@ struct Engine {
         }
         break;
       }
-      // p = d / total, also into the (idle) phase scratch when it fits, so
-      // the sequential cumsum below reads shared memory
-      double *const ps = (size_t)n * 8 <= scratch_bytes<NT>(nlev, tab) ? (double *)scr : pbuf;
-      for (int64_t k = tid; k < n; k += NT) {
-        const double v = ddiv(dbuf[k], total);
-        pbuf[k] = v;
-        ps[k] = v;
-      }
-      __syncthreads();
-      if (warp == 0) {
-        // Generator.choice(n, p): cdf = cumsum(p); cdf /= cdf[-1];
-        // searchsorted(cdf, random(), 'right').  The cumsum is numpy's
-        // sequential chain: lane 0 runs it as a bare DADD chain (the loads
-        // are independent of it and run ahead), keeping the value before
-        // each 32-element chunk so the search rescans one chunk instead of
-        // storing the whole cdf.
-        const int64_t nch = (n + 31) / 32;
+      // p = d / total; numpy's sequential cumsum is a bare DADD chain on
+      // thread 0 over shared memory, fed in chunks of the (idle) phase
+      // scratch by the whole block, keeping the value before each
+      // 32-element block of the cdf so the search rescans one block
+      for (int64_t k = tid; k < n; k += NT) pbuf[k] = ddiv(dbuf[k], total);
+      {
+        double *const ps = (double *)scr;
+        const int64_t cs = (int64_t)(scratch_bytes<NT>(nlev, tab) / 8) & ~(int64_t)31;
         double acc = 0.0;
-        if (lane == 0) {
-          for (int64_t c = 0; c < nch; ++c) {
-            cbk[c] = acc;
-            const double *pc = ps + c * 32;
-            if (n - c * 32 >= 32) {
+        for (int64_t base = 0; base < n; base += cs) {
+          const int64_t len = n - base < cs ? n - base : cs;
+          __syncthreads();  // pbuf written / the previous chunk consumed
+          for (int64_t k = tid; k < len; k += NT) ps[k] = pbuf[base + k];
+          __syncthreads();
+          if (tid == 0) {
+            for (int64_t c0 = 0; c0 < len; c0 += 32) {
+              cbk[(base + c0) >> 5] = acc;
+              const double *pc = ps + c0;
+              if (len - c0 >= 32) {
 #pragma unroll
-              for (int l = 0; l < 32; ++l) acc = dadd(acc, pc[l]);
-            } else {
-              for (int l = 0; l < (int)(n - c * 32); ++l) acc = dadd(acc, pc[l]);
+                for (int l = 0; l < 32; ++l) acc = dadd(acc, pc[l]);
+              } else {
+                for (int l = 0; l < (int)(len - c0); ++l) acc = dadd(acc, pc[l]);
+              }
             }
           }
         }
-        __syncwarp();
-        const double last = __shfl_sync(AMVM_FULL, acc, 0);  // cdf[n-1]
+        if (tid == 0) sh->bc_d[3] = acc;
+        __syncthreads();
+      }
+      if (warp == 0) {
+        // Generator.choice(n, p): cdf = cumsum(p); cdf /= cdf[-1];
+        // searchsorted(cdf, random(), 'right')
+        const int64_t nch = (n + 31) / 32;
+        const double last = sh->bc_d[3];  // cdf[n-1]
         double u = 0.0;
         if (lane == 0) u = pcg_random(sh->rng);
         u = __shfl_sync(AMVM_FULL, u, 0);
