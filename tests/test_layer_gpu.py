@@ -48,3 +48,30 @@ def test_layer_rows_match_reference(name):
         np.testing.assert_array_equal(tr["trace_best_t"][k, :it], rec["trace_best_t"])
         np.testing.assert_array_equal(tr["trace_pair"][k, :it], rec["trace_pair"])
         np.testing.assert_array_equal(tr["trace_accepted"][k, :it], rec["trace_accepted"])
+
+
+def test_c5_random_rows_full_depth_match_oracle():
+    """64 fixed random rows of the C5 layer at the full 100 iterations (the
+    bench's CPU baseline sample, tools/cpu_full_depth.py) against the CPU
+    oracle's run of the same rows: every trace, code and objective bitwise."""
+    import os
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a visible CUDA device")
+    from paper_2508_13437_b200 import SolverConfig, ptq
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "c5_fulldepth64.npz")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c5_fulldepth64.npz not generated (tools/cpu_full_depth.py)")
+    g = np.load(path)
+    rows = g["rows"]
+    X, W = recipes.ptq_layer(4096, 14336)
+    rep = ptq.solve_layer(X, W, bits=4, cfg=SolverConfig(max_iters=100), rows=rows, trace=True)
+    tr = rep.seconds["trace"]
+    np.testing.assert_array_equal(rep.iterations, g["iterations"])
+    np.testing.assert_array_equal(rep.objective, g["best_objective"])
+    np.testing.assert_array_equal(rep.codes.astype(np.int8), g["best_idx"])
+    for f in ("trace_current_t", "trace_best_t", "trace_pair", "trace_accepted"):
+        np.testing.assert_array_equal(tr[f][:, :100], g[f][:, :100], err_msg=f)
