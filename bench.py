@@ -604,6 +604,17 @@ def run_amvm(args, rank, world):
     if world == 1:
         cpu.pop("_out")
         line["cpu_baseline"] = {k: v for k, v in cpu.items() if k not in ("seconds", "moves")}
+        fd = os.path.join(ROOT, "profiles", "r02_cpu_full_depth.json")
+        if os.path.exists(fd):  # BASELINE.md §3 plan: 64 random rows at full depth (run once, dev container)
+            f = json.load(open(fd))
+            line["cpu_baseline"]["full_depth_sample"] = {
+                "rows": len(f["rows"]), "iterations": f["iterations"], "cores": f["threads"],
+                "mean_row_seconds_per_core": round(f["mean_row_seconds_per_core"], 2),
+                "extrapolated_full_layer_s_16_cores": round(f["extrapolated_full_layer_s_on_16_cores"]),
+                "moves_per_s": f["moves_per_s"], "kind": "port",
+                "note": "tools/cpu_full_depth.py on the dev container (not this box); T_cpu = mean row time x "
+                        "14336 / cores, extrapolated; the GPU matches these 64 rows bitwise "
+                        "(tests/test_layer_gpu.py)"}
         if not args.no_ttr:
             line["time_to_reference_linf"] = time_to_reference()
         sc = scorer_roofline(X, dev, flush)
