@@ -1433,6 +1433,22 @@ struct Engine {
     // j-buckets are walked through the skip list of non-empty levels.
     const int32_t *nxt = lst + (nlev + 1);
     const int64_t ngrp = (n + 31) / 32 + nlev;
+    // few groups (small buckets: C1 has 15 for 16 warps): each group's lower
+    // levels are split round-robin into P parts claimed separately, so the
+    // warps share the long groups instead of waiting for them
+    // (the wide CTA only: single instances; the batch engine keeps the plain loop)
+    constexpr bool kParts = NT >= 512;
+    if (kParts && warp == 0) {
+      int64_t G = 0;
+      for (int64_t k = lane; k < nlev; k += 32) G += (lst[k + 1] - lst[k] + 31) >> 5;
+      for (int o = 16; o; o >>= 1) G += __shfl_xor_sync(AMVM_FULL, G, o);
+      if (lane == 0) {
+        int64_t P = G > 0 ? (4 * NW) / G : 1;
+        sh->bc_i[10] = (int)(P < 1 ? 1 : P > 8 ? 8 : P);
+      }
+    }
+    if (kParts) __syncthreads();
+    const int P = kParts ? sh->bc_i[10] : 1;
     for (int64_t p0 = 0; p0 < n; p0 += kTJ) {
       const int64_t p1 = n - p0 < kTJ ? n : p0 + kTJ;
       for (int64_t e = tid; e < p1 - p0; e += NT) {
@@ -1451,9 +1467,11 @@ struct Engine {
       int ki = (int)nlev - 1;
       int64_t gbase = 0;  // first group id of bucket ki (groups are claimed in increasing order)
       for (;;) {
-        int64_t grp = 0;
-        if (lane == 0) grp = atomicAdd(&sh->gnext, 1);
-        grp = __shfl_sync(AMVM_FULL, grp, 0);
+        int64_t item = 0;
+        if (lane == 0) item = atomicAdd(&sh->gnext, 1);
+        item = __shfl_sync(AMVM_FULL, item, 0);
+        const int64_t grp = P == 1 ? item : item / P;
+        const int part = P == 1 ? 0 : (int)(item - grp * P);
         if (grp >= ngrp) break;
         while (ki >= 0 && grp >= gbase + ((lst[ki + 1] - lst[ki] + 31) >> 5)) {
           gbase += (lst[ki + 1] - lst[ki] + 31) >> 5;
@@ -1468,7 +1486,9 @@ struct Engine {
 #pragma unroll
         for (int q = 0; q < kG; ++q) bi[q] = (have && q < g) ? ag[(int64_t)q * n + ip] : 0.0;
         const double xi = lv[ki];
+        int rk = -1;
         for (int kj = nxt[nlev]; kj < ki; kj = nxt[kj]) {
+          if (P > 1 && ++rk % P != part) continue;
           const int64_t s0 = (int64_t)lst[kj] > p0 ? (int64_t)lst[kj] : p0;
           const int64_t s1 = (int64_t)lst[kj + 1] < p1 ? (int64_t)lst[kj + 1] : p1;
           if (s0 >= s1) continue;
