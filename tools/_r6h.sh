@@ -1,5 +1,5 @@
 #!/bin/bash
-# fc_pass: groups split into parts when few
+# select_screen: warp sorts + merge
 OUT=${OUT:-r6h}; mkdir -p gpurun_out/$OUT
 timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/$OUT/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/$OUT/pytest.log
 tail -2 gpurun_out/$OUT/pytest.log
