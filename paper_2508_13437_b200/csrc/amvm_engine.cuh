@@ -57,6 +57,9 @@ constexpr int kDrainLong = 1024;  // queue length that keeps the batched passes 
 // row-0 prefix) when the mean non-empty level bucket holds fewer than this
 // many variables (0: never): the i-groups would leave most lanes idle
 constexpr int kFcPairs = AMVM_FC_PAIRS;
+#ifndef AMVM_FC_PARTS_MUL
+#define AMVM_FC_PARTS_MUL 2  // wide CTA: pair-loop work items per warp (C1 A/B: 2 -> 98.8, 4 -> 101.9, 8 -> 107.7 us/it)
+#endif
 constexpr int kDrainShort = AMVM_DRAIN_SHORT;  // at or below: no row passes, warp-per-pair checks
 constexpr int kRowPasses = AMVM_ROW_PASSES;  // queue passes (one filter row each) before fc_rest
 constexpr int kMaxDeltaClasses = 4096;  // overflow path: distinct level differences
@@ -1443,7 +1446,7 @@ struct Engine {
       for (int64_t k = lane; k < nlev; k += 32) G += (lst[k + 1] - lst[k] + 31) >> 5;
       for (int o = 16; o; o >>= 1) G += __shfl_xor_sync(AMVM_FULL, G, o);
       if (lane == 0) {
-        int64_t P = G > 0 ? (4 * NW) / G : 1;
+        int64_t P = G > 0 ? (AMVM_FC_PARTS_MUL * NW) / G : 1;
         sh->bc_i[10] = (int)(P < 1 ? 1 : P > 8 ? 8 : P);
       }
     }
