@@ -585,8 +585,9 @@ struct Engine {
     __syncthreads();
   }
 
-  // Screening rows for one_opt: each thread's largest |s|, then the kS largest
-  // of those (a block bitonic sort of NT keys).  ANY row subset gives an exact
+  // Screening rows for one_opt: each thread's largest |s|, then the kS/NW
+  // largest of each warp's (register sorts, no block-wide sort), the overall
+  // largest first.  ANY row subset gives an exact
   // rejection test; large |s| rows reject almost every non-improving shift.
   // one_opt reads the screening rows straight from the row-major copy Ar.
   __device__ void select_screen() {
@@ -597,24 +598,43 @@ struct Engine {
       const uint64_t key = abs_key(cr[i]);
       if (key > best || i == tid) { best = key; brow = (int)i; }
     }
-    sh->skey[tid] = tid < m ? best : 0;
-    sh->sidx[tid] = tid < m ? brow : 0;
-    __syncthreads();
-    for (int k = 2; k <= NT; k <<= 1) {
+    // each warp sorts its 32 maxima in registers; the screening rows are the
+    // top kS/NW of every warp (no block-wide sort), with the overall largest
+    // moved to srow[0] (it follows the objective)
+    uint64_t key = tid < m ? best : 0;
+    int row = tid < m ? brow : 0;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
       for (int jj = k >> 1; jj > 0; jj >>= 1) {
-        const int x = tid ^ jj;
-        if (x > tid) {
-          const uint64_t ka = sh->skey[tid], kb = sh->skey[x];
-          const bool desc = (tid & k) == 0;
-          if (desc ? ka < kb : ka > kb) {
-            sh->skey[tid] = kb; sh->skey[x] = ka;
-            const int t0 = sh->sidx[tid]; sh->sidx[tid] = sh->sidx[x]; sh->sidx[x] = t0;
-          }
-        }
-        __syncthreads();
+        const uint64_t ok = __shfl_xor_sync(AMVM_FULL, key, jj);
+        const int orow = __shfl_xor_sync(AMVM_FULL, row, jj);
+        const bool lower = (lane & jj) == 0, desc = (lane & k) == 0;
+        if ((lower == desc) ? ok > key : ok < key) { key = ok; row = orow; }
       }
     }
-    if (tid < kS) sh->srow[tid] = sh->sidx[tid < m ? tid : 0];
+    sh->skey[tid] = key;
+    sh->sidx[tid] = row;  // (each thread's second-screen row: any permutation of the maxima)
+    __syncthreads();
+    if (warp == 0) {
+      constexpr int per = kS / NW;  // rows taken from each warp's sorted list
+      static_assert(kS % NW == 0 && per >= 1, "screening rows split evenly over the warps");
+      int r = sh->sidx[(lane / per) * 32 + lane % per];
+      // the overall largest: the best warp head
+      uint64_t hk = lane < NW ? sh->skey[lane * 32] : 0;
+      int hw = lane < NW ? lane : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(AMVM_FULL, hk, o);
+        const int w2 = __shfl_xor_sync(AMVM_FULL, hw, o);
+        if (k2 > hk || (k2 == hk && w2 < hw)) { hk = k2; hw = w2; }
+      }
+      // swap slots 0 and hw * per (both hold warp heads)
+      const int r0 = __shfl_sync(AMVM_FULL, r, 0), rh = __shfl_sync(AMVM_FULL, r, hw * per);
+      if (lane == 0) r = rh;
+      else if (lane == hw * per) r = r0;
+      sh->srow[lane] = r;
+    }
     __syncthreads();
   }
 
