@@ -162,3 +162,28 @@ def test_column_indexed_filter_overflow_path(tomo, monkeypatch, side, n_angles):
     for key in ("iterations", "best_objective", "best_idx", "trace_current_t", "trace_best_t", "trace_pair",
                 "trace_accepted", "moves_scored"):
         np.testing.assert_array_equal(outs[0][key].cpu().numpy(), outs[1][key].cpu().numpy(), err_msg=key)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_solve_routes_general_sparse_A_bitwise(tomo, monkeypatch, seed):
+    """solve() on a general sparse A (mixed signs, explicit structure unlike a
+    projector, 1.6M entries at ~2 % density) runs the sparse engine; its
+    report equals the dense engine's (AMVM_SPARSE_ROUTE=0) bit for bit."""
+    import paper_2508_13437_b200 as P
+
+    rng = np.random.default_rng(100 + seed)
+    m, n = 1536, 1024
+    A = np.where(rng.random((m, n)) < 0.02, rng.standard_normal((m, n)), 0.0)
+    x = rng.integers(0, 5, n).astype(float) - 2.0
+    b = A @ x + rng.uniform(-0.5, 0.5, m)
+    inst = P.Instance(A, b, P.ValueSet(np.array([-2.0, -1.0, 0.0, 1.0, 2.0])))
+    cfg = P.SolverConfig(max_iters=25, seed=seed, destroy_rate=0.02)
+    reps = []
+    for route in ("1", "0"):
+        monkeypatch.setenv("AMVM_SPARSE_ROUTE", route)
+        reps.append(P.solve(P.Instance(A, b, inst.values), cfg))
+    sp, de = reps
+    assert sp.best.objective == de.best.objective
+    np.testing.assert_array_equal(sp.best.idx, de.best.idx)
+    assert [(e.current_t, e.best_t, e.op_pair, e.accepted) for e in sp.trace] == \
+        [(e.current_t, e.best_t, e.op_pair, e.accepted) for e in de.trace]
