@@ -133,3 +133,36 @@ def test_api_validation_matches_reference():
     np.testing.assert_array_equal(bank.probabilities(), [0.25] * 4)
     with pytest.raises(KeyError):
         P.update_weights(bank, 0, "bogus")
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """Every struct the Python side hands to libamvm has the C header's size
+    and field offsets (gcc on include/amvm.h): the ABI cannot drift silently."""
+    import ctypes as C
+    import shutil
+    import subprocess
+
+    from paper_2508_13437_b200 import _native as N
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    pairs = {"amvm_problem": N.Problem, "amvm_sparse_problem": N.SparseProblem, "amvm_params": N.Params,
+             "amvm_pcg64": N.PCG64State, "amvm_bank": N.Bank, "amvm_solution": N.SolutionPtrs,
+             "amvm_result": N.ResultPtrs}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "amvm.h"', "int main(void) {"]
+    for cname, py in pairs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in pairs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, f"{cname}.{fname}"
